@@ -1,0 +1,1069 @@
+// B200 engine: GPU-resident workers, device-built neighbour table, fused
+// collide+stream kernels, edge-then-inner overlap with the halo exchange
+// (peer copies in-process, NCCL send/recv across processes).
+//
+// Reference: splb::Simulation (proj/include/splb/engine.hpp:121-650),
+// build_streaming_map (layout.hpp:181-286), build_exchange_plan
+// (exchange.hpp:36-83).
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <map>
+#include <thread>
+
+#include <cub/device/device_radix_sort.cuh>
+
+#include "engine.hpp"
+#include "kernels.cuh"
+
+namespace splbcu {
+
+#define CK(x)                                                                                \
+    do {                                                                                     \
+        cudaError_t e_ = (x);                                                                \
+        if (e_ != cudaSuccess)                                                               \
+            fail(ErrKind::Cuda, std::string("CUDA error: ") + cudaGetErrorString(e_) + " (" + \
+                                    #x + ")");                                               \
+    } while (0)
+
+#define NK(x)                                                                                   \
+    do {                                                                                        \
+        ncclResult_t r_ = (x);                                                                  \
+        if (r_ != ncclSuccess)                                                                  \
+            fail(ErrKind::Comm, std::string("exchange failure: NCCL error: ") + ncclGetErrorString(r_)); \
+    } while (0)
+
+std::string nccl_unique_id(void* out128) {
+    ncclUniqueId id;
+    NK(ncclGetUniqueId(&id));
+    std::memcpy(out128, &id, sizeof(id));
+    return {};
+}
+
+namespace {
+
+struct DevMem {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DevMem() = default;
+    DevMem(const DevMem&) = delete;
+    DevMem& operator=(const DevMem&) = delete;
+    ~DevMem() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    template <class T>
+    T* alloc(size_t n) {
+        release();
+        bytes = std::max<size_t>(n * sizeof(T), 16);
+        CK(cudaMalloc(&p, bytes));
+        return static_cast<T*>(p);
+    }
+    template <class T>
+    T* get() const { return static_cast<T*>(p); }
+};
+
+template <class T>
+T* upload(DevMem& m, const std::vector<T>& v, cudaStream_t s) {
+    T* d = m.alloc<T>(v.size());
+    if (!v.empty()) CK(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+    return d;
+}
+
+inline unsigned blocks_for(uint64_t n, unsigned tpb = 256) { return unsigned((n + tpb - 1) / tpb); }
+
+// ---- device lookup over the worker's own + halo sites ----------------------
+struct DLookup {
+    const uint64_t* keys;
+    const int32_t* owner;
+    const uint32_t* local;   // internal index when owner == this worker
+    const uint32_t* global;  // global site index
+    uint64_t n;
+    const uint64_t* row_off;  // null: whole-array binary search
+    int32_t lo1, hi1, lo2, hi2;
+    int64_t ny;
+};
+
+__device__ __forceinline__ uint64_t d_zyx_key(int32_t x, int32_t y, int32_t z) {
+    const int64_t b = int64_t(1) << 20;
+    return (uint64_t(int64_t(z) + b) << 42) | (uint64_t(int64_t(y) + b) << 21) | uint64_t(int64_t(x) + b);
+}
+
+__device__ int64_t d_find(const DLookup& L, int32_t x, int32_t y, int32_t z) {
+    const uint64_t key = d_zyx_key(x, y, z);
+    uint64_t b = 0, e = L.n;
+    if (L.row_off) {
+        if (y < L.lo1 || y > L.hi1 || z < L.lo2 || z > L.hi2) return -1;
+        const uint64_t r = uint64_t(int64_t(z - L.lo2) * L.ny + (y - L.lo1));
+        b = L.row_off[r];
+        e = L.row_off[r + 1];
+    }
+    while (b < e) {
+        const uint64_t m = (b + e) >> 1;
+        if (L.keys[m] < key) b = m + 1;
+        else e = m;
+    }
+    return (b < L.n && L.keys[b] == key) ? int64_t(b) : -1;
+}
+
+// Neighbour table build (build_streaming_map, layout.hpp:181-286), one
+// thread per (site, direction).  Cross-worker links are collected with the
+// reference's canonical sort key (neighbour, sender global site, direction)
+// and slotted after a device radix sort.
+__global__ void build_links(uint32_t n, uint64_t P, const int32_t* __restrict__ coords,
+                            const uint8_t* __restrict__ kind, const uint32_t* __restrict__ gidx,
+                            int32_t w, DLookup L, uint32_t* __restrict__ tab,
+                            unsigned long long* out_keys, unsigned long long* out_vals, unsigned* n_out,
+                            unsigned long long* in_keys, unsigned long long* in_vals, unsigned* n_in,
+                            unsigned* err) {
+    const uint64_t idx = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= uint64_t(n) * 18) return;
+    const uint32_t s = uint32_t(idx / 18);
+    const int i = int(idx % 18) + 1;
+    const int32_t x = coords[3 * uint64_t(s)], y = coords[3 * uint64_t(s) + 1], z = coords[3 * uint64_t(s) + 2];
+    const uint8_t k = kind[18 * uint64_t(s) + uint64_t(i - 1)];
+    const uint64_t tpos = uint64_t(i - 1) * P + s;
+    if (k == 0) {
+        const int64_t e = d_find(L, x + cx(i), y + cy(i), z + cz(i));
+        if (e < 0) {
+            atomicExch(err, 1u);
+            return;
+        }
+        const int32_t o = L.owner[e];
+        if (o == w) {
+            tab[tpos] = L.local[e];
+        } else {
+            const unsigned p = atomicAdd(n_out, 1u);
+            out_keys[p] = (static_cast<unsigned long long>(o) << 40) |
+                          (static_cast<unsigned long long>(gidx[s]) * 18ull + unsigned(i - 1));
+            out_vals[p] = tpos;
+            tab[tpos] = kSpecial | (kOpShared << kOpShift);
+        }
+        // incoming partner: the site at x - c_i streams into (s, i)
+        const int64_t src = d_find(L, x - cx(i), y - cy(i), z - cz(i));
+        if (src >= 0 && L.owner[src] != w) {
+            const unsigned p = atomicAdd(n_in, 1u);
+            in_keys[p] = (static_cast<unsigned long long>(L.owner[src]) << 40) |
+                         (static_cast<unsigned long long>(L.global[src]) * 18ull + unsigned(i - 1));
+            in_vals[p] = uint64_t(i) * P + s;
+        }
+    } else if (k == 1) {
+        tab[tpos] = kSpecial | (kOpBounce << kOpShift);
+    } else {
+        tab[tpos] = kSpecial | (kOpIolet << kOpShift);  // id patched below
+    }
+}
+
+__global__ void patch_iolets(const uint64_t* __restrict__ pos, const uint16_t* __restrict__ id, uint32_t n,
+                             uint32_t* __restrict__ tab) {
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n) tab[pos[k]] = kSpecial | (kOpIolet << kOpShift) | id[k];
+}
+
+__global__ void assign_slots(const unsigned long long* __restrict__ out_vals, const unsigned long long* __restrict__ in_vals,
+                             uint32_t n, uint32_t* __restrict__ tab, uint64_t* __restrict__ recv_flat,
+                             uint64_t* __restrict__ send_pos) {
+    const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    tab[out_vals[r]] = kSpecial | (kOpShared << kOpShift) | r;
+    send_pos[r] = out_vals[r];
+    recv_flat[r] = in_vals[r];
+}
+
+struct Seg {
+    int nb;
+    uint32_t base, count;
+};
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+struct WorkerDev {
+    int w = 0, dev = 0;
+    cudaStream_t sE = nullptr, sM = nullptr;
+    cudaEvent_t evSend = nullptr, evMid = nullptr, evEnd = nullptr;
+    uint32_t n = 0, n_edge = 0, ep = 0, mp = 0;  // ranges: [0,ep) [ep,n_edge) [n_edge,n_edge+mp) [.., n)
+    uint64_t P = 0;
+    uint32_t shared = 0;
+    std::vector<uint32_t> ref_of_int, int_of_ref, global_of_int;
+    DevMem fbuf[2];
+    int old = 0;
+    DevMem tab, recv_flat, send_pos, io_coords, io_geo, staged, cap4, obs_site, obs_iolet, obs_buf;
+    std::vector<Seg> segs;
+    // observation: per iolet k, the internal sites in ascending global order
+    std::vector<std::vector<uint32_t>> obs_sites;
+    std::vector<uint32_t> obs_off;  // flattened offsets per iolet
+    uint32_t n_obs = 0;
+    uint64_t obs_row_base = 0, obs_rows = 0;
+    // kernel timing
+    std::vector<cudaEvent_t> tev;
+    size_t tev_used = 0;
+
+    double* f_old() const { return fbuf[old].get<double>(); }
+    double* f_new() const { return fbuf[1 - old].get<double>(); }
+    uint64_t fsize() const { return uint64_t(kQ) * P + shared; }
+};
+
+class Engine {
+  public:
+    Domain dom;
+    std::vector<BCEntry> bcs;
+    Params prm;
+    double omega = 0.0;
+    Partition part;
+    std::vector<std::unique_ptr<WorkerDev>> W;  // index = worker id; null if not local
+    bool dist = false;
+    int rank = 0, nranks = 1;
+    ncclComm_t comm = nullptr;
+    std::vector<Capture> caps;
+    Series series;
+    std::vector<std::vector<std::pair<int, uint32_t>>> obs_order;  // per iolet: (worker, pos)
+    uint64_t steps_run = 0;
+    double loop_s = 0.0, dev_loop_s = 0.0, plain_s = 0.0;
+    uint64_t plain_launches = 0, plain_sites = 0;
+    bool kernel_timing = false;
+    std::vector<IoletDev> io_host;
+
+    Engine(const Domain& d, std::vector<BCEntry> b, Params p, int rank_, int nranks_, const void* nccl_id)
+        : dom(d), bcs(std::move(b)), prm(std::move(p)) {
+        dist = nccl_id != nullptr;
+        rank = rank_;
+        nranks = nranks_;
+        validate_setup();
+        omega = 1.0 / prm.tau;  // RelaxationParams (lattice.hpp:83-84), dt = 1
+        part = splbcu::partition(dom, prm.workers);
+        if (dist && nranks != prm.workers) config_error("engine: dist mode needs workers == nranks");
+        if (prm.devices.empty()) {
+            int cur = 0;
+            CK(cudaGetDevice(&cur));
+            prm.devices.push_back(cur);
+        }
+        for (auto& g : dom.iolets) {
+            IoletDev x{};
+            for (int a = 0; a < 3; ++a) x.center[a] = g.center[a], x.normal[a] = g.normal[a];
+            x.radius = g.radius;
+            io_host.push_back(x);
+        }
+        for (size_t k = 0; k < bcs.size(); ++k) io_host[k].is_velocity = bcs[k].kind == 1;
+
+        const SiteIndex ix = index_domain(dom);
+        W.resize(size_t(prm.workers));
+        for (int w = 0; w < prm.workers; ++w) {
+            if (dist && w != rank) continue;
+            const int dev = dist ? prm.devices[0] : prm.devices[size_t(w) % prm.devices.size()];
+            W[size_t(w)] = std::make_unique<WorkerDev>();
+            setup_worker(*W[size_t(w)], w, dev, ix);
+        }
+        if (!dist) {
+            // exchange plan cross-check (exchange.hpp:43-83): both endpoints agree
+            for (int w = 0; w < prm.workers; ++w)
+                for (const Seg& sg : W[size_t(w)]->segs) {
+                    const Seg* peer = find_seg(*W[size_t(sg.nb)], w);
+                    if (!peer || peer->count != sg.count)
+                        runtime_error("build_exchange_plan: endpoints disagree on link count for pair " +
+                                      std::to_string(w) + " <-> " + std::to_string(sg.nb));
+                }
+            enable_peers();
+        } else {
+            WorkerDev& wk = *W[size_t(rank)];
+            CK(cudaSetDevice(wk.dev));
+            ncclUniqueId id;
+            std::memcpy(&id, nccl_id, sizeof(id));
+            NK(ncclCommInitRank(&comm, nranks, id, rank));
+        }
+        if (prm.observe_iolets) init_observation();
+        for (auto& wp : W)
+            if (wp) CK(cudaStreamSynchronize(wp->sM));
+    }
+
+    ~Engine() {
+        if (comm) ncclCommDestroy(comm);
+        for (auto& wp : W) {
+            if (!wp) continue;
+            cudaSetDevice(wp->dev);
+            for (auto e : wp->tev) cudaEventDestroy(e);
+            if (wp->evSend) cudaEventDestroy(wp->evSend);
+            if (wp->evMid) cudaEventDestroy(wp->evMid);
+            if (wp->evEnd) cudaEventDestroy(wp->evEnd);
+            if (wp->sE) cudaStreamDestroy(wp->sE);
+            if (wp->sM) cudaStreamDestroy(wp->sM);
+        }
+    }
+
+    static const Seg* find_seg(const WorkerDev& wk, int nb) {
+        for (const Seg& s : wk.segs)
+            if (s.nb == nb) return &s;
+        return nullptr;
+    }
+
+    // validate_setup (engine.hpp:223-241)
+    void validate_setup() {
+        validate_domain(dom);
+        if (prm.workers < 1) config_error("engine: workers must be >= 1");
+        if (bcs.size() != dom.iolets.size())
+            config_error("engine: boundary conditions configured for " + std::to_string(bcs.size()) +
+                         " iolets but the geometry declares " + std::to_string(dom.iolets.size()));
+        for (size_t k = 0; k < bcs.size(); ++k) {
+            bcs[k].table.validate();
+            if (bcs[k].kind == 0)  // PressureBC::validate (boundary.hpp:86-92)
+                for (double vn : bcs[k].table.v)
+                    if (!(vn / kCs2 > 0.0))
+                        config_error("pressure BC: ghost density must stay positive (table value " +
+                                     std::to_string(vn) + ")");
+        }
+        if (!(prm.tau > 0.5)) config_error("engine: tau must exceed 0.5");
+    }
+
+    void enable_peers() {
+        std::vector<int> devs(prm.devices);
+        std::sort(devs.begin(), devs.end());
+        devs.erase(std::unique(devs.begin(), devs.end()), devs.end());
+        for (int a : devs)
+            for (int b : devs) {
+                if (a == b) continue;
+                int can = 0;
+                CK(cudaDeviceCanAccessPeer(&can, a, b));
+                if (!can) continue;
+                CK(cudaSetDevice(a));
+                cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+                if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+                else CK(e);
+            }
+    }
+
+    void setup_worker(WorkerDev& wk, int w, int dev, const SiteIndex& ix) {
+        wk.w = w;
+        wk.dev = dev;
+        CK(cudaSetDevice(dev));
+        int lo_pri = 0, hi_pri = 0;
+        CK(cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri));
+        CK(cudaStreamCreateWithPriority(&wk.sE, cudaStreamNonBlocking, hi_pri));
+        CK(cudaStreamCreateWithPriority(&wk.sM, cudaStreamNonBlocking, lo_pri));
+        CK(cudaEventCreateWithFlags(&wk.evSend, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&wk.evMid, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&wk.evEnd, cudaEventDisableTiming));
+        cudaStream_t s = wk.sM;
+
+        const WorkerPart& wp = part.parts[size_t(w)];
+        wk.n = uint32_t(wp.sites.size());
+        wk.n_edge = wp.n_edge;
+        if (wk.n >= (1u << 29)) runtime_error("engine: worker holds too many sites for a u32 table");
+        wk.P = (uint64_t(wk.n) + 63) / 64 * 64;
+        if (wk.P == 0) wk.P = 64;
+
+        // Internal order: per group, plain sites (types 0,1) merged in zyx
+        // order, then iolet sites (types 2..5) in reference order.
+        auto key_of = [&](uint32_t g) {
+            return zyx_key(dom.coords[3 * uint64_t(g)], dom.coords[3 * uint64_t(g) + 1], dom.coords[3 * uint64_t(g) + 2]);
+        };
+        wk.ref_of_int.clear();
+        wk.ref_of_int.reserve(wk.n);
+        auto add_group = [&](const uint64_t ranges[6][2]) -> uint32_t {
+            // plain: merge type-0 and type-1 runs by key
+            uint64_t a = ranges[0][0], ae = ranges[0][1], b = ranges[1][0], be = ranges[1][1];
+            while (a < ae || b < be) {
+                if (b >= be || (a < ae && key_of(wp.sites[a]) < key_of(wp.sites[b])))
+                    wk.ref_of_int.push_back(uint32_t(a++));
+                else
+                    wk.ref_of_int.push_back(uint32_t(b++));
+            }
+            const uint32_t plain = uint32_t((ae - ranges[0][0]) + (be - ranges[1][0]));
+            for (uint64_t r = ranges[2][0]; r < ranges[5][1]; ++r) wk.ref_of_int.push_back(uint32_t(r));
+            return plain;
+        };
+        wk.ep = add_group(wp.edge_ranges);
+        wk.mp = add_group(wp.mid_ranges);
+        wk.int_of_ref.assign(wk.n, 0);
+        wk.global_of_int.resize(wk.n);
+        for (uint32_t j = 0; j < wk.n; ++j) {
+            wk.int_of_ref[wk.ref_of_int[j]] = j;
+            wk.global_of_int[j] = wp.sites[wk.ref_of_int[j]];
+        }
+
+        // Lookup subset: own sites + halo (slab: the two adjacent planes;
+        // fallback split: every site), in zyx order.
+        std::vector<uint64_t> lkeys;
+        std::vector<int32_t> lowner;
+        std::vector<uint32_t> llocal, lglobal;
+        {
+            int32_t pmin = INT32_MAX, pmax = INT32_MIN;
+            if (part.slab) {
+                for (size_t k = 0; k < part.plane_owner.size(); ++k)
+                    if (part.plane_owner[k] == w) {
+                        pmin = std::min(pmin, part.plane_lo + int32_t(k));
+                        pmax = std::max(pmax, part.plane_lo + int32_t(k));
+                    }
+            }
+            const int ax = part.axis;
+            std::vector<uint32_t> g_int_local(0);
+            for (uint64_t q = 0; q < ix.keys.size(); ++q) {
+                const uint32_t g = ix.value[q];
+                const int32_t c = dom.coords[3 * uint64_t(g) + ax];
+                if (part.slab && (c < pmin - 1 || c > pmax + 1)) continue;
+                lkeys.push_back(ix.keys[q]);
+                lowner.push_back(part.owner[g]);
+                lglobal.push_back(g);
+                llocal.push_back(part.owner[g] == w ? wk.int_of_ref[part.local_index[g]] : 0u);
+            }
+        }
+        SiteIndex lix;
+        lix.keys = lkeys;
+        lix.build_rows();
+
+        // upload build inputs
+        std::vector<int32_t> coords(3 * uint64_t(wk.n));
+        std::vector<uint8_t> kind(18 * uint64_t(wk.n));
+        for (uint32_t j = 0; j < wk.n; ++j) {
+            const uint64_t g = wk.global_of_int[j];
+            std::memcpy(&coords[3 * uint64_t(j)], &dom.coords[3 * g], 12);
+            std::memcpy(&kind[18 * uint64_t(j)], &dom.link_kind[18 * g], 18);
+        }
+        std::vector<uint64_t> io_pos;
+        std::vector<uint16_t> io_id;
+        for (size_t q = 0; q < dom.iolet_link_pos.size(); ++q) {
+            const uint64_t g = dom.iolet_link_pos[q] / 18;
+            if (part.owner[g] != w) continue;
+            const uint32_t j = wk.int_of_ref[part.local_index[g]];
+            const uint64_t i1 = dom.iolet_link_pos[q] % 18;  // i - 1
+            io_pos.push_back(i1 * wk.P + j);
+            io_id.push_back(dom.iolet_link_id[q]);
+        }
+        DevMem d_coords, d_kind, d_gidx, d_lk, d_lo, d_ll, d_lg, d_row, d_iop, d_ioi;
+        const int32_t* dc = upload(d_coords, coords, s);
+        const uint8_t* dk = upload(d_kind, kind, s);
+        const uint32_t* dg = upload(d_gidx, wk.global_of_int, s);
+        DLookup L{};
+        L.keys = upload(d_lk, lkeys, s);
+        L.owner = upload(d_lo, lowner, s);
+        L.local = upload(d_ll, llocal, s);
+        L.global = upload(d_lg, lglobal, s);
+        L.n = lkeys.size();
+        if (lix.rows) {
+            L.row_off = upload(d_row, lix.row_off, s);
+            L.lo1 = lix.lo[1];
+            L.hi1 = lix.hi[1];
+            L.lo2 = lix.lo[2];
+            L.hi2 = lix.hi[2];
+            L.ny = lix.ny;
+        }
+        uint32_t* tab = wk.tab.alloc<uint32_t>(18 * wk.P);
+        CK(cudaMemsetAsync(tab, 0, 18 * wk.P * sizeof(uint32_t), s));
+        const uint64_t cap = 18 * uint64_t(wk.n_edge) + 1;
+        DevMem ok_, ov_, ik_, iv_, cnt, ok2, ov2, ik2, iv2;
+        auto* okeys = ok_.alloc<unsigned long long>(cap);
+        auto* ovals = ov_.alloc<unsigned long long>(cap);
+        auto* ikeys = ik_.alloc<unsigned long long>(cap);
+        auto* ivals = iv_.alloc<unsigned long long>(cap);
+        unsigned* counters = cnt.alloc<unsigned>(4);
+        CK(cudaMemsetAsync(counters, 0, 4 * sizeof(unsigned), s));
+        if (wk.n)
+            build_links<<<blocks_for(uint64_t(wk.n) * 18), 256, 0, s>>>(
+                wk.n, wk.P, dc, dk, dg, w, L, tab, okeys, ovals, counters + 0, ikeys, ivals, counters + 1,
+                counters + 2);
+        CK(cudaGetLastError());
+        const uint64_t* dip = upload(d_iop, io_pos, s);
+        const uint16_t* dii = upload(d_ioi, io_id, s);
+        if (!io_pos.empty())
+            patch_iolets<<<blocks_for(io_pos.size()), 256, 0, s>>>(dip, dii, uint32_t(io_pos.size()), tab);
+        CK(cudaGetLastError());
+        unsigned hc[4];
+        CK(cudaMemcpyAsync(hc, counters, sizeof(hc), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (hc[2]) runtime_error("build_streaming_map: fluid link to a site outside the worker's halo");
+        if (hc[0] > cap || hc[1] > cap) runtime_error("build_streaming_map: cross-link overflow");
+        const uint32_t n_out = hc[0], n_in = hc[1];
+        // canonical order: (neighbour, sender global site, direction)
+        auto* okeys2 = ok2.alloc<unsigned long long>(cap);
+        auto* ovals2 = ov2.alloc<unsigned long long>(cap);
+        auto* ikeys2 = ik2.alloc<unsigned long long>(cap);
+        auto* ivals2 = iv2.alloc<unsigned long long>(cap);
+        auto radix = [&](unsigned long long* k, unsigned long long* v, unsigned long long* k2,
+                         unsigned long long* v2, uint32_t m) {
+            if (!m) return;
+            size_t tmp = 0;
+            CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, k, k2, v, v2, int(m), 0, 64, s));
+            DevMem t;
+            void* tp = t.alloc<char>(tmp);
+            CK(cub::DeviceRadixSort::SortPairs(tp, tmp, k, k2, v, v2, int(m), 0, 64, s));
+            CK(cudaStreamSynchronize(s));
+        };
+        radix(okeys, ovals, okeys2, ovals2, n_out);
+        radix(ikeys, ivals, ikeys2, ivals2, n_in);
+        std::vector<unsigned long long> hok(n_out), hik(n_in);
+        if (n_out) CK(cudaMemcpy(hok.data(), okeys2, n_out * 8ull, cudaMemcpyDeviceToHost));
+        if (n_in) CK(cudaMemcpy(hik.data(), ikeys2, n_in * 8ull, cudaMemcpyDeviceToHost));
+        std::map<int, uint32_t> cout_, cin_;
+        for (auto k : hok) ++cout_[int(k >> 40)];
+        for (auto k : hik) ++cin_[int(k >> 40)];
+        if (cout_ != cin_) runtime_error("build_streaming_map: asymmetric cross-link counts");
+        // neighbours must match the partition's list (decomp.hpp:170-171)
+        std::vector<int> nbs;
+        for (auto& kv : cout_) nbs.push_back(kv.first);
+        if (nbs != wp.neighbors) runtime_error("build_streaming_map: neighbour set mismatch");
+        uint32_t base = 0;
+        wk.segs.clear();
+        for (auto& kv : cout_) {
+            wk.segs.push_back({kv.first, base, kv.second});
+            base += kv.second;
+        }
+        wk.shared = base;
+        if (wk.shared >= (1u << 29)) runtime_error("engine: shared region exceeds the table payload");
+        uint64_t* rf = wk.recv_flat.alloc<uint64_t>(std::max<uint32_t>(wk.shared, 1));
+        uint64_t* sp = wk.send_pos.alloc<uint64_t>(std::max<uint32_t>(wk.shared, 1));
+        if (wk.shared)
+            assign_slots<<<blocks_for(wk.shared), 256, 0, s>>>(ovals2, ivals2, wk.shared, tab, rf, sp);
+        CK(cudaGetLastError());
+
+        // distribution store, f_old = equilibrium(rho0, 0) (engine.hpp:243-260)
+        for (int b = 0; b < 2; ++b) {
+            double* f = wk.fbuf[b].alloc<double>(wk.fsize());
+            CK(cudaMemsetAsync(f, 0, wk.fsize() * sizeof(double), s));
+        }
+        wk.old = 0;
+        Eq19 eq;
+        feq_all(prm.rho0, 0.0, 0.0, 0.0, eq.v);
+        if (wk.n) lbm_init_equilibrium<<<blocks_for(wk.n), 256, 0, s>>>(wk.f_old(), wk.P, wk.n, eq);
+        CK(cudaGetLastError());
+
+        // iolet sites' coordinates (edge iolet range then mid iolet range)
+        std::vector<int32_t> ioc;
+        for (uint32_t j = wk.ep; j < wk.n_edge; ++j)
+            for (int a = 0; a < 3; ++a) ioc.push_back(coords[3 * uint64_t(j) + a]);
+        for (uint32_t j = wk.n_edge + wk.mp; j < wk.n; ++j)
+            for (int a = 0; a < 3; ++a) ioc.push_back(coords[3 * uint64_t(j) + a]);
+        upload(wk.io_coords, ioc, s);
+        upload(wk.io_geo, io_host, s);
+        wk.cap4.alloc<double>(4 * uint64_t(std::max<uint32_t>(wk.n, 1)));
+        CK(cudaStreamSynchronize(s));
+    }
+
+    // init_observation (engine.hpp:262-288)
+    void init_observation() {
+        const size_t n_io = dom.iolets.size();
+        obs_order.assign(n_io, {});
+        for (auto& wp : W)
+            if (wp) wp->obs_sites.assign(n_io, {});
+        std::vector<std::vector<uint32_t>> per_w_count(size_t(prm.workers), std::vector<uint32_t>(n_io, 0));
+        size_t q = 0;
+        std::vector<uint8_t> member(n_io);
+        while (q < dom.iolet_link_pos.size()) {
+            const uint64_t g = dom.iolet_link_pos[q] / 18;
+            std::fill(member.begin(), member.end(), 0);
+            while (q < dom.iolet_link_pos.size() && dom.iolet_link_pos[q] / 18 == g) {
+                member[dom.iolet_link_id[q]] = 1;
+                ++q;
+            }
+            for (size_t k = 0; k < n_io; ++k) {
+                if (!member[k]) continue;
+                const int w = part.owner[g];
+                obs_order[k].push_back({w, per_w_count[size_t(w)][k]++});
+                if (W[size_t(w)]) {
+                    WorkerDev& wk = *W[size_t(w)];
+                    wk.obs_sites[k].push_back(wk.int_of_ref[part.local_index[g]]);
+                }
+            }
+        }
+        for (auto& wp : W) {
+            if (!wp) continue;
+            WorkerDev& wk = *wp;
+            CK(cudaSetDevice(wk.dev));
+            std::vector<uint32_t> site;
+            std::vector<uint16_t> iol;
+            wk.obs_off.assign(n_io + 1, 0);
+            for (size_t k = 0; k < n_io; ++k) {
+                wk.obs_off[k] = uint32_t(site.size());
+                for (uint32_t j : wk.obs_sites[k]) {
+                    site.push_back(j);
+                    iol.push_back(uint16_t(k));
+                }
+            }
+            wk.obs_off[n_io] = uint32_t(site.size());
+            wk.n_obs = uint32_t(site.size());
+            upload(wk.obs_site, site, wk.sM);
+            upload(wk.obs_iolet, iol, wk.sM);
+            CK(cudaStreamSynchronize(wk.sM));
+        }
+    }
+
+    // ---- stepping -----------------------------------------------------------
+    void launch_range(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, bool iolet, const double* staged,
+                      const int32_t* coords) {
+        if (e <= b) return;
+        IoletArgs ia{wk.io_geo.get<IoletDev>(), staged, coords};
+        const unsigned nb = blocks_for(e - b);
+        if (iolet) {
+            lbm_push<true><<<nb, 256, 0, s>>>(wk.f_old(), wk.f_new(), wk.tab.get<uint32_t>(), wk.P, b, e, omega, ia);
+        } else {
+            cudaEvent_t e0 = nullptr, e1 = nullptr;
+            if (kernel_timing) {
+                if (wk.tev_used + 2 > wk.tev.size()) {
+                    for (int k = 0; k < 2; ++k) {
+                        cudaEvent_t ev;
+                        CK(cudaEventCreate(&ev));
+                        wk.tev.push_back(ev);
+                    }
+                }
+                e0 = wk.tev[wk.tev_used++];
+                e1 = wk.tev[wk.tev_used++];
+                CK(cudaEventRecord(e0, s));
+            }
+            lbm_push<false><<<nb, 256, 0, s>>>(wk.f_old(), wk.f_new(), wk.tab.get<uint32_t>(), wk.P, b, e, omega, ia);
+            if (kernel_timing) CK(cudaEventRecord(e1, s));
+            plain_launches++;
+            plain_sites += e - b;
+        }
+        CK(cudaGetLastError());
+    }
+
+    void advance_group(WorkerDev& wk, cudaStream_t s, bool edge, const double* staged) {
+        const int32_t* ioc = wk.io_coords.get<int32_t>();
+        if (edge) {
+            launch_range(wk, s, 0, wk.ep, false, staged, ioc);
+            launch_range(wk, s, wk.ep, wk.n_edge, true, staged, ioc);
+        } else {
+            launch_range(wk, s, wk.n_edge, wk.n_edge + wk.mp, false, staged, ioc);
+            launch_range(wk, s, wk.n_edge + wk.mp, wk.n, true, staged, ioc + 3 * uint64_t(wk.n_edge - wk.ep));
+        }
+    }
+
+    void send_inproc(WorkerDev& wk) {
+        for (const Seg& sg : wk.segs) {
+            WorkerDev& peer = *W[size_t(sg.nb)];
+            const Seg* ps = find_seg(peer, wk.w);
+            const double* src = wk.f_new() + uint64_t(kQ) * wk.P + sg.base;
+            double* dst = peer.f_old() + uint64_t(kQ) * peer.P + ps->base;
+            if (wk.dev == peer.dev)
+                CK(cudaMemcpyAsync(dst, src, sg.count * sizeof(double), cudaMemcpyDeviceToDevice, wk.sE));
+            else
+                CK(cudaMemcpyPeerAsync(dst, peer.dev, src, wk.dev, sg.count * sizeof(double), wk.sE));
+        }
+        CK(cudaEventRecord(wk.evSend, wk.sE));
+    }
+
+    void exchange_nccl(WorkerDev& wk) {
+        NK(ncclGroupStart());
+        for (const Seg& sg : wk.segs) {
+            NK(ncclSend(wk.f_new() + uint64_t(kQ) * wk.P + sg.base, sg.count, ncclDouble, sg.nb, comm, wk.sE));
+            NK(ncclRecv(wk.f_old() + uint64_t(kQ) * wk.P + sg.base, sg.count, ncclDouble, sg.nb, comm, wk.sE));
+        }
+        NK(ncclGroupEnd());
+    }
+
+    void post_receive(WorkerDev& wk) {
+        if (!wk.shared) return;
+        lbm_post_receive<<<blocks_for(wk.shared), 256, 0, wk.sE>>>(
+            wk.f_old() + uint64_t(kQ) * wk.P, wk.f_new(), wk.recv_flat.get<uint64_t>(), wk.shared);
+        CK(cudaGetLastError());
+    }
+
+    void observe(WorkerDev& wk, cudaStream_t s, const double* f, uint64_t row) {
+        if (!wk.n_obs) return;
+        double* out = wk.obs_buf.get<double>() + 3 * (row - wk.obs_row_base) * wk.n_obs;
+        lbm_iolet_observe<<<blocks_for(wk.n_obs), 256, 0, s>>>(f, wk.P, wk.n_obs, wk.obs_site.get<uint32_t>(),
+                                                               wk.obs_iolet.get<uint16_t>(), wk.io_geo.get<IoletDev>(), out);
+        CK(cudaGetLastError());
+    }
+
+    void capture(WorkerDev& wk, cudaStream_t s, const double* f, uint64_t step) {
+        Capture* c = nullptr;
+        for (Capture& x : caps)
+            if (x.step == step) c = &x;
+        if (!c) return;
+        if (wk.n)
+            lbm_capture_moments<<<blocks_for(wk.n), 256, 0, s>>>(f, wk.P, wk.n, wk.cap4.get<double>());
+        CK(cudaGetLastError());
+        std::vector<double> h(4 * uint64_t(wk.n));
+        if (wk.n) CK(cudaMemcpyAsync(h.data(), wk.cap4.get<double>(), h.size() * 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        for (uint32_t j = 0; j < wk.n; ++j)
+            std::memcpy(&c->fields[4 * uint64_t(wk.global_of_int[j])], &h[4 * uint64_t(j)], 32);
+    }
+
+    // record_state (engine.hpp:546-555)
+    void record_state(WorkerDev& wk, cudaStream_t s, uint64_t step, const double* f) {
+        if (prm.capture_period > 0 && step % prm.capture_period == 0) capture(wk, s, f, step);
+        if (prm.observe_iolets) observe(wk, s, f, step);
+    }
+
+    // prepare_records (engine.hpp:290-315)
+    void prepare_records(uint64_t n) {
+        if (prm.capture_period > 0) {
+            const uint64_t p = prm.capture_period;
+            for (uint64_t st = steps_run; st <= steps_run + n; ++st) {
+                if (st % p != 0) continue;
+                if (!caps.empty() && caps.back().step == st) continue;
+                Capture c;
+                c.step = st;
+                c.fields.assign(4 * dom.n, 0.0);
+                caps.push_back(std::move(c));
+            }
+        }
+        if (prm.observe_iolets) {
+            const uint64_t rows = steps_run + n + 1;
+            const uint64_t first = steps_run == 0 ? 0 : steps_run + 1;
+            for (auto& wp : W) {
+                if (!wp) continue;
+                wp->obs_row_base = first;
+                wp->obs_rows = rows - first;
+                CK(cudaSetDevice(wp->dev));
+                wp->obs_buf.alloc<double>(3 * std::max<uint64_t>(wp->obs_rows * wp->n_obs, 1));
+            }
+        }
+    }
+
+    void run(uint64_t n) {
+        prepare_records(n);
+        if (steps_run == 0)
+            for (auto& wp : W)
+                if (wp) {
+                    CK(cudaSetDevice(wp->dev));
+                    record_state(*wp, wp->sM, 0, wp->f_old());
+                }
+        // host staging of the per-step iolet values (engine.hpp:332-341)
+        const size_t n_io = bcs.size();
+        std::vector<double> staged(std::max<size_t>(n * n_io, 1), 0.0);
+        for (uint64_t k = 0; k < n; ++k) {
+            const double t = double(steps_run + k + 1) * prm.dt_s;
+            for (size_t io = 0; io < n_io; ++io) {
+                const double v = bcs[io].table.at(t);
+                staged[k * n_io + io] = bcs[io].kind == 1 ? v : v / kCs2;
+            }
+        }
+        for (auto& wp : W) {
+            if (!wp) continue;
+            CK(cudaSetDevice(wp->dev));
+            upload(wp->staged, staged, wp->sM);
+            CK(cudaStreamSynchronize(wp->sM));
+            wp->tev_used = 0;
+        }
+        std::vector<cudaEvent_t> t0(W.size(), nullptr), t1(W.size(), nullptr);
+        for (size_t w = 0; w < W.size(); ++w)
+            if (W[w]) {
+                CK(cudaSetDevice(W[w]->dev));
+                CK(cudaEventCreate(&t0[w]));
+                CK(cudaEventCreate(&t1[w]));
+            }
+        const auto h0 = std::chrono::steady_clock::now();
+        for (size_t w = 0; w < W.size(); ++w)
+            if (W[w]) {
+                CK(cudaSetDevice(W[w]->dev));
+                CK(cudaEventRecord(t0[w], W[w]->sM));
+                CK(cudaStreamWaitEvent(W[w]->sE, t0[w], 0));
+            }
+        try {
+            for (uint64_t k = 0; k < n; ++k) step_once(k, k * n_io);
+        } catch (const Error& e) {
+            if (e.kind == ErrKind::Comm) throw Error(ErrKind::Comm, "worker " + std::to_string(rank) + ": " + e.what());
+            throw;
+        }
+        for (size_t w = 0; w < W.size(); ++w)
+            if (W[w]) {
+                CK(cudaSetDevice(W[w]->dev));
+                CK(cudaEventRecord(t1[w], W[w]->sM));
+            }
+        wait_all(t1);
+        const auto h1 = std::chrono::steady_clock::now();
+        double dmax = 0.0;
+        for (size_t w = 0; w < W.size(); ++w)
+            if (W[w]) {
+                float ms = 0.f;
+                CK(cudaEventElapsedTime(&ms, t0[w], t1[w]));
+                dmax = std::max(dmax, double(ms) * 1e-3);
+                if (kernel_timing)
+                    for (size_t q = 0; q + 1 < W[w]->tev_used; q += 2) {
+                        float kms = 0.f;
+                        CK(cudaEventElapsedTime(&kms, W[w]->tev[q], W[w]->tev[q + 1]));
+                        plain_s += double(kms) * 1e-3;
+                    }
+                cudaEventDestroy(t0[w]);
+                cudaEventDestroy(t1[w]);
+            }
+        dev_loop_s += dmax;
+        loop_s += std::chrono::duration<double>(h1 - h0).count();
+        steps_run += n;
+        assemble_series();
+    }
+
+    // Waits for the step loop; in NCCL mode polls for async comm errors and
+    // applies the reference's exchange timeout (engine.hpp:92-101).
+    void wait_all(const std::vector<cudaEvent_t>& ev) {
+        const auto start = std::chrono::steady_clock::now();
+        for (size_t w = 0; w < W.size(); ++w) {
+            if (!W[w]) continue;
+            CK(cudaSetDevice(W[w]->dev));
+            if (!dist) {
+                CK(cudaEventSynchronize(ev[w]));
+                continue;
+            }
+            for (;;) {
+                cudaError_t q = cudaEventQuery(ev[w]);
+                if (q == cudaSuccess) break;
+                if (q != cudaErrorNotReady) CK(q);
+                ncclResult_t ar = ncclSuccess;
+                NK(ncclCommGetAsyncError(comm, &ar));
+                if (ar != ncclSuccess && ar != ncclInProgress)
+                    fail(ErrKind::Comm, std::string("exchange failure: NCCL async error: ") + ncclGetErrorString(ar));
+                const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - start).count();
+                if (el > prm.exchange_timeout_s * 1000.0) {  // generous: whole run, not one take
+                    ncclCommAbort(comm);
+                    comm = nullptr;
+                    const int nb = W[w]->segs.empty() ? -1 : W[w]->segs.front().nb;
+                    fail(ErrKind::Comm, "exchange failure: worker " + std::to_string(w) +
+                                            " timed out waiting for neighbor " + std::to_string(nb));
+                }
+                std::this_thread::sleep_for(std::chrono::microseconds(50));
+            }
+        }
+    }
+
+    // advance_one (engine.hpp:330-363) for every local worker.
+    void step_once(uint64_t k, uint64_t staged_off) {
+        const bool classic = prm.sequence == 0;
+        // PreSend: edge sites
+        for (auto& wp : W) {
+            if (!wp) continue;
+            WorkerDev& wk = *wp;
+            CK(cudaSetDevice(wk.dev));
+            advance_group(wk, wk.sE, true, wk.staged.get<double>() + staged_off);
+            if (classic) {
+                if (dist) exchange_nccl(wk);
+                else send_inproc(wk);
+            }
+        }
+        // PreReceive: mid sites on the second stream
+        for (auto& wp : W) {
+            if (!wp) continue;
+            WorkerDev& wk = *wp;
+            CK(cudaSetDevice(wk.dev));
+            advance_group(wk, wk.sM, false, wk.staged.get<double>() + staged_off);
+            CK(cudaEventRecord(wk.evMid, wk.sM));
+            if (!classic) {
+                CK(cudaStreamWaitEvent(wk.sE, wk.evMid, 0));
+                if (dist) exchange_nccl(wk);
+                else send_inproc(wk);
+            }
+        }
+        // Receive + PostReceive
+        for (auto& wp : W) {
+            if (!wp) continue;
+            WorkerDev& wk = *wp;
+            CK(cudaSetDevice(wk.dev));
+            if (!dist)
+                for (const Seg& sg : wk.segs) CK(cudaStreamWaitEvent(wk.sE, W[size_t(sg.nb)]->evSend, 0));
+            post_receive(wk);
+        }
+        // EndIteration: join, record, swap
+        const uint64_t done = steps_run + k + 1;
+        for (auto& wp : W) {
+            if (!wp) continue;
+            WorkerDev& wk = *wp;
+            CK(cudaSetDevice(wk.dev));
+            CK(cudaStreamWaitEvent(wk.sE, wk.evMid, 0));
+            if (prm.capture_period > 0 && done % prm.capture_period == 0)
+                record_state(wk, wk.sE, done, wk.f_new());
+            else if (prm.observe_iolets)
+                observe(wk, wk.sE, wk.f_new(), done);
+            CK(cudaEventRecord(wk.evEnd, wk.sE));
+            CK(cudaStreamWaitEvent(wk.sM, wk.evEnd, 0));
+            wk.old = 1 - wk.old;
+        }
+    }
+
+    // assemble_series (engine.hpp:602-629): reduce in ascending global order.
+    void assemble_series() {
+        if (!prm.observe_iolets) return;
+        const size_t n_io = dom.iolets.size();
+        std::vector<std::vector<double>> hb(W.size());
+        for (size_t w = 0; w < W.size(); ++w) {
+            if (!W[w]) continue;
+            WorkerDev& wk = *W[w];
+            CK(cudaSetDevice(wk.dev));
+            hb[w].resize(3 * wk.obs_rows * wk.n_obs);
+            if (!hb[w].empty())
+                CK(cudaMemcpy(hb[w].data(), wk.obs_buf.get<double>(), hb[w].size() * 8, cudaMemcpyDeviceToHost));
+        }
+        const uint64_t first_row = series.rows;
+        const uint64_t rows = steps_run + 1;
+        series.max_speed.resize(n_io);
+        series.pressure.resize(n_io);
+        series.flow.resize(n_io);
+        for (size_t k = 0; k < n_io; ++k)
+            for (uint64_t row = first_row; row < rows; ++row) {
+                double vmax = 0.0, psum = 0.0, qsum = 0.0;
+                for (const auto& [w, pos] : obs_order[k]) {
+                    if (!W[size_t(w)]) continue;  // dist mode: other ranks' sites
+                    const WorkerDev& wk = *W[size_t(w)];
+                    const double* v = &hb[size_t(w)][3 * ((row - wk.obs_row_base) * wk.n_obs + wk.obs_off[k] + pos)];
+                    vmax = std::max(vmax, v[0]);
+                    psum += v[1];
+                    qsum += v[2];
+                }
+                const double n_obs = double(obs_order[k].size());
+                series.max_speed[k].push_back(vmax);
+                series.pressure[k].push_back(psum / n_obs);
+                series.flow[k].push_back(qsum);
+            }
+        series.rows = rows;
+    }
+
+    // ---- host views -----------------------------------------------------------
+    WorkerDev& local(int w) const {
+        if (w < 0 || w >= prm.workers || !W[size_t(w)])
+            runtime_error("engine: worker " + std::to_string(w) + " is not held by this process");
+        return *W[size_t(w)];
+    }
+
+    void snapshot(double* out) {
+        for (auto& wp : W) {
+            if (!wp) continue;
+            WorkerDev& wk = *wp;
+            CK(cudaSetDevice(wk.dev));
+            if (wk.n)
+                lbm_capture_moments<<<blocks_for(wk.n), 256, 0, wk.sM>>>(wk.f_old(), wk.P, wk.n, wk.cap4.get<double>());
+            CK(cudaGetLastError());
+            std::vector<double> h(4 * uint64_t(wk.n));
+            if (wk.n) CK(cudaMemcpyAsync(h.data(), wk.cap4.get<double>(), h.size() * 8, cudaMemcpyDeviceToHost, wk.sM));
+            CK(cudaStreamSynchronize(wk.sM));
+            for (uint32_t j = 0; j < wk.n; ++j)
+                std::memcpy(&out[4 * uint64_t(wk.global_of_int[j])], &h[4 * uint64_t(j)], 32);
+        }
+    }
+
+    uint64_t ref_idx(const WorkerDev& wk, uint32_t r, int i) const {
+        return prm.layout == 0 ? uint64_t(kQ) * r + uint64_t(i) : uint64_t(i) * wk.n + r;
+    }
+
+    void get_f(int w, int which, double* host) {
+        WorkerDev& wk = local(w);
+        CK(cudaSetDevice(wk.dev));
+        CK(cudaDeviceSynchronize());
+        std::vector<double> h(wk.fsize());
+        const double* src = which == 0 ? wk.f_old() : wk.f_new();
+        CK(cudaMemcpy(h.data(), src, h.size() * 8, cudaMemcpyDeviceToHost));
+        for (uint32_t r = 0; r < wk.n; ++r) {
+            const uint32_t j = wk.int_of_ref[r];
+            for (int i = 0; i < kQ; ++i) host[ref_idx(wk, r, i)] = h[uint64_t(i) * wk.P + j];
+        }
+        for (uint32_t k = 0; k < wk.shared; ++k) host[uint64_t(kQ) * wk.n + k] = h[uint64_t(kQ) * wk.P + k];
+    }
+
+    void set_f(int w, int which, const double* host) {
+        WorkerDev& wk = local(w);
+        CK(cudaSetDevice(wk.dev));
+        CK(cudaDeviceSynchronize());
+        std::vector<double> h(wk.fsize(), 0.0);
+        for (uint32_t r = 0; r < wk.n; ++r) {
+            const uint32_t j = wk.int_of_ref[r];
+            for (int i = 0; i < kQ; ++i) h[uint64_t(i) * wk.P + j] = host[ref_idx(wk, r, i)];
+        }
+        for (uint32_t k = 0; k < wk.shared; ++k) h[uint64_t(kQ) * wk.P + k] = host[uint64_t(kQ) * wk.n + k];
+        double* dst = which == 0 ? wk.f_old() : wk.f_new();
+        CK(cudaMemcpy(dst, h.data(), h.size() * 8, cudaMemcpyHostToDevice));
+    }
+
+    // StreamingMap in the reference encoding (layout.hpp:181-286) from the
+    // device-built table.
+    ExportedMap export_map(int w) {
+        WorkerDev& wk = local(w);
+        CK(cudaSetDevice(wk.dev));
+        CK(cudaDeviceSynchronize());
+        std::vector<uint32_t> tab(18 * wk.P);
+        CK(cudaMemcpy(tab.data(), wk.tab.get<uint32_t>(), tab.size() * 4, cudaMemcpyDeviceToHost));
+        std::vector<uint64_t> rf(wk.shared), sp(wk.shared);
+        if (wk.shared) {
+            CK(cudaMemcpy(rf.data(), wk.recv_flat.get<uint64_t>(), rf.size() * 8, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(sp.data(), wk.send_pos.get<uint64_t>(), sp.size() * 8, cudaMemcpyDeviceToHost));
+        }
+        ExportedMap m;
+        m.n_local = wk.n;
+        m.shared_size = wk.shared;
+        m.dest.resize(18 * uint64_t(wk.n));
+        m.op.resize(18 * uint64_t(wk.n));
+        m.iolet.resize(18 * uint64_t(wk.n));
+        for (uint32_t j = 0; j < wk.n; ++j) {
+            const uint32_t r = wk.ref_of_int[j];
+            for (int i = 1; i < kQ; ++i) {
+                const uint32_t v = tab[uint64_t(i - 1) * wk.P + j];
+                const uint64_t q = 18 * uint64_t(r) + uint64_t(i - 1);
+                uint32_t dest;
+                uint8_t op;
+                uint16_t io = 0;
+                if (v < kSpecial) {
+                    dest = uint32_t(ref_idx(wk, wk.ref_of_int[v], i));
+                    op = 0;
+                } else {
+                    const uint32_t o = (v >> kOpShift) & 3u;
+                    if (o == kOpShared) {
+                        dest = uint32_t(uint64_t(kQ) * wk.n + (v & kPayload));
+                        op = 1;
+                    } else if (o == kOpBounce) {
+                        dest = uint32_t(ref_idx(wk, r, inv(i)));
+                        op = 2;
+                    } else {
+                        dest = uint32_t(ref_idx(wk, r, inv(i)));
+                        op = 3;
+                        io = uint16_t(v & kPayload);
+                    }
+                }
+                m.dest[q] = dest;
+                m.op[q] = op;
+                m.iolet[q] = io;
+            }
+        }
+        m.recv_dest.resize(wk.shared);
+        m.send_site.resize(wk.shared);
+        m.send_dir.resize(wk.shared);
+        for (uint32_t k = 0; k < wk.shared; ++k) {
+            const uint64_t i = rf[k] / wk.P, j = rf[k] % wk.P;
+            m.recv_dest[k] = uint32_t(ref_idx(wk, wk.ref_of_int[j], int(i)));
+            const uint64_t i1 = sp[k] / wk.P, js = sp[k] % wk.P;
+            m.send_site[k] = wk.ref_of_int[js];
+            m.send_dir[k] = uint8_t(i1 + 1);
+        }
+        for (const Seg& sg : wk.segs) {
+            m.seg_neighbor.push_back(sg.nb);
+            m.seg_base.push_back(sg.base);
+            m.seg_count.push_back(sg.count);
+        }
+        return m;
+    }
+};
+
+// ---------------------------------------------------------------------------
+Simulation::Simulation(const Domain& d, std::vector<BCEntry> bcs, Params p)
+    : e_(std::make_unique<Engine>(d, std::move(bcs), std::move(p), 0, 1, nullptr)) {}
+Simulation::Simulation(const Domain& d, std::vector<BCEntry> bcs, Params p, int rank, int nranks,
+                       const void* nccl_id)
+    : e_(std::make_unique<Engine>(d, std::move(bcs), std::move(p), rank, nranks, nccl_id)) {}
+Simulation::~Simulation() = default;
+void Simulation::run(uint64_t n) { e_->run(n); }
+uint64_t Simulation::steps_run() const { return e_->steps_run; }
+double Simulation::step_loop_seconds() const { return e_->loop_s; }
+double Simulation::device_loop_seconds() const { return e_->dev_loop_s; }
+double Simulation::plain_kernel_seconds() const { return e_->plain_s; }
+uint64_t Simulation::plain_kernel_launches() const { return e_->plain_launches; }
+uint64_t Simulation::plain_kernel_sites() const { return e_->plain_sites; }
+void Simulation::set_kernel_timing(bool on) { e_->kernel_timing = on; }
+void Simulation::snapshot(double* out) { e_->snapshot(out); }
+int Simulation::n_workers() const { return e_->prm.workers; }
+bool Simulation::is_local(int w) const {
+    return w >= 0 && w < e_->prm.workers && e_->W[size_t(w)] != nullptr;
+}
+void Simulation::store_shape(int w, uint32_t* n, uint32_t* shared) const {
+    WorkerDev& wk = e_->local(w);
+    if (n) *n = wk.n;
+    if (shared) *shared = wk.shared;
+}
+void Simulation::get_f(int w, int which, double* host) { e_->get_f(w, which, host); }
+void Simulation::set_f(int w, int which, const double* host) { e_->set_f(w, which, host); }
+ExportedMap Simulation::export_map(int w) { return e_->export_map(w); }
+const Partition& Simulation::partition() const { return e_->part; }
+const std::vector<Capture>& Simulation::captures() const { return e_->caps; }
+const Series& Simulation::series() const { return e_->series; }
+
+}  // namespace splbcu

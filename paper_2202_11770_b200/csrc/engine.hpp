@@ -1,0 +1,85 @@
+// B200 engine: the reference's splb::Simulation (engine.hpp:121-650)
+// re-designed around GPU-resident workers.
+#pragma once
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "host.hpp"
+
+namespace splbcu {
+
+struct BCEntry {
+    int kind = 0;  // 0 pressure, 1 velocity
+    TimeTable table;
+};
+
+struct Params {
+    double tau = 0.9, rho0 = 1.0, dt_s = 1.0;
+    int layout = 0, scheme = 0, sequence = 0, workers = 1;
+    uint64_t capture_period = 0;
+    bool observe_iolets = false;
+    double exchange_timeout_s = 30.0;
+    std::vector<int> devices;
+};
+
+struct Capture {
+    uint64_t step = 0;
+    std::vector<double> fields;
+};
+
+struct Series {
+    uint64_t rows = 0;
+    std::vector<std::vector<double>> max_speed, pressure, flow;
+};
+
+// Exported StreamingMap in the reference encoding (layout.hpp:113-140).
+struct ExportedMap {
+    uint32_t n_local = 0, shared_size = 0;
+    std::vector<uint32_t> dest;
+    std::vector<uint8_t> op;
+    std::vector<uint16_t> iolet;
+    std::vector<uint32_t> recv_dest, send_site;
+    std::vector<uint8_t> send_dir;
+    std::vector<int> seg_neighbor;
+    std::vector<uint32_t> seg_base, seg_count;
+};
+
+class Engine;  // defined in engine.cu
+
+class Simulation {
+  public:
+    // In-process: all workers in this process.
+    Simulation(const Domain& d, std::vector<BCEntry> bcs, Params p);
+    // One process per GPU with NCCL (rank owns worker `rank`).
+    Simulation(const Domain& d, std::vector<BCEntry> bcs, Params p, int rank, int nranks,
+               const void* nccl_id);
+    ~Simulation();
+
+    void run(uint64_t n);
+    uint64_t steps_run() const;
+    double step_loop_seconds() const;
+    double device_loop_seconds() const;
+    double plain_kernel_seconds() const;
+    uint64_t plain_kernel_launches() const;
+    uint64_t plain_kernel_sites() const;
+    void set_kernel_timing(bool on);
+    void snapshot(double* out4n);
+    int n_workers() const;
+    bool is_local(int w) const;
+    void store_shape(int w, uint32_t* n, uint32_t* shared) const;
+    void get_f(int w, int which, double* host);
+    void set_f(int w, int which, const double* host);
+    ExportedMap export_map(int w);
+    const Partition& partition() const;
+    const std::vector<Capture>& captures() const;
+    const Series& series() const;
+
+  private:
+    std::unique_ptr<Engine> e_;
+};
+
+std::string nccl_unique_id(void* out128);
+
+}  // namespace splbcu

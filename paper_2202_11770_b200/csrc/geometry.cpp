@@ -1,0 +1,783 @@
+// Sparse domain construction, validation, builders and SPLB file I/O.
+// Semantics follow the reference geometry.hpp / geometry_io.hpp; the data
+// structures are B200-host-first: structure-of-arrays, O(n) generation in
+// (z,y,x) order, a CSR row index instead of a hash map, and parallel loops,
+// so 10^8-site domains build in seconds.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <fstream>
+#include <mutex>
+#include <thread>
+
+#include "host.hpp"
+
+namespace splbcu {
+
+int hw_threads() {
+    static int n = [] {
+        unsigned h = std::thread::hardware_concurrency();
+        return int(h == 0 ? 1 : std::min(h, 64u));
+    }();
+    return n;
+}
+
+void parallel_for(uint64_t n, const std::function<void(uint64_t, uint64_t, int)>& fn,
+                  uint64_t min_chunk) {
+    const int nt = int(std::min<uint64_t>(hw_threads(), (n + min_chunk - 1) / std::max<uint64_t>(min_chunk, 1)));
+    if (nt <= 1) {
+        if (n) fn(0, n, 0);
+        return;
+    }
+    std::vector<std::thread> th;
+    std::vector<std::exception_ptr> err(nt);
+    const uint64_t chunk = (n + nt - 1) / nt;
+    for (int t = 0; t < nt; ++t) {
+        const uint64_t b = uint64_t(t) * chunk, e = std::min(n, b + chunk);
+        th.emplace_back([&, b, e, t] {
+            try {
+                if (b < e) fn(b, e, t);
+            } catch (...) {
+                err[t] = std::current_exception();
+            }
+        });
+    }
+    for (auto& t : th) t.join();
+    for (auto& e : err)
+        if (e) std::rethrow_exception(e);
+}
+
+uint16_t Domain::link_iolet(uint64_t s, int i) const {
+    const uint64_t pos = 18 * s + uint64_t(i - 1);
+    auto it = std::lower_bound(iolet_link_pos.begin(), iolet_link_pos.end(), pos);
+    if (it == iolet_link_pos.end() || *it != pos) return 0;
+    return iolet_link_id[size_t(it - iolet_link_pos.begin())];
+}
+
+// ---- SiteIndex --------------------------------------------------------------
+
+static inline void key_coords(uint64_t k, int32_t& x, int32_t& y, int32_t& z) {
+    const uint64_t m = (uint64_t(1) << 21) - 1;
+    x = int32_t(int64_t(k & m) - kBias);
+    y = int32_t(int64_t((k >> 21) & m) - kBias);
+    z = int32_t(int64_t(k >> 42) - kBias);
+}
+
+void SiteIndex::build_rows() {
+    rows = false;
+    row_off.clear();
+    if (keys.empty()) return;
+    for (int a = 0; a < 3; ++a) lo[a] = INT32_MAX, hi[a] = INT32_MIN;
+    // keys are sorted: z range from ends; x/y ranges need a scan
+    int32_t x, y, z;
+    key_coords(keys.front(), x, y, z);
+    lo[2] = z;
+    key_coords(keys.back(), x, y, z);
+    hi[2] = z;
+    std::vector<int32_t> lx(hw_threads(), INT32_MAX), hx(hw_threads(), INT32_MIN),
+        ly(hw_threads(), INT32_MAX), hy(hw_threads(), INT32_MIN);
+    parallel_for(keys.size(), [&](uint64_t b, uint64_t e, int t) {
+        int32_t X, Y, Z;
+        for (uint64_t k = b; k < e; ++k) {
+            key_coords(keys[k], X, Y, Z);
+            lx[t] = std::min(lx[t], X);
+            hx[t] = std::max(hx[t], X);
+            ly[t] = std::min(ly[t], Y);
+            hy[t] = std::max(hy[t], Y);
+        }
+    });
+    lo[0] = *std::min_element(lx.begin(), lx.end());
+    hi[0] = *std::max_element(hx.begin(), hx.end());
+    lo[1] = *std::min_element(ly.begin(), ly.end());
+    hi[1] = *std::max_element(hy.begin(), hy.end());
+    ny = int64_t(hi[1]) - lo[1] + 1;
+    nz = int64_t(hi[2]) - lo[2] + 1;
+    const double nrows = double(ny) * double(nz);
+    if (nrows > double(uint64_t(1) << 28) || nrows > 8.0 * double(keys.size()) + 4096.0) return;
+    row_off.assign(size_t(ny * nz + 1), 0);
+    // count per row then prefix (keys sorted, so rows are contiguous)
+    for (uint64_t k = 0; k < keys.size(); ++k) {
+        key_coords(keys[k], x, y, z);
+        ++row_off[size_t((int64_t(z) - lo[2]) * ny + (int64_t(y) - lo[1])) + 1];
+    }
+    for (size_t r = 1; r < row_off.size(); ++r) row_off[r] += row_off[r - 1];
+    rows = true;
+}
+
+int64_t SiteIndex::find(int32_t x, int32_t y, int32_t z) const {
+    const uint64_t key = zyx_key(x, y, z);
+    uint64_t b = 0, e = keys.size();
+    if (rows) {
+        if (y < lo[1] || y > hi[1] || z < lo[2] || z > hi[2]) return -1;
+        const size_t r = size_t((int64_t(z) - lo[2]) * ny + (int64_t(y) - lo[1]));
+        b = row_off[r];
+        e = row_off[r + 1];
+    }
+    auto it = std::lower_bound(keys.begin() + b, keys.begin() + e, key);
+    if (it == keys.begin() + e || *it != key) return -1;
+    return int64_t(it - keys.begin());
+}
+
+SiteIndex index_domain(const Domain& d) {
+    SiteIndex ix;
+    ix.keys.resize(d.n);
+    std::vector<uint32_t> perm(d.n);
+    parallel_for(d.n, [&](uint64_t b, uint64_t e, int) {
+        for (uint64_t s = b; s < e; ++s) {
+            ix.keys[s] = zyx_key(d.coords[3 * s], d.coords[3 * s + 1], d.coords[3 * s + 2]);
+            perm[s] = uint32_t(s);
+        }
+    });
+    // Domain order is type-major and zyx-sorted inside each type range: a
+    // 6-way merge gives the global zyx order.
+    std::vector<uint64_t> mk(d.n);
+    std::vector<uint32_t> mv(d.n);
+    {
+        std::vector<std::pair<uint64_t, uint64_t>> runs;
+        for (int t = 0; t < 6; ++t)
+            if (d.type_ranges[t][1] > d.type_ranges[t][0])
+                runs.push_back({d.type_ranges[t][0], d.type_ranges[t][1]});
+        bool sorted_runs = true;
+        for (auto& r : runs)
+            for (uint64_t k = r.first + 1; k < r.second && sorted_runs; ++k)
+                if (!(ix.keys[k - 1] < ix.keys[k])) sorted_runs = false;
+        if (!sorted_runs || runs.empty()) {
+            std::sort(perm.begin(), perm.end(),
+                      [&](uint32_t a, uint32_t b) { return ix.keys[a] < ix.keys[b]; });
+            for (uint64_t k = 0; k < d.n; ++k) mk[k] = ix.keys[perm[k]], mv[k] = perm[k];
+        } else {
+            std::vector<uint64_t> pos(runs.size());
+            for (size_t r = 0; r < runs.size(); ++r) pos[r] = runs[r].first;
+            for (uint64_t k = 0; k < d.n; ++k) {
+                int best = -1;
+                for (size_t r = 0; r < runs.size(); ++r)
+                    if (pos[r] < runs[r].second &&
+                        (best < 0 || ix.keys[pos[r]] < ix.keys[pos[size_t(best)]]))
+                        best = int(r);
+                const uint64_t s = pos[size_t(best)]++;
+                mk[k] = ix.keys[s];
+                mv[k] = uint32_t(s);
+            }
+        }
+    }
+    ix.keys.swap(mk);
+    ix.value.swap(mv);
+    ix.build_rows();
+    return ix;
+}
+
+// ---- classification (geometry.hpp:100-208) ----------------------------------
+
+static double dot3(const double* a, const double* b) { return (a[0] * b[0] + a[1] * b[1]) + a[2] * b[2]; }
+
+// crosses_iolet (geometry.hpp:102-113)
+static bool crosses_iolet(const double a[3], const double b[3], const IoletGeo& io) {
+    const double da[3] = {a[0] - io.center[0], a[1] - io.center[1], a[2] - io.center[2]};
+    const double db[3] = {b[0] - io.center[0], b[1] - io.center[1], b[2] - io.center[2]};
+    const double sa = dot3(da, io.normal);
+    const double sb = dot3(db, io.normal);
+    if (!(sa > 0.0 && sb <= 0.0)) return false;
+    const double t = sa / (sa - sb);
+    const double p[3] = {a[0] + t * (b[0] - a[0]), a[1] + t * (b[1] - a[1]), a[2] + t * (b[2] - a[2])};
+    const double d[3] = {p[0] - io.center[0], p[1] - io.center[1], p[2] - io.center[2]};
+    const double r2 = dot3(d, d);
+    const double rmax = io.radius + 1.0;  // kIoletClassifyMargin (geometry.hpp:78)
+    return r2 <= rmax * rmax;
+}
+
+static bool unit_normal(const IoletGeo& io) {
+    return !(std::abs(std::sqrt(dot3(io.normal, io.normal)) - 1.0) > 1e-12);
+}
+
+static uint8_t type_of(bool wall, bool inlet, bool outlet) {
+    if (inlet) return wall ? 4 : 2;
+    if (outlet) return wall ? 5 : 3;
+    return wall ? 1 : 0;
+}
+
+// Core of classify_sites for voxels already in strictly ascending zyx order
+// (duplicates rejected by the caller).  input_index maps a sorted position
+// back to the caller's order so error reports name the same site as the
+// reference (the first offending voxel in input order).
+static Domain classify_sorted(std::vector<int32_t>&& coords, const std::vector<uint64_t>& keys,
+                              const std::vector<uint32_t>* input_index,
+                              std::vector<IoletGeo>&& iolets, double voxel_size) {
+    const uint64_t n = keys.size();
+    SiteIndex ix;
+    ix.keys = keys;
+    ix.build_rows();
+
+    std::vector<uint8_t> kind(18 * n);
+    std::vector<uint8_t> type(n);
+    const int nt = hw_threads();
+    std::vector<std::vector<uint32_t>> io_count(nt, std::vector<uint32_t>(iolets.size(), 0));
+    std::vector<std::vector<std::pair<uint64_t, uint16_t>>> io_links(nt);
+    // per thread: smallest input index of an inlet+outlet site, and its position
+    std::vector<uint64_t> bad_in(nt, UINT64_MAX), bad_pos(nt, UINT64_MAX);
+
+    parallel_for(n, [&](uint64_t b, uint64_t e, int t) {
+        for (uint64_t s = b; s < e; ++s) {
+            const int32_t x = coords[3 * s], y = coords[3 * s + 1], z = coords[3 * s + 2];
+            const double a[3] = {double(x), double(y), double(z)};
+            bool wall = false, inlet = false, outlet = false;
+            for (int i = 1; i < kQ; ++i) {
+                const int32_t tx = x + cx(i), ty = y + cy(i), tz = z + cz(i);
+                uint8_t k;
+                // +-x neighbours are adjacent in zyx order
+                bool member;
+                if (cy(i) == 0 && cz(i) == 0) {
+                    const int64_t p = int64_t(s) + cx(i);
+                    member = p >= 0 && uint64_t(p) < n && keys[uint64_t(p)] == zyx_key(tx, ty, tz);
+                } else {
+                    member = ix.find(tx, ty, tz) >= 0;
+                }
+                if (member) {
+                    k = 0;
+                } else {
+                    k = 1;
+                    const double bb[3] = {double(tx), double(ty), double(tz)};
+                    for (size_t io = 0; io < iolets.size(); ++io)
+                        if (crosses_iolet(a, bb, iolets[io])) {
+                            k = iolets[io].kind == 0 ? 2 : 3;
+                            io_links[t].push_back({18 * s + uint64_t(i - 1), uint16_t(io)});
+                            ++io_count[t][io];
+                            break;
+                        }
+                }
+                kind[18 * s + uint64_t(i - 1)] = k;
+                wall |= k == 1;
+                inlet |= k == 2;
+                outlet |= k == 3;
+            }
+            if (inlet && outlet) {
+                const uint64_t in_idx = input_index ? (*input_index)[s] : s;
+                if (in_idx < bad_in[t]) bad_in[t] = in_idx, bad_pos[t] = s;
+            }
+            type[s] = type_of(wall, inlet, outlet);
+        }
+    });
+    uint64_t s = UINT64_MAX, best_in = UINT64_MAX;
+    for (int t = 0; t < nt; ++t)
+        if (bad_in[t] < best_in) best_in = bad_in[t], s = bad_pos[t];
+    if (s != UINT64_MAX) {
+        geometry_error("classify_sites: site (" + std::to_string(coords[3 * s]) + "," +
+                       std::to_string(coords[3 * s + 1]) + "," + std::to_string(coords[3 * s + 2]) +
+                       ") carries both inlet and outlet links");
+    }
+    for (size_t io = 0; io < iolets.size(); ++io) {
+        uint64_t c = 0;
+        for (int t = 0; t < nt; ++t) c += io_count[t][io];
+        if (c == 0)
+            geometry_error("classify_sites: iolet " + std::to_string(io) +
+                           " intersects no boundary links");
+    }
+
+    // Stable counting sort by type over the zyx order == sort by (type,z,y,x)
+    // (geometry.hpp:189-195).
+    Domain d;
+    d.voxel_size = voxel_size;
+    d.n = n;
+    d.iolets = std::move(iolets);
+    uint64_t cnt[6] = {};
+    for (uint64_t s = 0; s < n; ++s) ++cnt[type[s]];
+    uint64_t pos = 0;
+    for (int t = 0; t < 6; ++t) {
+        d.type_ranges[t][0] = pos;
+        pos += cnt[t];
+        d.type_ranges[t][1] = pos;
+    }
+    std::vector<uint64_t> dst(n);
+    {
+        uint64_t next[6];
+        for (int t = 0; t < 6; ++t) next[t] = d.type_ranges[t][0];
+        for (uint64_t s = 0; s < n; ++s) dst[s] = next[type[s]]++;
+    }
+    d.coords.resize(3 * n);
+    d.types.resize(n);
+    d.link_kind.resize(18 * n);
+    parallel_for(n, [&](uint64_t b, uint64_t e, int) {
+        for (uint64_t s = b; s < e; ++s) {
+            const uint64_t g = dst[s];
+            std::memcpy(&d.coords[3 * g], &coords[3 * s], 12);
+            d.types[g] = type[s];
+            std::memcpy(&d.link_kind[18 * g], &kind[18 * s], 18);
+        }
+    });
+    std::vector<std::pair<uint64_t, uint16_t>> links;
+    for (auto& v : io_links)
+        for (auto& p : v) links.push_back({18 * dst[p.first / 18] + p.first % 18, p.second});
+    std::sort(links.begin(), links.end());
+    d.iolet_link_pos.resize(links.size());
+    d.iolet_link_id.resize(links.size());
+    for (size_t k = 0; k < links.size(); ++k) {
+        d.iolet_link_pos[k] = links[k].first;
+        d.iolet_link_id[k] = links[k].second;
+    }
+    return d;
+}
+
+Domain classify_sites(const std::vector<int32_t>& voxels, std::vector<IoletGeo> iolets,
+                      double voxel_size) {
+    const uint64_t n = voxels.size() / 3;
+    if (n == 0) geometry_error("classify_sites: empty voxel set");
+    for (size_t k = 0; k < iolets.size(); ++k)
+        if (!unit_normal(iolets[k]))
+            geometry_error("classify_sites: iolet " + std::to_string(k) + " normal is not unit length");
+    for (uint64_t s = 0; s < 3 * n; ++s)
+        if (voxels[s] < -(int32_t(1) << 20) + 1 || voxels[s] >= (int32_t(1) << 20) - 1)
+            geometry_error("classify_sites: voxel coordinate out of range");
+    std::vector<uint64_t> keys(n);
+    for (uint64_t s = 0; s < n; ++s) keys[s] = zyx_key(voxels[3 * s], voxels[3 * s + 1], voxels[3 * s + 2]);
+    bool sorted = true;
+    for (uint64_t s = 1; s < n && sorted; ++s) sorted = keys[s - 1] < keys[s];
+    if (sorted) {
+        std::vector<int32_t> c(voxels);
+        return classify_sorted(std::move(c), keys, nullptr, std::move(iolets), voxel_size);
+    }
+    std::vector<uint32_t> perm(n);
+    for (uint64_t s = 0; s < n; ++s) perm[s] = uint32_t(s);
+    std::sort(perm.begin(), perm.end(), [&](uint32_t a, uint32_t b) {
+        return keys[a] < keys[b] || (keys[a] == keys[b] && a < b);
+    });
+    std::vector<uint64_t> sk(n);
+    std::vector<int32_t> sc(3 * n);
+    for (uint64_t k = 0; k < n; ++k) {
+        sk[k] = keys[perm[k]];
+        std::memcpy(&sc[3 * k], &voxels[3 * uint64_t(perm[k])], 12);
+        if (k && sk[k] == sk[k - 1]) geometry_error("classify_sites: duplicate voxel");
+    }
+    return classify_sorted(std::move(sc), sk, &perm, std::move(iolets), voxel_size);
+}
+
+// validate_domain (geometry.hpp:212-271).  Checks run in parallel; the
+// reported violation is the first one in the reference's sequential order.
+void validate_domain(const Domain& d) {
+    if (d.n == 0) geometry_error("domain: empty site list");
+    if (!(d.voxel_size > 0.0)) geometry_error("domain: voxel size must be positive");
+    for (size_t k = 0; k < d.iolets.size(); ++k)
+        if (!unit_normal(d.iolets[k]))
+            geometry_error("domain: iolet " + std::to_string(k) + " normal is not unit length");
+    // duplicates (index_coords)
+    std::vector<uint64_t> keys(d.n);
+    for (uint64_t s = 0; s < d.n; ++s)
+        keys[s] = zyx_key(d.coords[3 * s], d.coords[3 * s + 1], d.coords[3 * s + 2]);
+    std::vector<uint64_t> sk(keys);
+    std::sort(sk.begin(), sk.end());
+    for (uint64_t k = 1; k < d.n; ++k)
+        if (sk[k] == sk[k - 1]) geometry_error("classify_sites: duplicate voxel");
+    uint64_t pos = 0;
+    for (int t = 0; t < 6; ++t) {
+        if (d.type_ranges[t][0] != pos || d.type_ranges[t][1] < pos || d.type_ranges[t][1] > d.n)
+            geometry_error("domain: type_ranges do not partition the sites");
+        pos = d.type_ranges[t][1];
+        for (uint64_t s = d.type_ranges[t][0]; s < d.type_ranges[t][1]; ++s)
+            if (int(d.types[s]) != t) geometry_error("domain: site type outside its range");
+    }
+    if (pos != d.n) geometry_error("domain: type_ranges do not partition the sites");
+
+    SiteIndex ix;
+    ix.keys = std::move(sk);
+    ix.build_rows();
+    const int nt = hw_threads();
+    std::vector<uint64_t> first_bad(nt, UINT64_MAX);
+    std::vector<int> first_code(nt, 0);
+    parallel_for(d.n, [&](uint64_t b, uint64_t e, int t) {
+        size_t lk = size_t(std::lower_bound(d.iolet_link_pos.begin(), d.iolet_link_pos.end(), 18 * b) -
+                           d.iolet_link_pos.begin());
+        for (uint64_t s = b; s < e && first_bad[t] == UINT64_MAX; ++s) {
+            bool wall = false, inlet = false, outlet = false;
+            int code = 0;
+            const int32_t x = d.coords[3 * s], y = d.coords[3 * s + 1], z = d.coords[3 * s + 2];
+            for (int i = 1; i < kQ && !code; ++i) {
+                const uint8_t k = d.link_kind[18 * s + uint64_t(i - 1)];
+                uint16_t io = 0;
+                while (lk < d.iolet_link_pos.size() && d.iolet_link_pos[lk] < 18 * s + uint64_t(i - 1)) ++lk;
+                if (lk < d.iolet_link_pos.size() && d.iolet_link_pos[lk] == 18 * s + uint64_t(i - 1))
+                    io = d.iolet_link_id[lk];
+                const bool in_set = ix.find(x + cx(i), y + cy(i), z + cz(i)) >= 0;
+                if (k == 0) {
+                    if (!in_set) code = 1;
+                } else {
+                    if (in_set) code = 1;
+                    else if (k != 1 && io >= d.iolets.size()) code = 2;
+                }
+                wall |= k == 1;
+                inlet |= k == 2;
+                outlet |= k == 3;
+            }
+            if (!code && inlet && outlet) code = 3;
+            if (!code && d.types[s] != type_of(wall, inlet, outlet)) code = 4;
+            if (code) {
+                first_bad[t] = s;
+                first_code[t] = code;
+            }
+        }
+    });
+    uint64_t best = UINT64_MAX;
+    int code = 0;
+    for (int t = 0; t < nt; ++t)
+        if (first_bad[t] < best) best = first_bad[t], code = first_code[t];
+    switch (code) {
+        case 1: geometry_error("domain: inconsistent link closure");
+        case 2: geometry_error("domain: link references unknown iolet");
+        case 3: geometry_error("domain: site carries both inlet and outlet links");
+        case 4: geometry_error("domain: collision type inconsistent with links");
+        default: break;
+    }
+}
+
+// ---- builders ------------------------------------------------------------------
+
+constexpr double kAxisOffsetX = 0.375;  // geometry.hpp:279
+constexpr double kAxisOffsetY = 0.5;    // geometry.hpp:280
+
+// build_pipe (geometry.hpp:285-308).  Slices are generated in parallel and
+// concatenated in z order, so the voxel list is already zyx-sorted.
+Domain build_pipe(int radius, int length, double voxel_size) {
+    if (radius < 2 || length < 4) geometry_error("build_pipe: need radius >= 2 and length >= 4");
+    const double r2 = double(radius) * radius;
+    std::vector<int32_t> slice;
+    for (int y = -radius - 2; y <= radius + 2; ++y)
+        for (int x = -radius - 2; x <= radius + 2; ++x) {
+            const double dx = x - kAxisOffsetX, dy = y - kAxisOffsetY;
+            if (dx * dx + dy * dy < r2) {
+                slice.push_back(x);
+                slice.push_back(y);
+            }
+        }
+    const uint64_t per = slice.size() / 2;
+    std::vector<int32_t> vox(3 * per * uint64_t(length));
+    parallel_for(uint64_t(length), [&](uint64_t b, uint64_t e, int) {
+        for (uint64_t z = b; z < e; ++z)
+            for (uint64_t k = 0; k < per; ++k) {
+                int32_t* v = &vox[3 * (z * per + k)];
+                v[0] = slice[2 * k];
+                v[1] = slice[2 * k + 1];
+                v[2] = int32_t(z);
+            }
+    }, 1);
+    std::vector<IoletGeo> io = {
+        {0, {kAxisOffsetX, kAxisOffsetY, -0.5}, {0.0, 0.0, 1.0}, double(radius)},
+        {1, {kAxisOffsetX, kAxisOffsetY, double(length - 1) + 0.5}, {0.0, 0.0, -1.0}, double(radius)},
+    };
+    return classify_sites(vox, std::move(io), voxel_size);
+}
+
+// build_bifurcation (geometry.hpp:313-363)
+Domain build_bifurcation(int tr, int br, int tl, int bl, double voxel_size) {
+    if (tr < 2 || br < 2 || tl < 4 || bl < 4)
+        geometry_error("build_bifurcation: need radii >= 2 and lengths >= 4");
+    constexpr double kSlope = 0.5;
+    std::vector<int32_t> vox;
+    const int xmax = int(std::ceil(kSlope * bl)) + tr + br + 2;
+    const int rmax = std::max(tr, br) + 2;
+    for (int z = 0; z < tl + bl; ++z)
+        for (int y = -rmax; y <= rmax; ++y)
+            for (int x = -xmax; x <= xmax; ++x) {
+                const double dy = y - kAxisOffsetY;
+                bool fluid;
+                if (z < tl) {
+                    const double dx = x - kAxisOffsetX;
+                    fluid = dx * dx + dy * dy < tr * tr;
+                } else {
+                    const double xc = kSlope * (z - tl + 1);
+                    const double dp = (x - kAxisOffsetX - xc);
+                    const double dm = (x - kAxisOffsetX + xc);
+                    fluid = dp * dp + dy * dy < br * br || dm * dm + dy * dy < br * br;
+                }
+                if (fluid) {
+                    vox.push_back(x);
+                    vox.push_back(y);
+                    vox.push_back(z);
+                }
+            }
+    const double zend = double(tl + bl - 1) + 0.5;
+    const double xend = kSlope * bl;
+    std::vector<IoletGeo> io = {
+        {0, {kAxisOffsetX, kAxisOffsetY, -0.5}, {0.0, 0.0, 1.0}, double(tr)},
+        {1, {kAxisOffsetX + xend, kAxisOffsetY, zend}, {0.0, 0.0, -1.0}, double(br)},
+        {1, {kAxisOffsetX - xend, kAxisOffsetY, zend}, {0.0, 0.0, -1.0}, double(br)},
+    };
+    return classify_sites(vox, std::move(io), voxel_size);
+}
+
+// Synthetic bifurcating vessel tree (config C3; no reference equivalent —
+// a recursive generalisation of build_bifurcation).  Level 0 is a trunk
+// along +z; every vessel of level k splits into two level-(k+1) vessels
+// whose centrelines diverge linearly, in x for odd levels and in y for even
+// ones, by a lateral offset sized so sibling subtrees never touch.  Each
+// z-slice is a union of discs (one per active vessel).  One pressure/velocity
+// inlet at the trunk start, one outlet disc per leaf in the last slice + 0.5.
+Domain build_tree(int root_radius, int root_length, int levels, double radius_ratio,
+                  double length_ratio, double voxel_size) {
+    if (root_radius < 2 || root_length < 4 || levels < 0 || levels > 12 ||
+        !(radius_ratio > 0.0 && radius_ratio <= 1.0) || !(length_ratio > 0.0))
+        geometry_error("build_tree: need radius >= 2, length >= 4, 0 <= levels <= 12, "
+                       "0 < radius_ratio <= 1, length_ratio > 0");
+    const int L = levels + 1;
+    std::vector<double> rad(L), disp(L, 0.0);
+    std::vector<int> len(L);
+    for (int k = 0; k < L; ++k) {
+        rad[k] = std::max(2.0, root_radius * std::pow(radius_ratio, k));
+    }
+    // lateral offset of a level-k vessel over its length (k >= 1), from the
+    // leaves up: clear the widest descendant spread on the same axis.
+    for (int k = L - 1; k >= 1; --k) {
+        double spread = 0.0;
+        for (int j = k + 2; j < L; j += 2) spread += disp[j];
+        disp[k] = spread + rad[k] + 2.0;
+    }
+    for (int k = 0; k < L; ++k) {
+        int l = int(std::lround(root_length * std::pow(length_ratio, k)));
+        l = std::max(l, 4);
+        if (k >= 1) l = std::max(l, int(std::ceil(1.5 * disp[k])));  // slope <= 2/3
+        len[k] = l;
+    }
+    std::vector<int> z0(L + 1, 0);
+    for (int k = 0; k < L; ++k) z0[k + 1] = z0[k] + len[k];
+    const int nz = z0[L];
+    // Vessel v of level k runs from its parent's end point to that point
+    // +- disp[k] (level 0: the straight trunk).
+    std::vector<std::vector<std::array<double, 4>>> seg(L);  // x0,y0,x1,y1
+    seg[0].push_back({kAxisOffsetX, kAxisOffsetY, kAxisOffsetX, kAxisOffsetY});
+    for (int k = 1; k < L; ++k)
+        for (auto& p : seg[k - 1]) {
+            const double dx = (k % 2 == 1) ? disp[k] : 0.0;
+            const double dy = (k % 2 == 0) ? disp[k] : 0.0;
+            seg[k].push_back({p[2], p[3], p[2] - dx, p[3] - dy});
+            seg[k].push_back({p[2], p[3], p[2] + dx, p[3] + dy});
+        }
+    // voxelise slice by slice (parallel over slices), each slice sorted (y,x)
+    std::vector<std::vector<int32_t>> slices{size_t(nz)};
+    parallel_for(uint64_t(nz), [&](uint64_t b, uint64_t e, int) {
+        std::vector<uint64_t> keys;
+        for (uint64_t zz = b; zz < e; ++zz) {
+            const int z = int(zz);
+            int k = 0;
+            while (k + 1 < L && z >= z0[k + 1]) ++k;
+            keys.clear();
+            const double r = rad[k];
+            const double r2 = r * r;
+            const double f = len[k] > 1 ? double(z - z0[k] + 1) / double(len[k]) : 1.0;
+            auto add_disc = [&](double cx, double cy, double rr2, double rr) {
+                const int x0 = int(std::floor(cx - rr)) - 1, x1 = int(std::ceil(cx + rr)) + 1;
+                const int y0 = int(std::floor(cy - rr)) - 1, y1 = int(std::ceil(cy + rr)) + 1;
+                for (int y = y0; y <= y1; ++y)
+                    for (int x = x0; x <= x1; ++x) {
+                        const double dx = x - cx, dy = y - cy;
+                        if (dx * dx + dy * dy < rr2)
+                            keys.push_back((uint64_t(int64_t(y) + kBias) << 21) | uint64_t(int64_t(x) + kBias));
+                    }
+            };
+            for (auto& s : seg[size_t(k)]) {
+                const double cx = s[0] + f * (s[2] - s[0]);
+                const double cy = s[1] + f * (s[3] - s[1]);
+                add_disc(cx, cy, r2, r);
+            }
+            std::sort(keys.begin(), keys.end());
+            keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
+            auto& out = slices[zz];
+            out.resize(3 * keys.size());
+            const uint64_t m = (uint64_t(1) << 21) - 1;
+            for (size_t q = 0; q < keys.size(); ++q) {
+                out[3 * q] = int32_t(int64_t(keys[q] & m) - kBias);
+                out[3 * q + 1] = int32_t(int64_t(keys[q] >> 21) - kBias);
+                out[3 * q + 2] = z;
+            }
+        }
+    }, 1);
+    uint64_t total = 0;
+    for (auto& s : slices) total += s.size();
+    std::vector<int32_t> vox;
+    vox.reserve(total);
+    for (auto& s : slices) {
+        vox.insert(vox.end(), s.begin(), s.end());
+        std::vector<int32_t>().swap(s);
+    }
+    std::vector<IoletGeo> io;
+    io.push_back({0, {kAxisOffsetX, kAxisOffsetY, -0.5}, {0.0, 0.0, 1.0}, rad[0]});
+    const int k = L - 1;
+    const double zend = double(nz - 1) + 0.5;
+    for (auto& s : seg[size_t(k)]) {
+        // leaf centre extrapolated to the outlet plane
+        const double f = (zend - z0[k] + 1.0) / double(len[k]);
+        io.push_back({1, {s[0] + f * (s[2] - s[0]), s[1] + f * (s[3] - s[1]), zend}, {0.0, 0.0, -1.0}, rad[k]});
+    }
+    return classify_sites(vox, std::move(io), voxel_size);
+}
+
+// Dense rectangular channel (config C4): every voxel of [0,nx)x[0,ny)x[0,nz)
+// is fluid; inlet/outlet discs cover the whole cross-section.
+Domain build_channel(int nx, int ny, int nz, double voxel_size) {
+    if (nx < 2 || ny < 2 || nz < 4) geometry_error("build_channel: need nx, ny >= 2 and nz >= 4");
+    const uint64_t per = uint64_t(nx) * uint64_t(ny);
+    std::vector<int32_t> vox(3 * per * uint64_t(nz));
+    parallel_for(uint64_t(nz), [&](uint64_t b, uint64_t e, int) {
+        for (uint64_t z = b; z < e; ++z)
+            for (int y = 0; y < ny; ++y)
+                for (int x = 0; x < nx; ++x) {
+                    int32_t* v = &vox[3 * (z * per + uint64_t(y) * nx + uint64_t(x))];
+                    v[0] = x;
+                    v[1] = y;
+                    v[2] = int32_t(z);
+                }
+    }, 1);
+    const double cx = 0.5 * (nx - 1), cy = 0.5 * (ny - 1);
+    const double rad = 0.5 * std::sqrt(double(nx) * nx + double(ny) * ny);
+    std::vector<IoletGeo> io = {
+        {0, {cx, cy, -0.5}, {0.0, 0.0, 1.0}, rad},
+        {1, {cx, cy, double(nz - 1) + 0.5}, {0.0, 0.0, -1.0}, rad},
+    };
+    return classify_sites(vox, std::move(io), voxel_size);
+}
+
+// ---- SPLB v1 file format (geometry_io.hpp:14-129) ----------------------------
+
+namespace {
+template <typename T>
+void put(std::ostream& os, const T& v) {
+    os.write(reinterpret_cast<const char*>(&v), sizeof(T));
+}
+template <typename T>
+T get(std::istream& is) {
+    T v;
+    is.read(reinterpret_cast<char*>(&v), sizeof(T));
+    if (!is) geometry_error("geometry load: truncated file");
+    return v;
+}
+}  // namespace
+
+void write_domain(const Domain& d, const std::string& path) {
+    std::ofstream os(path, std::ios::binary);
+    if (!os) geometry_error("geometry write: cannot open " + path);
+    os.write("SPLB", 4);
+    put(os, uint32_t(1));
+    put(os, d.voxel_size);
+    put(os, uint64_t(d.n));
+    put(os, uint32_t(d.iolets.size()));
+    for (const IoletGeo& io : d.iolets) {
+        put(os, uint8_t(io.kind));
+        for (double c : io.center) put(os, c);
+        for (double c : io.normal) put(os, c);
+        put(os, io.radius);
+    }
+    size_t lk = 0;
+    for (uint64_t s = 0; s < d.n; ++s) {
+        for (int a = 0; a < 3; ++a) put(os, d.coords[3 * s + a]);
+        put(os, d.types[s]);
+        for (int i = 1; i < kQ; ++i) {
+            const uint8_t k = d.link_kind[18 * s + uint64_t(i - 1)];
+            put(os, k);
+            if (k >= 2) {
+                while (lk < d.iolet_link_pos.size() && d.iolet_link_pos[lk] < 18 * s + uint64_t(i - 1)) ++lk;
+                uint16_t id = 0;
+                if (lk < d.iolet_link_pos.size() && d.iolet_link_pos[lk] == 18 * s + uint64_t(i - 1))
+                    id = d.iolet_link_id[lk];
+                put(os, id);
+            }
+        }
+    }
+    if (!os) geometry_error("geometry write: stream failure");
+}
+
+Domain read_domain(const std::string& path) {
+    std::ifstream is(path, std::ios::binary);
+    if (!is) geometry_error("geometry load: cannot open " + path);
+    char magic[4];
+    is.read(magic, 4);
+    if (!is || std::memcmp(magic, "SPLB", 4) != 0) geometry_error("geometry load: not a SPLB file");
+    const auto version = get<uint32_t>(is);
+    if (version != 1)
+        geometry_error("geometry load: version mismatch (file has " + std::to_string(version) +
+                       ", expected 1)");
+    Domain d;
+    d.voxel_size = get<double>(is);
+    const auto nsites = get<uint64_t>(is);
+    const auto niolets = get<uint32_t>(is);
+    d.iolets.resize(niolets);
+    for (IoletGeo& io : d.iolets) {
+        const auto kind = get<uint8_t>(is);
+        if (kind > 1) geometry_error("geometry load: bad iolet kind");
+        io.kind = kind;
+        for (double& c : io.center) c = get<double>(is);
+        for (double& c : io.normal) c = get<double>(is);
+        io.radius = get<double>(is);
+    }
+    d.n = nsites;
+    d.coords.resize(3 * nsites);
+    d.types.resize(nsites);
+    d.link_kind.resize(18 * nsites);
+    for (uint64_t s = 0; s < nsites; ++s) {
+        for (int a = 0; a < 3; ++a) d.coords[3 * s + a] = get<int32_t>(is);
+        const auto type = get<uint8_t>(is);
+        if (type >= 6) geometry_error("geometry load: bad collision type");
+        d.types[s] = type;
+        for (int i = 1; i < kQ; ++i) {
+            const auto tag = get<uint8_t>(is);
+            if (tag > 3) geometry_error("geometry load: bad link tag");
+            d.link_kind[18 * s + uint64_t(i - 1)] = tag;
+            if (tag >= 2) {
+                const auto id = get<uint16_t>(is);
+                d.iolet_link_pos.push_back(18 * s + uint64_t(i - 1));
+                d.iolet_link_id.push_back(id);
+            }
+        }
+    }
+    uint64_t pos = 0;
+    for (int t = 0; t < 6; ++t) {
+        d.type_ranges[t][0] = pos;
+        while (pos < d.n && int(d.types[pos]) == t) ++pos;
+        d.type_ranges[t][1] = pos;
+    }
+    validate_domain(d);
+    return d;
+}
+
+// ---- TimeTable (boundary.hpp:18-74) ------------------------------------------
+
+void TimeTable::validate() const {
+    if (t.empty()) config_error("time table: empty table");
+    for (size_t k = 1; k < t.size(); ++k)
+        if (!(t[k] > t[k - 1])) config_error("time table: times must be strictly ascending");
+    if (period != 0.0) {
+        if (!(period > 0.0)) config_error("time table: period must be > 0");
+        if (!(t.back() < period)) config_error("time table: nodes must lie inside one period");
+        if (!(t.front() >= 0.0)) config_error("time table: periodic table starts before t=0");
+    }
+}
+
+double TimeTable::at(double tq) const {
+    if (t.size() == 1 && period == 0.0) return v.front();
+    double tb = tq;
+    if (period > 0.0) {
+        tb = std::fmod(tq, period);
+        if (tb < 0.0) tb += period;
+    }
+    for (size_t k = 0; k < t.size(); ++k)
+        if (tb == t[k]) return v[k];
+    if (period == 0.0) {
+        if (tb <= t.front()) return v.front();
+        if (tb >= t.back()) return v.back();
+    }
+    const size_t after = size_t(std::upper_bound(t.begin(), t.end(), tb) - t.begin());
+    double t0, v0, t1, v1;
+    if (after == 0) {
+        t0 = t.back() - period;
+        v0 = v.back();
+        t1 = t.front();
+        v1 = v.front();
+    } else if (after == t.size()) {
+        t0 = t.back();
+        v0 = v.back();
+        t1 = t.front() + period;
+        v1 = v.front();
+    } else {
+        t0 = t[after - 1];
+        v0 = v[after - 1];
+        t1 = t[after];
+        v1 = v[after];
+    }
+    return v0 + (v1 - v0) * ((tb - t0) / (t1 - t0));
+}
+
+}  // namespace splbcu

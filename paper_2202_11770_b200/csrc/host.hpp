@@ -1,0 +1,131 @@
+// Host-side data model of the B200 engine: sparse domain, site lookup,
+// partition.  Fresh C++ with the reference's semantics; the site order,
+// link tags, decomposition and error texts are the parity contract.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <functional>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "lattice.hpp"
+
+namespace splbcu {
+
+// ---- error taxonomy (reference common.hpp:11-28) -------------------------
+enum class ErrKind { Config = 1, Runtime = 2, Comm = 3, Geometry = 4, Degenerate = 5, Cuda = 6 };
+
+struct Error : std::runtime_error {
+    ErrKind kind;
+    Error(ErrKind k, const std::string& m) : std::runtime_error(m), kind(k) {}
+};
+[[noreturn]] inline void fail(ErrKind k, const std::string& m) { throw Error(k, m); }
+[[noreturn]] inline void geometry_error(const std::string& m) { fail(ErrKind::Geometry, m); }
+[[noreturn]] inline void config_error(const std::string& m) { fail(ErrKind::Config, m); }
+[[noreturn]] inline void runtime_error(const std::string& m) { fail(ErrKind::Runtime, m); }
+
+// ---- small helpers ---------------------------------------------------------
+int hw_threads();
+// Runs fn(begin, end, thread_index) over [0, n) split in contiguous chunks.
+void parallel_for(uint64_t n, const std::function<void(uint64_t, uint64_t, int)>& fn,
+                  uint64_t min_chunk = 1 << 15);
+
+// (z, y, x) lexicographic key: the order sites take inside each collision
+// type (geometry.hpp:189-195).  21 bits per axis with the reference's bias
+// (geometry.hpp:82-86 uses the same bias, x-major; we need z-major).
+constexpr int64_t kBias = int64_t{1} << 20;
+inline uint64_t zyx_key(int32_t x, int32_t y, int32_t z) {
+    return (uint64_t(int64_t(z) + kBias) << 42) | (uint64_t(int64_t(y) + kBias) << 21) |
+           uint64_t(int64_t(x) + kBias);
+}
+
+struct IoletGeo {
+    int32_t kind;  // 0 inlet, 1 outlet
+    double center[3];
+    double normal[3];
+    double radius;
+};
+
+// Link tag per (site, direction i = 1..18) as in geometry.hpp:14-22.  Iolet
+// ids are kept sparsely: only iolet links carry one.
+struct Domain {
+    double voxel_size = 1.0;
+    uint64_t n = 0;
+    std::vector<int32_t> coords;     // 3n, domain order
+    std::vector<uint8_t> types;      // n
+    std::vector<uint8_t> link_kind;  // 18n, [18*s + i-1]
+    // sorted by (site, dir): iolet link -> iolet id
+    std::vector<uint64_t> iolet_link_pos;  // 18*s + i-1
+    std::vector<uint16_t> iolet_link_id;
+    std::vector<IoletGeo> iolets;
+    uint64_t type_ranges[6][2] = {};
+
+    uint16_t link_iolet(uint64_t s, int i) const;  // 0 when not an iolet link
+};
+
+// Lookup of a site by coordinates: sites sorted by zyx key, with a CSR row
+// index over (z, y) when the bounding box allows it.  Used for link closure,
+// decomposition edges and (uploaded to the device) the neighbour table.
+struct SiteIndex {
+    std::vector<uint64_t> keys;   // ascending
+    std::vector<uint32_t> value;  // payload per key (e.g. global site index)
+    int32_t lo[3] = {0, 0, 0}, hi[3] = {-1, -1, -1};
+    bool rows = false;
+    std::vector<uint64_t> row_off;  // (ny*nz + 1) offsets when rows
+    int64_t ny = 0, nz = 0;
+
+    void build_rows();
+    // position in keys of (x,y,z) or -1
+    int64_t find(int32_t x, int32_t y, int32_t z) const;
+};
+
+// Builds the lookup over all sites of a domain (value = global site index).
+SiteIndex index_domain(const Domain& d);
+
+// ---- geometry (geometry.hpp) --------------------------------------------
+Domain classify_sites(const std::vector<int32_t>& voxels, std::vector<IoletGeo> iolets,
+                      double voxel_size);
+void validate_domain(const Domain& d);
+Domain build_pipe(int radius, int length, double voxel_size);
+Domain build_bifurcation(int trunk_radius, int branch_radius, int trunk_length,
+                         int branch_length, double voxel_size);
+Domain build_tree(int root_radius, int root_length, int levels, double radius_ratio,
+                  double length_ratio, double voxel_size);
+Domain build_channel(int nx, int ny, int nz, double voxel_size);
+Domain read_domain(const std::string& path);
+void write_domain(const Domain& d, const std::string& path);
+
+// ---- decomposition (decomp.hpp) ------------------------------------------
+struct WorkerPart {
+    std::vector<uint32_t> sites;  // global indices, worker-local order
+    uint32_t n_edge = 0;
+    uint64_t edge_ranges[6][2] = {};
+    uint64_t mid_ranges[6][2] = {};
+    std::vector<int> neighbors;
+};
+
+struct Partition {
+    int n_workers = 1;
+    int axis = 2;
+    bool slab = true;               // greedy plane split (else contiguous fallback)
+    int32_t plane_lo = 0;           // slab mode: plane coordinate range
+    std::vector<int32_t> plane_owner;  // slab mode: owner per plane (plane_lo + k)
+    std::vector<int32_t> owner;     // per global site
+    std::vector<uint32_t> local_index;
+    std::vector<WorkerPart> parts;
+    double imbalance() const;
+};
+
+Partition partition(const Domain& d, int n_workers, const SiteIndex* index = nullptr);
+
+// ---- time tables (boundary.hpp:18-74) ------------------------------------
+struct TimeTable {
+    std::vector<double> t, v;
+    double period = 0.0;
+    void validate() const;
+    double at(double tq) const;
+};
+
+}  // namespace splbcu

@@ -1,0 +1,162 @@
+// sm_100a kernels of the sparse D3Q19 LBM step.
+//
+// Data layout in HBM (per worker):
+//   f_old / f_new : 19 direction planes of P doubles (P = n_local rounded up
+//                   to 64 sites, 512 B), then the totalSharedFs tail
+//                   (reference layout.hpp:47-53 with a padded plane pitch).
+//   tab           : 18 direction planes of P u32 — the push destination of
+//                   (site s, direction i) as the neighbour's site index
+//                   (ToLocal), or a tagged special entry (bounce-back,
+//                   shared slot, iolet).  Direction-major so a warp's 32
+//                   lanes read 128 contiguous bytes per direction.
+// Site order inside a worker: edge group then mid group (decomp.hpp:155-186),
+// each split into a plain range (Inner+Wall merged in (z,y,x) order, so row
+// neighbours are adjacent and scattered writes coalesce) and an iolet range.
+#pragma once
+
+#include <cstdint>
+
+#include "lattice.hpp"
+
+namespace splbcu {
+
+constexpr uint32_t kSpecial = 0x80000000u;
+constexpr uint32_t kOpShift = 29;
+constexpr uint32_t kPayload = (1u << 29) - 1;
+constexpr uint32_t kOpBounce = 0, kOpShared = 1, kOpIolet = 2;
+
+struct IoletDev {
+    double center[3];
+    double normal[3];
+    double radius;
+    int32_t is_velocity;
+    int32_t pad;
+};
+
+#if defined(__CUDACC__)
+
+// Streaming loads: each f_old / tab element is read once per step.
+__device__ __forceinline__ double ld_f(const double* p) { return __ldcs(p); }
+__device__ __forceinline__ uint32_t ld_t(const uint32_t* p) { return __ldcs(p); }
+
+// Value streamed into (s, inverse(i)) by an iolet link i (engine.hpp:385-402).
+__device__ __forceinline__ double iolet_link_value(int i, double fpost, const Macro& m,
+                                                   const IoletDev& g, double staged,
+                                                   int x, int y, int z) {
+    if (g.is_velocity) {
+        const double sw = staged * iolet_weight(g.center, g.normal, g.radius, x, y, z);
+        const double ub0 = g.normal[0] * sw, ub1 = g.normal[1] * sw, ub2 = g.normal[2] * sw;
+        return fpost - ladd_term(i, m.rho, ub0, ub1, ub2);
+    }
+    const double un = (m.ux * g.normal[0] + m.uy * g.normal[1]) + m.uz * g.normal[2];
+    return feq_one(inv(i), staged, g.normal[0] * un, g.normal[1] * un, g.normal[2] * un);
+}
+
+struct IoletArgs {
+    const IoletDev* io;
+    const double* staged;    // this step's per-iolet value (speed or ghost density)
+    const int32_t* coords;   // 3 ints per site of this launch's range, [s - begin]
+};
+
+// Fused collide + push-stream over sites [begin, end) (update_push,
+// engine.hpp:404-433).  One thread per site.
+template <bool kIolets>
+__global__ void __launch_bounds__(256)
+lbm_push(const double* __restrict__ fo, double* __restrict__ fn, const uint32_t* __restrict__ tab,
+         uint64_t P, uint32_t begin, uint32_t end, double omega, IoletArgs ia) {
+    const uint32_t s = begin + blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= end) return;
+    double f[kQ];
+#pragma unroll
+    for (int i = 0; i < kQ; ++i) f[i] = ld_f(fo + uint64_t(i) * P + s);
+    uint32_t t[kQ - 1];
+#pragma unroll
+    for (int i = 0; i < kQ - 1; ++i) t[i] = ld_t(tab + uint64_t(i) * P + s);
+
+    const Macro m = macro_of(f);
+    double feq[kQ];
+    feq_all(m.rho, m.ux, m.uy, m.uz, feq);
+    fn[s] = relax(f[0], feq[0], omega);
+#pragma unroll
+    for (int i = 1; i < kQ; ++i) {
+        double fpost = relax(f[i], feq[i], omega);
+        const uint32_t v = t[i - 1];
+        uint64_t dst;
+        if (v < kSpecial) {
+            dst = uint64_t(i) * P + v;
+        } else {
+            const uint32_t op = (v >> kOpShift) & 3u;
+            if (op == kOpShared) {
+                dst = uint64_t(kQ) * P + (v & kPayload);
+            } else {
+                dst = uint64_t(inv(i)) * P + s;
+                if constexpr (kIolets) {
+                    if (op == kOpIolet) {
+                        const uint32_t k = v & kPayload;
+                        const int32_t* c = ia.coords + 3 * uint64_t(s - begin);
+                        fpost = iolet_link_value(i, fpost, m, ia.io[k], ia.staged[k], c[0], c[1], c[2]);
+                    }
+                }
+            }
+        }
+        fn[dst] = fpost;
+    }
+}
+
+// PostReceive re-allocation (engine.hpp:534-542): fn[recv_dest[k]] = fo[tail + k].
+__global__ void lbm_post_receive(const double* __restrict__ fo_tail, double* __restrict__ fn,
+                                 const uint64_t* __restrict__ recv_flat, uint32_t n) {
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n) fn[recv_flat[k]] = fo_tail[k];
+}
+
+// f_old = equilibrium(rho0, 0) (engine.hpp:254-259); eq computed on the host.
+struct Eq19 {
+    double v[kQ];
+};
+__global__ void lbm_init_equilibrium(double* __restrict__ f, uint64_t P, uint32_t n, Eq19 eq) {
+    const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+#pragma unroll
+    for (int i = 0; i < kQ; ++i) f[uint64_t(i) * P + s] = eq.v[i];
+}
+
+// Moments of every site (fields_of_worker, engine.hpp:583-597), internal order.
+__global__ void lbm_capture_moments(const double* __restrict__ f, uint64_t P, uint32_t n,
+                                    double* __restrict__ out4) {
+    const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    double fl[kQ];
+#pragma unroll
+    for (int i = 0; i < kQ; ++i) fl[i] = f[uint64_t(i) * P + s];
+    const Macro m = macro_of(fl);
+    double* o = out4 + 4 * uint64_t(s);
+    o[0] = m.rho;
+    o[1] = m.ux;
+    o[2] = m.uy;
+    o[3] = m.uz;
+}
+
+// Per iolet boundary site: |u|, cs2*rho, u.n (record_observation,
+// engine.hpp:557-581).  One row of n_obs triples.
+__global__ void lbm_iolet_observe(const double* __restrict__ f, uint64_t P, uint32_t n_obs,
+                                  const uint32_t* __restrict__ obs_site,
+                                  const uint16_t* __restrict__ obs_iolet,
+                                  const IoletDev* __restrict__ io, double* __restrict__ out_row) {
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n_obs) return;
+    const uint32_t s = obs_site[j];
+    double fl[kQ];
+#pragma unroll
+    for (int i = 0; i < kQ; ++i) fl[i] = f[uint64_t(i) * P + s];
+    const Macro m = macro_of(fl);
+    const IoletDev& g = io[obs_iolet[j]];
+    double* o = out_row + 3 * uint64_t(j);
+    o[0] = sqrt((m.ux * m.ux + m.uy * m.uy) + m.uz * m.uz);
+    o[1] = kCs2 * m.rho;
+    o[2] = (m.ux * g.normal[0] + m.uy * g.normal[1]) + m.uz * g.normal[2];
+}
+
+#endif  // __CUDACC__
+
+}  // namespace splbcu

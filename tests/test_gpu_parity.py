@@ -1,0 +1,190 @@
+"""Parity of the B200 engine (sm_100a kernels, device-built tables) with the
+reference, through the C-ABI.  Bar: bit-exact tables/decomposition and
+bit-exact f/rho/u (== semantics: -0.0 == +0.0) — the engine compiles with
+--fmad=false and restates the reference's expression trees, so the FP64
+tolerance stated in BASELINE (1e-12 relative) is not needed; the tests
+assert equality and would report the max deviation if it ever appeared."""
+import numpy as np
+import pytest
+
+import cases
+
+pytestmark = pytest.mark.gpu
+
+FAST_RUNS = [k for k in cases.RUNS]
+
+
+@pytest.mark.parametrize("key", sorted(cases.MAP_CASES))
+def test_device_table_bit_exact(product, golden, key):
+    run = cases.MAP_CASES[key]
+    d = cases.make_domain(product, cases.DOMAINS[run["domain"]])
+    s = product.Simulation(d, cases.make_bcs(product, run["bcs"]),
+                           product.EngineParams(workers=run["W"], layout=run["layout"]))
+    assert [cases.map_digest(s.map(w)) for w in range(run["W"])] == golden["maps"][key]
+
+
+@pytest.mark.parametrize("key", FAST_RUNS)
+def test_runs_bit_exact(product, golden, golden_arrays, key):
+    res = cases.execute_run(product, cases.RUNS[key])
+    want = golden["runs"][key]
+    got = cases.run_digest(res)
+    arr = golden_arrays.get(f"run_{key}_snapshot")
+    if got["snapshot"] != want["snapshot"] and arr is not None:
+        dev = np.max(np.abs(res["snapshot"] - arr) / np.maximum(np.abs(arr), 1e-300))
+        pytest.fail(f"snapshot differs from the reference, max rel deviation {dev:.3e}")
+    assert got == want
+
+
+def test_live_reference_random_case(product, reference):
+    """A case outside the golden set, against the reference run live."""
+    run = dict(domain="bif_3_2_6_8", bcs=("bif", "bif_inlet"), tau=0.7, dt=2e-3, W=3, layout=1, steps=30,
+               capture=10, observe=True, noise=(7, 0.01))
+    a = cases.execute_run(product, run)
+    b = cases.execute_run(reference, run)
+    assert cases.run_digest(a) == cases.run_digest(b)
+
+
+def test_partition_invariance_many_workers(product):
+    """1 vs 2/4/7 workers bitwise (test_engine.cpp:302-315)."""
+    d = product.build_pipe(5, 40)
+    bcs = cases.make_bcs(product, ("pressure", 0.34, cases.CS2))
+    snaps = []
+    for W in (1, 2, 4, 7):
+        s = product.Simulation(d, bcs, product.EngineParams(tau=0.8, workers=W, capture_period=25))
+        s.run(50)
+        snaps.append(s.snapshot_fields())
+    for x in snaps[1:]:
+        assert np.array_equal(x, snaps[0])
+
+
+def test_fixed_point_closed_box(product):
+    """test_engine.cpp:69-78"""
+    d = product.classify_sites(cases.closed_box(6), [])
+    s = product.Simulation(d, product.BCSet([]), product.EngineParams(tau=0.8))
+    before = s.snapshot_fields()
+    s.run(50)
+    assert np.max(np.abs(s.snapshot_fields() - before)) <= 1e-13
+
+
+def test_locality_one_link_per_step(product):
+    """test_engine.cpp:80-119"""
+    d = product.classify_sites(cases.closed_box(9), [])
+    e = d.export()
+    ref = product.Simulation(d, product.BCSet([]), product.EngineParams(tau=0.8))
+    poke = product.Simulation(d, product.BCSet([]), product.EngineParams(tau=0.8))
+    center = int(np.where((e["coords"] == [4, 4, 4]).all(1))[0][0])
+    lc = poke.assignment().local_index[center]
+    st = poke.store(0)
+    f = st.f_old()
+    f[st.idx(lc, 3)] += 0.01
+    st.set_f_old(f)
+    ref.run(1)
+    poke.run(1)
+    a, b = ref.snapshot_fields().reshape(-1, 4), poke.snapshot_fields().reshape(-1, 4)
+    changed = np.where((a != b).any(1))[0]
+    assert 1 < len(changed) <= 19
+    dc = np.abs(e["coords"][changed] - 4)
+    assert (dc <= 1).all() and (dc.sum(1) <= 2).all()
+
+
+def test_capture_schedule_and_rest(product):
+    """test_engine.cpp:140-192"""
+    d = product.build_pipe(3, 8)
+    bcs = cases.make_bcs(product, ("pressure", cases.CS2, cases.CS2))
+    s = product.Simulation(d, bcs, product.EngineParams(tau=0.8, capture_period=100))
+    f = s.snapshot_fields().reshape(-1, 4)
+    assert np.all(np.abs(f[:, 0] - 1.0) <= 1e-15) and np.all(f[:, 1:] == 0.0)
+    s.run(0)
+    c = s.cache()
+    assert len(c) == 1 and c[0].step == 0 and np.array_equal(c[0].fields, f.ravel())
+    s.run(201)
+    assert np.max(np.abs(s.snapshot_fields().reshape(-1, 4)[:, 1:])) <= 1e-10
+    s2 = product.Simulation(product.build_pipe(2, 4), bcs, product.EngineParams(tau=0.8, capture_period=100))
+    s2.run(250)
+    assert [c.step for c in s2.cache()] == [0, 100, 200]
+
+
+def test_repeated_runs_continue(product, reference):
+    """run() may be called repeatedly; captures/series continue (engine.hpp:155-197)."""
+    outs = []
+    for M in (product, reference):
+        d = M.build_pipe(3, 8)
+        s = M.Simulation(d, cases.make_bcs(M, ("pressure", 0.34, cases.CS2)),
+                         M.EngineParams(tau=0.8, workers=2, capture_period=7, observe_iolets=True))
+        for n in (5, 0, 9, 11):
+            s.run(n)
+        outs.append((s.snapshot_fields(), [(c.step, cases.h(c.fields)) for c in s.cache()],
+                     {k: [cases.h(a) for a in v] for k, v in s.series().items() if k != "rows"}, s.steps_run()))
+    assert cases.h(outs[0][0]) == cases.h(outs[1][0])
+    assert outs[0][1:] == outs[1][1:]
+
+
+def test_store_roundtrip_layouts(product):
+    d = product.build_bifurcation(3, 2, 6, 8)
+    for lay in (product.AOS, product.SOA):
+        s = product.Simulation(d, cases.make_bcs(product, ("bif", "bif_inlet")),
+                               product.EngineParams(tau=0.8, workers=3, layout=lay))
+        for w in range(3):
+            st = s.store(w)
+            x = np.random.default_rng(w).uniform(0, 1, st.total_size())
+            st.set_f_old(x)
+            assert np.array_equal(st.f_old(), x)
+
+
+def test_multi_device_placement_single_gpu(product):
+    """Workers placed round-robin on the device list; with one device all
+    share it and exchange by device-to-device copies."""
+    d = product.build_pipe(4, 20)
+    bcs = cases.make_bcs(product, ("pressure", 0.3383333333333333, cases.CS2))
+    a = product.Simulation(d, bcs, product.EngineParams(tau=0.8, workers=4, devices=[0, 0]))
+    b = product.Simulation(d, bcs, product.EngineParams(tau=0.8, workers=1))
+    a.run(30)
+    b.run(30)
+    assert np.array_equal(a.snapshot_fields(), b.snapshot_fields())
+
+
+def test_velocity_pipe_centerline(product):
+    """test_engine.cpp:370-401: velocity-driven pipe reaches the imposed
+    centreline speed within 3% (R=8)."""
+    R, Len, u0 = 8, 64, 0.04
+    d = product.build_pipe(R, Len)
+    bcs = cases.make_bcs(product, ("velocity_const", u0))
+    s = product.Simulation(d, bcs, product.EngineParams(tau=0.9, workers=2))
+    e = d.export()
+    mid = np.where(e["coords"][:, 2] == Len // 2)[0]
+    r2 = (e["coords"][mid, 0] - 0.375) ** 2 + (e["coords"][mid, 1] - 0.5) ** 2
+    cidx = mid[np.argmin(r2)]
+    q_prev = 0.0
+    for _ in range(60):
+        s.run(250)
+        f = s.snapshot_fields().reshape(-1, 4)
+        q = f[mid, 3].sum()
+        if abs(q - q_prev) < 1e-7 * abs(q):
+            break
+        q_prev = q
+    assert abs(f[cidx, 3] - u0) / u0 <= 0.03
+
+
+def test_engine_rejects_bad_setup(product):
+    d = product.build_pipe(3, 8)
+    with pytest.raises(product.ConfigError, match="configured for 1 iolets"):
+        product.Simulation(d, product.BCSet([product.BCEntry(product.PRESSURE, product.TimeTable.constant(0.3))]),
+                           product.EngineParams())
+    with pytest.raises(product.ConfigError, match="tau must exceed 0.5"):
+        product.Simulation(d, cases.make_bcs(product, ("pressure", 0.3, 0.3)), product.EngineParams(tau=0.5))
+    with pytest.raises(product.ConfigError, match="ghost density must stay positive"):
+        product.Simulation(d, cases.make_bcs(product, ("pressure", -0.3, 0.3)), product.EngineParams())
+    with pytest.raises(product.Error, match="exceeds site count"):
+        product.Simulation(product.classify_sites(cases.closed_box(2), []), product.BCSet([]),
+                           product.EngineParams(workers=9))
+
+
+def test_kernel_timing_counts(product):
+    d = product.build_pipe(8, 64)
+    s = product.Simulation(d, cases.make_bcs(product, ("pressure", cases.CS2, cases.CS2)), product.EngineParams())
+    s.set_kernel_timing(True)
+    s.run(10)
+    secs, launches, sites = s.kernel_stats()
+    assert launches == 10 and secs > 0.0
+    e = d.export()["type_ranges"]
+    assert sites == 10 * int(e[1][1])  # Inner + Wall sites per step
