@@ -33,6 +33,7 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 BYTES_PER_SITE = 19 * 8 + 19 * 8 + 18 * 4  # 376
 CS2 = 1.0 / 3.0
@@ -173,6 +174,7 @@ def main():
     ap.add_argument("--workload", default=None)
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--quick", action="store_true", help="kernel-only number (tuning runs)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -223,12 +225,14 @@ def main():
     barrier()
     sim.set_kernel_timing(True)
     k0 = sim.kernel_stats()
+    l0 = sim.launch_count()
     d0 = sim.device_loop_seconds()
     with ClockSampler(local) as clk:
         sim.run(args.steps)  # run() syncs its streams before returning
     barrier()
     dev_s = max_over_ranks(sim.device_loop_seconds() - d0)
     k1 = sim.kernel_stats()
+    launches = sim.launch_count() - l0
     sim.set_kernel_timing(False)
     value = n * args.steps / dev_s / 1e6
     ks, kl, kn = k1[0] - k0[0], k1[1] - k0[1], k1[2] - k0[2]
@@ -241,6 +245,10 @@ def main():
             "peak_source": src, "kernel": "lbm_push<false> (Inner+Wall fused collide+stream)",
             "bytes_per_site": BYTES_PER_SITE, "kernel_share": ks / dev_s if dev_s else None}
 
+    if args.quick:
+        if rank == 0:
+            print(json.dumps({"value": value, "roofline": roof, "launches": launches, "clocks": clk.summary()}))
+        return
     # e2e through the public API: run(1) per step with the iolet series on
     sim.close()
     params_e = P.EngineParams(workers=world, devices=[local], observe_iolets=True, **p)
@@ -285,7 +293,7 @@ def main():
                            "l2": "inputs (f, table) 3.8 GB per step >> 126 MB L2; no flush needed",
                            "setup_s": round(setup_s, 2)},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": int(kl + kl * 0 + (args.steps * (1 if len(bcs.entries) else 0))),
+                "gpu_launches": int(launches),
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     if world > 1:

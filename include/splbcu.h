@@ -238,6 +238,8 @@ int splbcu_sim_series(const splbcu_sim* s, uint32_t iolet, double* max_speed,
 int splbcu_sim_set_kernel_timing(splbcu_sim* s, int32_t on);
 int splbcu_sim_kernel_stats(const splbcu_sim* s, double* plain_seconds,
                             uint64_t* plain_launches, uint64_t* plain_sites);
+/* Number of kernels this handle launched inside run() so far. */
+uint64_t splbcu_sim_launch_count(const splbcu_sim* s);
 void splbcu_sim_destroy(splbcu_sim* s);
 
 #ifdef __cplusplus

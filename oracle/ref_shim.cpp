@@ -384,6 +384,7 @@ int splbcu_sim_kernel_stats(const splbcu_sim*, double* a, uint64_t* b, uint64_t*
     if (c) *c = 0;
     return 0;
 }
+uint64_t splbcu_sim_launch_count(const splbcu_sim*) { return 0; }
 void splbcu_sim_destroy(splbcu_sim* s) { delete s; }
 
 }  // extern "C"

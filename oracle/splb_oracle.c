@@ -1202,6 +1202,10 @@ int splbcu_sim_kernel_stats(const splbcu_sim* S, double* a, uint64_t* b, uint64_
     if (c) *c = 0;
     return 0;
 }
+uint64_t splbcu_sim_launch_count(const splbcu_sim* S) {
+    (void)S;
+    return 0;
+}
 void splbcu_sim_destroy(splbcu_sim* S) {
     if (!S) return;
     for (int w = 0; w < S->part->W; ++w) {

@@ -9,6 +9,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <chrono>
 #include <cstring>
 #include <map>
@@ -144,18 +145,25 @@ __global__ void build_links(uint32_t n, uint64_t P, const int32_t* __restrict__ 
             out_vals[p] = tpos;
             tab[tpos] = kSpecial | (kOpShared << kOpShift);
         }
-        // incoming partner: the site at x - c_i streams into (s, i)
+    } else if (k == 1) {
+        tab[tpos] = kSpecial | (kOpBounce << kOpShift);
+    } else {
+        tab[tpos] = kSpecial | (kOpIolet << kOpShift);  // id patched below
+    }
+    // Incoming partner: the fluid site at x - c_i (this site's link inv(i)
+    // is Fluid) streams into (s, i); record it when another worker owns it.
+    if (kind[18 * uint64_t(s) + uint64_t(inv(i) - 1)] == 0) {
         const int64_t src = d_find(L, x - cx(i), y - cy(i), z - cz(i));
-        if (src >= 0 && L.owner[src] != w) {
+        if (src < 0) {
+            atomicExch(err, 1u);
+            return;
+        }
+        if (L.owner[src] != w) {
             const unsigned p = atomicAdd(n_in, 1u);
             in_keys[p] = (static_cast<unsigned long long>(L.owner[src]) << 40) |
                          (static_cast<unsigned long long>(L.global[src]) * 18ull + unsigned(i - 1));
             in_vals[p] = uint64_t(i) * P + s;
         }
-    } else if (k == 1) {
-        tab[tpos] = kSpecial | (kOpBounce << kOpShift);
-    } else {
-        tab[tpos] = kSpecial | (kOpIolet << kOpShift);  // id patched below
     }
 }
 
@@ -225,7 +233,7 @@ class Engine {
     std::vector<std::vector<std::pair<int, uint32_t>>> obs_order;  // per iolet: (worker, pos)
     uint64_t steps_run = 0;
     double loop_s = 0.0, dev_loop_s = 0.0, plain_s = 0.0;
-    uint64_t plain_launches = 0, plain_sites = 0;
+    uint64_t plain_launches = 0, plain_sites = 0, launches = 0;
     bool kernel_timing = false;
     std::vector<IoletDev> io_host;
 
@@ -591,13 +599,37 @@ class Engine {
     }
 
     // ---- stepping -----------------------------------------------------------
+    // Launch-shape variants of the plain kernel (SPLBCU_PLAIN_VARIANT picks
+    // one for tuning; the default is the measured best).
+    int plain_variant = [] {
+        const char* v = getenv("SPLBCU_PLAIN_VARIANT");
+        return v ? atoi(v) : 0;
+    }();
+    template <int T, int B>
+    void launch_plain_t(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia) {
+        lbm_push<false, T, B><<<unsigned((e - b + T - 1) / T), T, 0, s>>>(wk.f_old(), wk.f_new(),
+                                                                          wk.tab.get<uint32_t>(), wk.P, b, e, omega, ia);
+    }
+    void launch_plain(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia) {
+        switch (plain_variant) {
+            case 1: launch_plain_t<256, 1>(wk, s, b, e, ia); break;
+            case 2: launch_plain_t<256, 2>(wk, s, b, e, ia); break;
+            case 3: launch_plain_t<128, 4>(wk, s, b, e, ia); break;
+            case 4: launch_plain_t<128, 5>(wk, s, b, e, ia); break;
+            case 5: launch_plain_t<64, 8>(wk, s, b, e, ia); break;
+            case 6: launch_plain_t<256, 3>(wk, s, b, e, ia); break;
+            default: launch_plain_t<128, 4>(wk, s, b, e, ia); break;
+        }
+    }
+
     void launch_range(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, bool iolet, const double* staged,
                       const int32_t* coords) {
         if (e <= b) return;
         IoletArgs ia{wk.io_geo.get<IoletDev>(), staged, coords};
         const unsigned nb = blocks_for(e - b);
         if (iolet) {
-            lbm_push<true><<<nb, 256, 0, s>>>(wk.f_old(), wk.f_new(), wk.tab.get<uint32_t>(), wk.P, b, e, omega, ia);
+            lbm_push<true, 256, 1><<<nb, 256, 0, s>>>(wk.f_old(), wk.f_new(), wk.tab.get<uint32_t>(), wk.P, b, e,
+                                                      omega, ia);
         } else {
             cudaEvent_t e0 = nullptr, e1 = nullptr;
             if (kernel_timing) {
@@ -612,11 +644,12 @@ class Engine {
                 e1 = wk.tev[wk.tev_used++];
                 CK(cudaEventRecord(e0, s));
             }
-            lbm_push<false><<<nb, 256, 0, s>>>(wk.f_old(), wk.f_new(), wk.tab.get<uint32_t>(), wk.P, b, e, omega, ia);
+            launch_plain(wk, s, b, e, ia);
             if (kernel_timing) CK(cudaEventRecord(e1, s));
             plain_launches++;
             plain_sites += e - b;
         }
+        launches++;
         CK(cudaGetLastError());
     }
 
@@ -658,6 +691,7 @@ class Engine {
         if (!wk.shared) return;
         lbm_post_receive<<<blocks_for(wk.shared), 256, 0, wk.sE>>>(
             wk.f_old() + uint64_t(kQ) * wk.P, wk.f_new(), wk.recv_flat.get<uint64_t>(), wk.shared);
+        launches++;
         CK(cudaGetLastError());
     }
 
@@ -666,6 +700,7 @@ class Engine {
         double* out = wk.obs_buf.get<double>() + 3 * (row - wk.obs_row_base) * wk.n_obs;
         lbm_iolet_observe<<<blocks_for(wk.n_obs), 256, 0, s>>>(f, wk.P, wk.n_obs, wk.obs_site.get<uint32_t>(),
                                                                wk.obs_iolet.get<uint16_t>(), wk.io_geo.get<IoletDev>(), out);
+        launches++;
         CK(cudaGetLastError());
     }
 
@@ -676,6 +711,7 @@ class Engine {
         if (!c) return;
         if (wk.n)
             lbm_capture_moments<<<blocks_for(wk.n), 256, 0, s>>>(f, wk.P, wk.n, wk.cap4.get<double>());
+        launches++;
         CK(cudaGetLastError());
         std::vector<double> h(4 * uint64_t(wk.n));
         if (wk.n) CK(cudaMemcpyAsync(h.data(), wk.cap4.get<double>(), h.size() * 8, cudaMemcpyDeviceToHost, s));
@@ -1049,6 +1085,7 @@ double Simulation::plain_kernel_seconds() const { return e_->plain_s; }
 uint64_t Simulation::plain_kernel_launches() const { return e_->plain_launches; }
 uint64_t Simulation::plain_kernel_sites() const { return e_->plain_sites; }
 void Simulation::set_kernel_timing(bool on) { e_->kernel_timing = on; }
+uint64_t Simulation::launch_count() const { return e_->launches; }
 void Simulation::snapshot(double* out) { e_->snapshot(out); }
 int Simulation::n_workers() const { return e_->prm.workers; }
 bool Simulation::is_local(int w) const {

@@ -60,8 +60,8 @@ struct IoletArgs {
 
 // Fused collide + push-stream over sites [begin, end) (update_push,
 // engine.hpp:404-433).  One thread per site.
-template <bool kIolets>
-__global__ void __launch_bounds__(256)
+template <bool kIolets, int kThreads, int kMinBlocks>
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
 lbm_push(const double* __restrict__ fo, double* __restrict__ fn, const uint32_t* __restrict__ tab,
          uint64_t P, uint32_t begin, uint32_t end, double omega, IoletArgs ia) {
     const uint32_t s = begin + blockIdx.x * blockDim.x + threadIdx.x;

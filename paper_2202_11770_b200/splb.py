@@ -476,6 +476,9 @@ class Simulation:
         _check(lib.splbcu_sim_kernel_stats(self._h, C.byref(s), C.byref(n), C.byref(sites)))
         return s.value, n.value, sites.value
 
+    def launch_count(self) -> int:
+        return int(lib.splbcu_sim_launch_count(self._h))
+
     def snapshot_fields(self) -> np.ndarray:
         out = np.zeros(4 * self.domain_.n_sites())
         _check(lib.splbcu_sim_snapshot(self._h, _ptr(out, C.c_double)))
