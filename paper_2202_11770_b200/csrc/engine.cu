@@ -44,6 +44,8 @@ std::string nccl_unique_id(void* out128) {
     return {};
 }
 
+constexpr uint64_t kTilePad = 256;  // tail pad so the last TMA tile stays in bounds
+
 namespace {
 
 struct DevMem {
@@ -459,8 +461,8 @@ class Engine {
             L.hi2 = lix.hi[2];
             L.ny = lix.ny;
         }
-        uint32_t* tab = wk.tab.alloc<uint32_t>(18 * wk.P);
-        CK(cudaMemsetAsync(tab, 0, 18 * wk.P * sizeof(uint32_t), s));
+        uint32_t* tab = wk.tab.alloc<uint32_t>(18 * wk.P + kTilePad);
+        CK(cudaMemsetAsync(tab, 0, (18 * wk.P + kTilePad) * sizeof(uint32_t), s));
         const uint64_t cap = 18 * uint64_t(wk.n_edge) + 1;
         DevMem ok_, ov_, ik_, iv_, cnt, ok2, ov2, ik2, iv2;
         auto* okeys = ok_.alloc<unsigned long long>(cap);
@@ -529,8 +531,8 @@ class Engine {
 
         // distribution store, f_old = equilibrium(rho0, 0) (engine.hpp:243-260)
         for (int b = 0; b < 2; ++b) {
-            double* f = wk.fbuf[b].alloc<double>(wk.fsize());
-            CK(cudaMemsetAsync(f, 0, wk.fsize() * sizeof(double), s));
+            double* f = wk.fbuf[b].alloc<double>(wk.fsize() + kTilePad);
+            CK(cudaMemsetAsync(f, 0, (wk.fsize() + kTilePad) * sizeof(double), s));
         }
         wk.old = 0;
         Eq19 eq;
@@ -618,8 +620,35 @@ class Engine {
             case 4: launch_plain_t<128, 5>(wk, s, b, e, ia); break;
             case 5: launch_plain_t<64, 8>(wk, s, b, e, ia); break;
             case 6: launch_plain_t<256, 3>(wk, s, b, e, ia); break;
+            case 10: launch_tma<128, 3, 2>(wk, s, b, e); break;
+            case 11: launch_tma<128, 2, 3>(wk, s, b, e); break;
+            case 12: launch_tma<64, 3, 4>(wk, s, b, e); break;
+            case 13: launch_tma<256, 2, 1>(wk, s, b, e); break;
+            case 14: launch_tma<128, 4, 1>(wk, s, b, e); break;
+            case 15: launch_tma<64, 4, 3>(wk, s, b, e); break;
             default: launch_plain_t<128, 4>(wk, s, b, e, ia); break;
         }
+    }
+
+    // Persistent TMA-pipelined launch: grid = resident CTAs (occupancy x SMs).
+    template <int T, int S, int B>
+    void launch_tma(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e) {
+        using Lm = PushTmaSmem<T, S>;
+        static int cfg_dev = -1, resident = 0;
+        if (cfg_dev != wk.dev) {
+            CK(cudaFuncSetAttribute(lbm_push_tma<T, S, B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(Lm::kBytes)));
+            int per_sm = 0, sms = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lbm_push_tma<T, S, B>, T, Lm::kBytes));
+            CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, wk.dev));
+            resident = std::max(1, per_sm) * sms;
+            cfg_dev = wk.dev;
+        }
+        const uint32_t base = b & ~3u;
+        const uint32_t ntiles = (e - base + T - 1) / T;
+        const unsigned grid = unsigned(std::min<uint32_t>(ntiles, uint32_t(resident)));
+        lbm_push_tma<T, S, B><<<grid, T, Lm::kBytes, s>>>(wk.f_old(), wk.f_new(), wk.tab.get<uint32_t>(), wk.P, b, e,
+                                                           omega);
     }
 
     void launch_range(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, bool iolet, const double* staged,

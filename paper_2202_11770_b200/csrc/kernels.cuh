@@ -103,6 +103,128 @@ lbm_push(const double* __restrict__ fo, double* __restrict__ fn, const uint32_t*
     }
 }
 
+// ---- TMA-pipelined persistent variant -------------------------------------
+// The plain-site kernel is bound by HBM latency (ncu: long-scoreboard stalls
+// dominate at the register-limited occupancy).  This version decouples loads
+// from compute: a persistent CTA walks tiles of T sites; one thread streams
+// the tile's 19 f-plane segments and 18 table-plane segments into shared
+// memory with 1-D bulk async copies (cp.async.bulk, the TMA engine) completing
+// on an mbarrier, S stages deep, while the CTA's threads collide+stream the
+// previous tile from shared memory and scatter their 19 results to HBM.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t evict_first_policy() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
+template <int T, int S>
+struct PushTmaSmem {
+    static constexpr uint32_t kF = uint32_t(kQ) * T * 8;        // f tile
+    static constexpr uint32_t kT = uint32_t(kQ - 1) * T * 4;    // table tile
+    static constexpr uint32_t kStage = kF + kT;
+    static constexpr uint32_t kBytes = S * kStage + S * 8;
+};
+
+// Sites [begin, end) of the plain (Inner+Wall) range.  Tiles start at
+// begin rounded down to 4 sites (16-byte bulk-copy alignment); sites outside
+// the range are loaded but neither computed nor stored.  Buffers carry a
+// tail pad of T elements so the last tile's copies stay in bounds.
+template <int T, int S, int kMinBlocks>
+__global__ void __launch_bounds__(T, kMinBlocks)
+lbm_push_tma(const double* __restrict__ fo, double* __restrict__ fn, const uint32_t* __restrict__ tab,
+             uint64_t P, uint32_t begin, uint32_t end, double omega) {
+    using L = PushTmaSmem<T, S>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S * L::kStage);
+    const uint32_t base = begin & ~3u;
+    const uint32_t ntiles = (end - base + T - 1) / T;
+    const uint32_t G = gridDim.x;
+    const uint32_t tid = threadIdx.x;
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) mbar_init(&bar[s], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    const uint64_t policy = evict_first_policy();
+    auto issue = [&](uint32_t k) {
+        const uint32_t tile = blockIdx.x + k * G;
+        if (tile >= ntiles) return;
+        const int st = int(k % S);
+        unsigned char* buf = smem + st * L::kStage;
+        const uint64_t t0 = uint64_t(base) + uint64_t(tile) * T;
+        mbar_expect_tx(&bar[st], L::kStage);
+#pragma unroll 1
+        for (int i = 0; i < kQ; ++i) bulk_g2s(buf + i * T * 8, fo + uint64_t(i) * P + t0, T * 8, &bar[st], policy);
+#pragma unroll 1
+        for (int i = 0; i < kQ - 1; ++i)
+            bulk_g2s(buf + L::kF + i * T * 4, tab + uint64_t(i) * P + t0, T * 4, &bar[st], policy);
+    };
+    if (tid == 0)
+        for (uint32_t k = 0; k + 1 < uint32_t(S); ++k) issue(k);
+    for (uint32_t k = 0;; ++k) {
+        const uint32_t tile = blockIdx.x + k * G;
+        if (tile >= ntiles) break;
+        if (tid == 0) issue(k + S - 1);
+        const int st = int(k % S);
+        mbar_wait(&bar[st], (k / S) & 1u);
+        const double* fs = reinterpret_cast<const double*>(smem + st * L::kStage);
+        const uint32_t* ts = reinterpret_cast<const uint32_t*>(smem + st * L::kStage + L::kF);
+        const uint32_t s = base + tile * T + tid;
+        if (s >= begin && s < end) {
+            double f[kQ];
+#pragma unroll
+            for (int i = 0; i < kQ; ++i) f[i] = fs[i * T + tid];
+            const Macro m = macro_of(f);
+            double feq[kQ];
+            feq_all(m.rho, m.ux, m.uy, m.uz, feq);
+            fn[s] = relax(f[0], feq[0], omega);
+#pragma unroll
+            for (int i = 1; i < kQ; ++i) {
+                const double fpost = relax(f[i], feq[i], omega);
+                const uint32_t v = ts[(i - 1) * T + tid];
+                uint64_t dst;
+                if (v < kSpecial) dst = uint64_t(i) * P + v;
+                else if (((v >> kOpShift) & 3u) == kOpShared) dst = uint64_t(kQ) * P + (v & kPayload);
+                else dst = uint64_t(inv(i)) * P + s;
+                fn[dst] = fpost;
+            }
+        }
+        __syncthreads();  // stage st is free for the copy issued next iteration
+    }
+}
+
 // PostReceive re-allocation (engine.hpp:534-542): fn[recv_dest[k]] = fo[tail + k].
 __global__ void lbm_post_receive(const double* __restrict__ fo_tail, double* __restrict__ fn,
                                  const uint64_t* __restrict__ recv_flat, uint32_t n) {

@@ -35,6 +35,16 @@ def test_runs_bit_exact(product, golden, golden_arrays, key):
     assert got == want
 
 
+@pytest.mark.parametrize("variant", ["1", "3", "5", "10", "11", "12", "13", "14", "15"])
+def test_kernel_variants_bit_exact(product, golden, variant, monkeypatch):
+    """Every launch shape of the plain kernel (register-resident and
+    TMA-pipelined persistent) gives the reference's bits."""
+    monkeypatch.setenv("SPLBCU_PLAIN_VARIANT", variant)
+    for key in ("bif_W3_soa_reordered", "pipe_4_20_W4", "blob1_noise_W23"):
+        res = cases.execute_run(product, cases.RUNS[key])
+        assert cases.run_digest(res) == golden["runs"][key], key
+
+
 def test_live_reference_random_case(product, reference):
     """A case outside the golden set, against the reference run live."""
     run = dict(domain="bif_3_2_6_8", bcs=("bif", "bif_inlet"), tau=0.7, dt=2e-3, W=3, layout=1, steps=30,
