@@ -626,20 +626,27 @@ class Engine {
             case 13: launch_tma<256, 2, 1>(wk, s, b, e); break;
             case 14: launch_tma<128, 4, 1>(wk, s, b, e); break;
             case 15: launch_tma<64, 4, 3>(wk, s, b, e); break;
+            case 16: launch_tma<96, 2, 5>(wk, s, b, e); break;
+            case 17: launch_tma<160, 2, 3>(wk, s, b, e); break;
+            case 18: launch_tma<64, 2, 7>(wk, s, b, e); break;
+            case 19: launch_tma<128, 2, 5, false>(wk, s, b, e); break;
+            case 20: launch_tma<128, 2, 4, false>(wk, s, b, e); break;
+            case 21: launch_tma<256, 2, 2, false>(wk, s, b, e); break;
+            case 22: launch_tma<64, 2, 10, false>(wk, s, b, e); break;
             default: launch_plain_t<128, 4>(wk, s, b, e, ia); break;
         }
     }
 
     // Persistent TMA-pipelined launch: grid = resident CTAs (occupancy x SMs).
-    template <int T, int S, int B>
+    template <int T, int S, int B, bool TS = true>
     void launch_tma(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e) {
-        using Lm = PushTmaSmem<T, S>;
+        using Lm = PushTmaSmem<T, S, TS>;
         static int cfg_dev = -1, resident = 0;
         if (cfg_dev != wk.dev) {
-            CK(cudaFuncSetAttribute(lbm_push_tma<T, S, B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            CK(cudaFuncSetAttribute(lbm_push_tma<T, S, B, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     int(Lm::kBytes)));
             int per_sm = 0, sms = 0;
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lbm_push_tma<T, S, B>, T, Lm::kBytes));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lbm_push_tma<T, S, B, TS>, T, Lm::kBytes));
             CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, wk.dev));
             resident = std::max(1, per_sm) * sms;
             cfg_dev = wk.dev;
@@ -647,8 +654,8 @@ class Engine {
         const uint32_t base = b & ~3u;
         const uint32_t ntiles = (e - base + T - 1) / T;
         const unsigned grid = unsigned(std::min<uint32_t>(ntiles, uint32_t(resident)));
-        lbm_push_tma<T, S, B><<<grid, T, Lm::kBytes, s>>>(wk.f_old(), wk.f_new(), wk.tab.get<uint32_t>(), wk.P, b, e,
-                                                           omega);
+        lbm_push_tma<T, S, B, TS><<<grid, T, Lm::kBytes, s>>>(wk.f_old(), wk.f_new(), wk.tab.get<uint32_t>(), wk.P,
+                                                               b, e, omega);
     }
 
     void launch_range(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, bool iolet, const double* staged,

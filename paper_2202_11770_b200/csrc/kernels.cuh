@@ -149,10 +149,10 @@ __device__ __forceinline__ uint64_t evict_first_policy() {
     return p;
 }
 
-template <int T, int S>
+template <int T, int S, bool kTabSmem = true>
 struct PushTmaSmem {
-    static constexpr uint32_t kF = uint32_t(kQ) * T * 8;        // f tile
-    static constexpr uint32_t kT = uint32_t(kQ - 1) * T * 4;    // table tile
+    static constexpr uint32_t kF = uint32_t(kQ) * T * 8;                   // f tile
+    static constexpr uint32_t kT = kTabSmem ? uint32_t(kQ - 1) * T * 4 : 0;  // table tile
     static constexpr uint32_t kStage = kF + kT;
     static constexpr uint32_t kBytes = S * kStage + S * 8;
 };
@@ -161,11 +161,11 @@ struct PushTmaSmem {
 // begin rounded down to 4 sites (16-byte bulk-copy alignment); sites outside
 // the range are loaded but neither computed nor stored.  Buffers carry a
 // tail pad of T elements so the last tile's copies stay in bounds.
-template <int T, int S, int kMinBlocks>
+template <int T, int S, int kMinBlocks, bool kTabSmem = true>
 __global__ void __launch_bounds__(T, kMinBlocks)
 lbm_push_tma(const double* __restrict__ fo, double* __restrict__ fn, const uint32_t* __restrict__ tab,
              uint64_t P, uint32_t begin, uint32_t end, double omega) {
-    using L = PushTmaSmem<T, S>;
+    using L = PushTmaSmem<T, S, kTabSmem>;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S * L::kStage);
     const uint32_t base = begin & ~3u;
@@ -187,9 +187,11 @@ lbm_push_tma(const double* __restrict__ fo, double* __restrict__ fn, const uint3
         mbar_expect_tx(&bar[st], L::kStage);
 #pragma unroll 1
         for (int i = 0; i < kQ; ++i) bulk_g2s(buf + i * T * 8, fo + uint64_t(i) * P + t0, T * 8, &bar[st], policy);
+        if constexpr (kTabSmem) {
 #pragma unroll 1
-        for (int i = 0; i < kQ - 1; ++i)
-            bulk_g2s(buf + L::kF + i * T * 4, tab + uint64_t(i) * P + t0, T * 4, &bar[st], policy);
+            for (int i = 0; i < kQ - 1; ++i)
+                bulk_g2s(buf + L::kF + i * T * 4, tab + uint64_t(i) * P + t0, T * 4, &bar[st], policy);
+        }
     };
     if (tid == 0)
         for (uint32_t k = 0; k + 1 < uint32_t(S); ++k) issue(k);
@@ -198,11 +200,20 @@ lbm_push_tma(const double* __restrict__ fo, double* __restrict__ fn, const uint3
         if (tile >= ntiles) break;
         if (tid == 0) issue(k + S - 1);
         const int st = int(k % S);
+        const uint32_t s = base + tile * T + tid;
+        const bool live = s >= begin && s < end;
+        uint32_t treg[kTabSmem ? 1 : kQ - 1];
+        if constexpr (!kTabSmem) {
+            // table straight to registers (coalesced), overlapping the wait
+            if (live) {
+#pragma unroll
+                for (int i = 0; i < kQ - 1; ++i) treg[i] = ld_t(tab + uint64_t(i) * P + s);
+            }
+        }
         mbar_wait(&bar[st], (k / S) & 1u);
         const double* fs = reinterpret_cast<const double*>(smem + st * L::kStage);
         const uint32_t* ts = reinterpret_cast<const uint32_t*>(smem + st * L::kStage + L::kF);
-        const uint32_t s = base + tile * T + tid;
-        if (s >= begin && s < end) {
+        if (live) {
             double f[kQ];
 #pragma unroll
             for (int i = 0; i < kQ; ++i) f[i] = fs[i * T + tid];
@@ -213,7 +224,9 @@ lbm_push_tma(const double* __restrict__ fo, double* __restrict__ fn, const uint3
 #pragma unroll
             for (int i = 1; i < kQ; ++i) {
                 const double fpost = relax(f[i], feq[i], omega);
-                const uint32_t v = ts[(i - 1) * T + tid];
+                uint32_t v;
+                if constexpr (kTabSmem) v = ts[(i - 1) * T + tid];
+                else v = treg[i - 1];
                 uint64_t dst;
                 if (v < kSpecial) dst = uint64_t(i) * P + v;
                 else if (((v >> kOpShift) & 3u) == kOpShared) dst = uint64_t(kQ) * P + (v & kPayload);

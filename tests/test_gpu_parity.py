@@ -35,7 +35,8 @@ def test_runs_bit_exact(product, golden, golden_arrays, key):
     assert got == want
 
 
-@pytest.mark.parametrize("variant", ["1", "3", "5", "10", "11", "12", "13", "14", "15"])
+@pytest.mark.parametrize("variant", ["1", "3", "5", "10", "11", "12", "13", "14", "15", "16", "17", "18", "19",
+                                     "20", "21", "22"])
 def test_kernel_variants_bit_exact(product, golden, variant, monkeypatch):
     """Every launch shape of the plain kernel (register-resident and
     TMA-pipelined persistent) gives the reference's bits."""
