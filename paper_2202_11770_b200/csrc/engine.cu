@@ -46,6 +46,37 @@ std::string nccl_unique_id(void* out128) {
 
 constexpr uint64_t kTilePad = 256;  // tail pad so the last TMA tile stays in bounds
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        CK(cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q));
+        if (!p || q != cudaDriverEntryPointSuccess) fail(ErrKind::Cuda, "cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    return fn;
+}
+
+// 2-D map over `planes` direction planes of pitch P: dim0 = site, dim1 = plane;
+// one box = `box` sites x all planes.
+static void encode_planes(CUtensorMap* m, void* base, bool f64, int planes, uint64_t P, uint32_t box) {
+    std::memset(m, 0, sizeof(*m));
+    const cuuint64_t dims[2] = {cuuint64_t(P), cuuint64_t(planes)};
+    const cuuint64_t strides[1] = {cuuint64_t(P * (f64 ? 8 : 4))};
+    const cuuint32_t boxd[2] = {box, cuuint32_t(planes)};
+    const cuuint32_t es[2] = {1, 1};
+    const CUresult r = encode_fn()(m, f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, base,
+                                   dims, strides, boxd, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(ErrKind::Cuda, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+}
+
 namespace {
 
 struct DevMem {
@@ -212,6 +243,10 @@ struct WorkerDev {
     uint64_t obs_row_base = 0, obs_rows = 0;
     // kernel timing
     std::vector<cudaEvent_t> tev;
+    // 2-D tensor maps over the direction-major planes (per f buffer, table)
+    CUtensorMap tm_f[2][2];  // [buffer][box T variant: 0 -> 128 sites, 1 -> 256 sites]
+    CUtensorMap tm_t[2];
+    bool tma_ok = false;  // maps encoded (planes at least one box long)
     size_t tev_used = 0;
 
     double* f_old() const { return fbuf[old].get<double>(); }
@@ -549,6 +584,14 @@ class Engine {
         upload(wk.io_coords, ioc, s);
         upload(wk.io_geo, io_host, s);
         wk.cap4.alloc<double>(4 * uint64_t(std::max<uint32_t>(wk.n, 1)));
+        // tensor maps for the warp-specialised TMA kernel
+        wk.tma_ok = wk.P >= 256;
+        for (int v = 0; v < 2 && wk.tma_ok; ++v) {
+            const uint32_t box = v == 0 ? 128 : 256;
+            for (int b = 0; b < 2; ++b)
+                encode_planes(&wk.tm_f[b][v], wk.fbuf[b].get<double>(), true, kQ, wk.P, box);
+            encode_planes(&wk.tm_t[v], wk.tab.get<uint32_t>(), false, kQ - 1, wk.P, box);
+        }
         CK(cudaStreamSynchronize(s));
     }
 
@@ -633,8 +676,41 @@ class Engine {
             case 20: launch_tma<128, 2, 4, false>(wk, s, b, e); break;
             case 21: launch_tma<256, 2, 2, false>(wk, s, b, e); break;
             case 22: launch_tma<64, 2, 10, false>(wk, s, b, e); break;
+            case 30: launch_ws<128, 2, 3, true>(wk, s, b, e); break;
+            case 31: launch_ws<128, 3, 2, true>(wk, s, b, e); break;
+            case 32: launch_ws<256, 2, 1, true>(wk, s, b, e); break;
+            case 33: launch_ws<128, 2, 3, false>(wk, s, b, e); break;
+            case 34: launch_ws<256, 2, 2, false>(wk, s, b, e); break;
+            case 35: launch_ws<128, 3, 3, false>(wk, s, b, e); break;
+            case 36: launch_ws<128, 4, 2, false>(wk, s, b, e); break;
             default: launch_plain_t<128, 4>(wk, s, b, e, ia); break;
         }
+    }
+
+    // Warp-specialised 2-D TMA launch (producer warp + T/32 consumer warps).
+    template <int T, int S, int B, bool TS>
+    void launch_ws(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e) {
+        using Lm = PushWsSmem<T, S, TS>;
+        if (!wk.tma_ok) {  // tiny worker: planes shorter than one TMA box
+            IoletArgs ia{};
+            return launch_plain_t<128, 4>(wk, s, b, e, ia);
+        }
+        static int cfg_dev = -1, resident = 0;
+        if (cfg_dev != wk.dev) {
+            CK(cudaFuncSetAttribute(lbm_push_ws<T, S, B, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(Lm::kBytes)));
+            int per_sm = 0, sms = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lbm_push_ws<T, S, B, TS>, T + 32, Lm::kBytes));
+            CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, wk.dev));
+            resident = std::max(1, per_sm) * sms;
+            cfg_dev = wk.dev;
+        }
+        const int v = T == 128 ? 0 : 1;
+        const uint32_t base = b & ~3u;
+        const uint32_t ntiles = (e - base + T - 1) / T;
+        const unsigned grid = unsigned(std::min<uint32_t>(ntiles, uint32_t(resident)));
+        lbm_push_ws<T, S, B, TS><<<grid, T + 32, Lm::kBytes, s>>>(wk.tm_f[wk.old][v], wk.tm_t[v], wk.f_new(),
+                                                                   wk.tab.get<uint32_t>(), wk.P, b, e, omega);
     }
 
     // Persistent TMA-pipelined launch: grid = resident CTAs (occupancy x SMs).

@@ -16,6 +16,10 @@
 
 #include <cstdint>
 
+#if defined(__CUDACC__)
+#include <cuda.h>  // CUtensorMap (type only; encoding goes through the runtime's driver entry point)
+#endif
+
 #include "lattice.hpp"
 
 namespace splbcu {
@@ -235,6 +239,124 @@ lbm_push_tma(const double* __restrict__ fo, double* __restrict__ fn, const uint3
             }
         }
         __syncthreads();  // stage st is free for the copy issued next iteration
+    }
+}
+
+// ---- warp-specialised 2-D TMA variant --------------------------------------
+// One TMA instruction per tile moves the whole [19 planes x T sites] f box
+// (and, optionally, the [18 x T] table box) described by a CUtensorMap over
+// the direction-major store.  A dedicated producer warp runs the S-stage ring
+// with full/empty mbarriers; the T/32 consumer warps never meet at a CTA
+// barrier.  OOB boxes past the plane end are zero-filled by the TMA unit.
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int32_t x, int32_t y, uint64_t* bar,
+                                       uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+
+template <int T, int S, bool kTabSmem>
+struct PushWsSmem {
+    static constexpr uint32_t kF = uint32_t(kQ) * T * 8;
+    static constexpr uint32_t kT = kTabSmem ? uint32_t(kQ - 1) * T * 4 : 0;
+    static constexpr uint32_t kStage = kF + kT;
+    static constexpr uint32_t kBytes = S * kStage + 2 * S * 8 + 128;  // + barriers + alignment slack
+};
+
+template <int T, int S, int kMinBlocks, bool kTabSmem>
+__global__ void __launch_bounds__(T + 32, kMinBlocks)
+lbm_push_ws(const __grid_constant__ CUtensorMap tm_f, const __grid_constant__ CUtensorMap tm_t,
+            double* __restrict__ fn, const uint32_t* __restrict__ tab, uint64_t P, uint32_t begin, uint32_t end,
+            double omega) {
+    using L = PushWsSmem<T, S, kTabSmem>;
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * L::kStage);
+    uint64_t* empty = full + S;
+    constexpr int kConsumerWarps = T / 32;
+    const uint32_t base = begin & ~3u;
+    const uint32_t ntiles = (end - base + T - 1) / T;
+    const uint32_t G = gridDim.x;
+    const int warp = int(threadIdx.x >> 5), lane = int(threadIdx.x & 31);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kConsumerWarps);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    if (warp == kConsumerWarps) {  // producer
+        if (lane == 0) {
+            const uint64_t policy = evict_first_policy();
+            for (uint32_t k = 0;; ++k) {
+                const uint32_t tile = blockIdx.x + k * G;
+                if (tile >= ntiles) break;
+                const int st = int(k % S);
+                if (k >= uint32_t(S)) mbar_wait(&empty[st], ((k / S) - 1) & 1u);
+                mbar_expect_tx(&full[st], L::kStage);
+                const int32_t x = int32_t(base + tile * T);
+                tma_2d(smem + st * L::kStage, &tm_f, x, 0, &full[st], policy);
+                if constexpr (kTabSmem) tma_2d(smem + st * L::kStage + L::kF, &tm_t, x, 0, &full[st], policy);
+            }
+        }
+        return;
+    }
+    const uint32_t tid = threadIdx.x;
+    for (uint32_t k = 0;; ++k) {
+        const uint32_t tile = blockIdx.x + k * G;
+        if (tile >= ntiles) break;
+        const int st = int(k % S);
+        const uint32_t s = base + tile * T + tid;
+        const bool live = s >= begin && s < end;
+        uint32_t treg[kTabSmem ? 1 : kQ - 1];
+        if constexpr (!kTabSmem) {
+            if (live) {
+#pragma unroll
+                for (int i = 0; i < kQ - 1; ++i) treg[i] = ld_t(tab + uint64_t(i) * P + s);
+            }
+        }
+        mbar_wait(&full[st], (k / S) & 1u);
+        const double* fs = reinterpret_cast<const double*>(smem + st * L::kStage);
+        const uint32_t* ts = reinterpret_cast<const uint32_t*>(smem + st * L::kStage + L::kF);
+        double f[kQ];
+        if (live) {
+#pragma unroll
+            for (int i = 0; i < kQ; ++i) f[i] = fs[i * T + tid];
+        }
+        uint32_t tv[kQ - 1];
+        if constexpr (kTabSmem) {
+            if (live) {
+#pragma unroll
+                for (int i = 0; i < kQ - 1; ++i) tv[i] = ts[i * T + tid];
+            }
+        }
+        // stage consumed: hand it back to the producer before the math
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+        if (live) {
+            const Macro m = macro_of(f);
+            double feq[kQ];
+            feq_all(m.rho, m.ux, m.uy, m.uz, feq);
+            fn[s] = relax(f[0], feq[0], omega);
+#pragma unroll
+            for (int i = 1; i < kQ; ++i) {
+                const double fpost = relax(f[i], feq[i], omega);
+                uint32_t v;
+                if constexpr (kTabSmem) v = tv[i - 1];
+                else v = treg[i - 1];
+                uint64_t dst;
+                if (v < kSpecial) dst = uint64_t(i) * P + v;
+                else if (((v >> kOpShift) & 3u) == kOpShared) dst = uint64_t(kQ) * P + (v & kPayload);
+                else dst = uint64_t(inv(i)) * P + s;
+                fn[dst] = fpost;
+            }
+        }
     }
 }
 
