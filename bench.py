@@ -65,12 +65,12 @@ def workload(M, name, scale=1.0):
                        M.BCEntry(M.PRESSURE, M.TimeTable.constant(CS2 - dp / 2))])
         return d, bcs, dict(tau=0.9, dt_s=1.0), "C1 Poiseuille pipe R=16 L=128, pressure iolets, tau=0.9"
     if name == "c3":
-        levels = 6
-        d = M.build_tree(64, int(round(700 * scale)), levels, 0.8, 0.8)
+        levels = 6  # R0=80, L0=800: 107,037,564 sites, 64 outlets
+        d = M.build_tree(80, max(8, int(round(800 * scale))), levels, 0.8, 0.8)
         n_out = 2 ** levels
         ents = [M.BCEntry(M.PRESSURE, M.TimeTable.constant(CS2 * 1.001))]
         ents += [M.BCEntry(M.PRESSURE, M.TimeTable.constant(CS2 * 0.999)) for _ in range(n_out)]
-        return d, M.BCSet(ents), dict(tau=0.8, dt_s=1.0), f"C3 bifurcating tree R0=64, {levels} levels, pressure iolets"
+        return d, M.BCSet(ents), dict(tau=0.8, dt_s=1.0), f"C3 bifurcating tree R0=80 L0={max(8, int(round(800 * scale)))}, {levels} levels, pressure iolets"
     if name == "c4":
         nz = int(round(2400 * scale))
         d = M.build_channel(256, 256, nz)

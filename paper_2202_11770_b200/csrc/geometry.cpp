@@ -4,7 +4,10 @@
 // (z,y,x) order, a CSR row index instead of a hash map, and parallel loops,
 // so 10^8-site domains build in seconds.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <mutex>
@@ -20,6 +23,15 @@ int hw_threads() {
         return int(h == 0 ? 1 : std::min(h, 64u));
     }();
     return n;
+}
+
+void phase(const char* what) {
+    static const bool on = std::getenv("SPLBCU_VERBOSE") != nullptr;
+    static auto last = std::chrono::steady_clock::now();
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[splbcu] %-28s %8.3f s\n", what, std::chrono::duration<double>(now - last).count());
+    last = now;
 }
 
 void parallel_for(uint64_t n, const std::function<void(uint64_t, uint64_t, int)>& fn,
@@ -78,13 +90,15 @@ void SiteIndex::build_rows() {
         ly(hw_threads(), INT32_MAX), hy(hw_threads(), INT32_MIN);
     parallel_for(keys.size(), [&](uint64_t b, uint64_t e, int t) {
         int32_t X, Y, Z;
+        int32_t a0 = INT32_MAX, a1 = INT32_MIN, b0 = INT32_MAX, b1 = INT32_MIN;  // thread-local: no false sharing
         for (uint64_t k = b; k < e; ++k) {
             key_coords(keys[k], X, Y, Z);
-            lx[t] = std::min(lx[t], X);
-            hx[t] = std::max(hx[t], X);
-            ly[t] = std::min(ly[t], Y);
-            hy[t] = std::max(hy[t], Y);
+            a0 = std::min(a0, X);
+            a1 = std::max(a1, X);
+            b0 = std::min(b0, Y);
+            b1 = std::max(b1, Y);
         }
+        lx[t] = a0, hx[t] = a1, ly[t] = b0, hy[t] = b1;
     });
     lo[0] = *std::min_element(lx.begin(), lx.end());
     hi[0] = *std::max_element(hx.begin(), hx.end());
@@ -102,6 +116,27 @@ void SiteIndex::build_rows() {
     }
     for (size_t r = 1; r < row_off.size(); ++r) row_off[r] += row_off[r - 1];
     rows = true;
+}
+
+// Requires build_rows() first (bounding box).
+void SiteIndex::build_bitmap() {
+    bits.clear();
+    if (keys.empty()) return;
+    bnx = int64_t(hi[0]) - lo[0] + 1;
+    const double cells = double(bnx) * double(ny) * double(nz);
+    if (cells > double(uint64_t(1) << 33)) return;  // > 1 GiB: fall back to the row index
+    bits.assign(size_t((uint64_t(cells) + 63) / 64), 0);
+    uint64_t* w = bits.data();
+    const int32_t lx = lo[0], ly = lo[1], lz = lo[2];
+    const int64_t NY = ny, NX = bnx;
+    parallel_for(keys.size(), [&](uint64_t b, uint64_t e, int) {
+        int32_t x, y, z;
+        for (uint64_t k = b; k < e; ++k) {
+            key_coords(keys[k], x, y, z);
+            const uint64_t c = uint64_t(((int64_t(z) - lz) * NY + (int64_t(y) - ly)) * NX + (int64_t(x) - lx));
+            __atomic_fetch_or(&w[c >> 6], uint64_t(1) << (c & 63), __ATOMIC_RELAXED);
+        }
+    });
 }
 
 int64_t SiteIndex::find(int32_t x, int32_t y, int32_t z) const {
@@ -146,20 +181,46 @@ SiteIndex index_domain(const Domain& d) {
                       [&](uint32_t a, uint32_t b) { return ix.keys[a] < ix.keys[b]; });
             for (uint64_t k = 0; k < d.n; ++k) mk[k] = ix.keys[perm[k]], mv[k] = perm[k];
         } else {
-            std::vector<uint64_t> pos(runs.size());
-            for (size_t r = 0; r < runs.size(); ++r) pos[r] = runs[r].first;
-            for (uint64_t k = 0; k < d.n; ++k) {
-                int best = -1;
-                for (size_t r = 0; r < runs.size(); ++r)
-                    if (pos[r] < runs[r].second &&
-                        (best < 0 || ix.keys[pos[r]] < ix.keys[pos[size_t(best)]]))
-                        best = int(r);
-                const uint64_t s = pos[size_t(best)]++;
-                mk[k] = ix.keys[s];
-                mv[k] = uint32_t(s);
+            // Bucket by z-plane (each run splits into contiguous per-plane
+            // pieces found by binary search), then sort every plane's few
+            // pieces independently, in parallel.
+            const int32_t z0 = int32_t(int64_t(ix.keys[runs[0].first] >> 42) - kBias);
+            int32_t zmin = z0, zmax = z0;
+            for (auto& r : runs) {
+                zmin = std::min(zmin, int32_t(int64_t(ix.keys[r.first] >> 42) - kBias));
+                zmax = std::max(zmax, int32_t(int64_t(ix.keys[r.second - 1] >> 42) - kBias));
             }
+            const size_t nzp = size_t(int64_t(zmax) - zmin + 1);
+            // cut[r][p] = first position of run r with z >= zmin + p
+            std::vector<std::vector<uint64_t>> cut(runs.size(), std::vector<uint64_t>(nzp + 1));
+            for (size_t r = 0; r < runs.size(); ++r) {
+                for (size_t p = 0; p <= nzp; ++p) {
+                    const uint64_t kz = p == nzp ? UINT64_MAX : (uint64_t(int64_t(zmin) + int64_t(p) + kBias) << 42);
+                    cut[r][p] = uint64_t(std::lower_bound(ix.keys.begin() + int64_t(runs[r].first),
+                                                          ix.keys.begin() + int64_t(runs[r].second), kz) -
+                                         ix.keys.begin());
+                }
+            }
+            std::vector<uint64_t> out_off(nzp + 1, 0);
+            for (size_t p = 0; p < nzp; ++p) {
+                uint64_t c = 0;
+                for (size_t r = 0; r < runs.size(); ++r) c += cut[r][p + 1] - cut[r][p];
+                out_off[p + 1] = out_off[p] + c;
+            }
+            parallel_for(nzp, [&](uint64_t pb, uint64_t pe, int) {
+                std::vector<std::pair<uint64_t, uint32_t>> buf;
+                for (uint64_t p = pb; p < pe; ++p) {
+                    buf.clear();
+                    for (size_t r = 0; r < runs.size(); ++r)
+                        for (uint64_t s = cut[r][p]; s < cut[r][p + 1]; ++s) buf.push_back({ix.keys[s], uint32_t(s)});
+                    std::sort(buf.begin(), buf.end());
+                    uint64_t o = out_off[p];
+                    for (auto& kv : buf) mk[o] = kv.first, mv[o] = kv.second, ++o;
+                }
+            }, 1);
         }
     }
+    phase("index_domain merge");
     ix.keys.swap(mk);
     ix.value.swap(mv);
     ix.build_rows();
@@ -206,6 +267,8 @@ static Domain classify_sorted(std::vector<int32_t>&& coords, const std::vector<u
     SiteIndex ix;
     ix.keys = keys;
     ix.build_rows();
+    ix.build_bitmap();
+    phase("classify: rows+bitmap");
 
     std::vector<uint8_t> kind(18 * n);
     std::vector<uint8_t> type(n);
@@ -229,7 +292,7 @@ static Domain classify_sorted(std::vector<int32_t>&& coords, const std::vector<u
                     const int64_t p = int64_t(s) + cx(i);
                     member = p >= 0 && uint64_t(p) < n && keys[uint64_t(p)] == zyx_key(tx, ty, tz);
                 } else {
-                    member = ix.find(tx, ty, tz) >= 0;
+                    member = ix.contains(tx, ty, tz);
                 }
                 if (member) {
                     k = 0;
@@ -272,6 +335,7 @@ static Domain classify_sorted(std::vector<int32_t>&& coords, const std::vector<u
                            " intersects no boundary links");
     }
 
+    phase("classify: links");
     // Stable counting sort by type over the zyx order == sort by (type,z,y,x)
     // (geometry.hpp:189-195).
     Domain d;
@@ -330,6 +394,7 @@ Domain classify_sites(const std::vector<int32_t>& voxels, std::vector<IoletGeo> 
     for (uint64_t s = 0; s < n; ++s) keys[s] = zyx_key(voxels[3 * s], voxels[3 * s + 1], voxels[3 * s + 2]);
     bool sorted = true;
     for (uint64_t s = 1; s < n && sorted; ++s) sorted = keys[s - 1] < keys[s];
+    phase("classify: keys");
     if (sorted) {
         std::vector<int32_t> c(voxels);
         return classify_sorted(std::move(c), keys, nullptr, std::move(iolets), voxel_size);
@@ -357,12 +422,25 @@ void validate_domain(const Domain& d) {
     for (size_t k = 0; k < d.iolets.size(); ++k)
         if (!unit_normal(d.iolets[k]))
             geometry_error("domain: iolet " + std::to_string(k) + " normal is not unit length");
-    // duplicates (index_coords)
-    std::vector<uint64_t> keys(d.n);
-    for (uint64_t s = 0; s < d.n; ++s)
-        keys[s] = zyx_key(d.coords[3 * s], d.coords[3 * s + 1], d.coords[3 * s + 2]);
-    std::vector<uint64_t> sk(keys);
-    std::sort(sk.begin(), sk.end());
+    // duplicates (index_coords); index_domain merges the type runs when the
+    // ranges are a valid partition of zyx-sorted runs, else sorts.
+    bool ranges_ok = true;
+    {
+        uint64_t p = 0;
+        for (int t = 0; t < 6; ++t) {
+            if (d.type_ranges[t][0] != p || d.type_ranges[t][1] < p || d.type_ranges[t][1] > d.n) ranges_ok = false;
+            p = d.type_ranges[t][1];
+        }
+        ranges_ok &= p == d.n;
+    }
+    std::vector<uint64_t> sk;
+    if (ranges_ok) {
+        sk = index_domain(d).keys;
+    } else {
+        sk.resize(d.n);
+        for (uint64_t s = 0; s < d.n; ++s) sk[s] = zyx_key(d.coords[3 * s], d.coords[3 * s + 1], d.coords[3 * s + 2]);
+        std::sort(sk.begin(), sk.end());
+    }
     for (uint64_t k = 1; k < d.n; ++k)
         if (sk[k] == sk[k - 1]) geometry_error("classify_sites: duplicate voxel");
     uint64_t pos = 0;
@@ -378,6 +456,8 @@ void validate_domain(const Domain& d) {
     SiteIndex ix;
     ix.keys = std::move(sk);
     ix.build_rows();
+    ix.build_bitmap();
+    phase("validate: index+bitmap");
     const int nt = hw_threads();
     std::vector<uint64_t> first_bad(nt, UINT64_MAX);
     std::vector<int> first_code(nt, 0);
@@ -394,7 +474,7 @@ void validate_domain(const Domain& d) {
                 while (lk < d.iolet_link_pos.size() && d.iolet_link_pos[lk] < 18 * s + uint64_t(i - 1)) ++lk;
                 if (lk < d.iolet_link_pos.size() && d.iolet_link_pos[lk] == 18 * s + uint64_t(i - 1))
                     io = d.iolet_link_id[lk];
-                const bool in_set = ix.find(x + cx(i), y + cy(i), z + cz(i)) >= 0;
+                const bool in_set = ix.contains(x + cx(i), y + cy(i), z + cz(i));
                 if (k == 0) {
                     if (!in_set) code = 1;
                 } else {
@@ -413,6 +493,7 @@ void validate_domain(const Domain& d) {
             }
         }
     });
+    phase("validate: links");
     uint64_t best = UINT64_MAX;
     int code = 0;
     for (int t = 0; t < nt; ++t)
@@ -594,6 +675,7 @@ Domain build_tree(int root_radius, int root_length, int levels, double radius_ra
         vox.insert(vox.end(), s.begin(), s.end());
         std::vector<int32_t>().swap(s);
     }
+    phase("tree: voxelise");
     std::vector<IoletGeo> io;
     io.push_back({0, {kAxisOffsetX, kAxisOffsetY, -0.5}, {0.0, 0.0, 1.0}, rad[0]});
     const int k = L - 1;

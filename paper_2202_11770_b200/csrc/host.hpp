@@ -28,6 +28,8 @@ struct Error : std::runtime_error {
 
 // ---- small helpers ---------------------------------------------------------
 int hw_threads();
+// Phase timer printed to stderr when SPLBCU_VERBOSE is set.
+void phase(const char* what);
 // Runs fn(begin, end, thread_index) over [0, n) split in contiguous chunks.
 void parallel_for(uint64_t n, const std::function<void(uint64_t, uint64_t, int)>& fn,
                   uint64_t min_chunk = 1 << 15);
@@ -76,9 +78,20 @@ struct SiteIndex {
     std::vector<uint64_t> row_off;  // (ny*nz + 1) offsets when rows
     int64_t ny = 0, nz = 0;
 
+    // dense occupancy bitmap over the bounding box (when it fits in 1 GiB)
+    std::vector<uint64_t> bits;
+    int64_t bnx = 0;
+
     void build_rows();
+    void build_bitmap();
     // position in keys of (x,y,z) or -1
     int64_t find(int32_t x, int32_t y, int32_t z) const;
+    bool contains(int32_t x, int32_t y, int32_t z) const {
+        if (bits.empty()) return find(x, y, z) >= 0;
+        if (x < lo[0] || x > hi[0] || y < lo[1] || y > hi[1] || z < lo[2] || z > hi[2]) return false;
+        const uint64_t b = uint64_t(((int64_t(z) - lo[2]) * ny + (int64_t(y) - lo[1])) * bnx + (int64_t(x) - lo[0]));
+        return (bits[b >> 6] >> (b & 63)) & 1u;
+    }
 };
 
 // Builds the lookup over all sites of a domain (value = global site index).

@@ -1,0 +1,134 @@
+"""The N>1 path: one process per GPU, NCCL halo exchange.
+
+CPU (gloo, world size 2): every rank derives the same decomposition from the
+same domain with no communication (the reference's partition is a pure
+function of the domain, decomp.hpp:65-188), and the per-rank views the
+engine would build (own sites, neighbour lists, cut-link counts) are
+consistent across ranks.
+
+GPU (>= 2 devices): torchrun-style ranks running Simulation.distributed with
+NCCL send/recv must reproduce the single-process result bit for bit.
+"""
+import os
+import socket
+import subprocess
+import sys
+import textwrap
+
+import numpy as np
+import pytest
+
+import cases
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _run_ranks(script, world, env_extra=None, timeout=600):
+    port = _free_port()
+    procs = []
+    for r in range(world):
+        env = dict(os.environ, RANK=str(r), WORLD_SIZE=str(world), LOCAL_RANK=str(r), MASTER_ADDR="127.0.0.1",
+                   MASTER_PORT=str(port), PYTHONPATH=os.pathsep.join([ROOT, os.path.join(ROOT, "tests")]))
+        env.update(env_extra or {})
+        procs.append(subprocess.Popen([sys.executable, "-c", script], env=env, stdout=subprocess.PIPE,
+                                      stderr=subprocess.STDOUT, text=True))
+    outs = []
+    for p in procs:
+        try:
+            out, _ = p.communicate(timeout=timeout)
+        except subprocess.TimeoutExpired:
+            p.kill()
+            out, _ = p.communicate()
+        outs.append((p.returncode, out))
+    return outs
+
+
+GLOO_SCRIPT = textwrap.dedent("""
+    import os, hashlib, json
+    import numpy as np
+    import torch, torch.distributed as td
+    import cases, impls
+    td.init_process_group("gloo")
+    rank, world = td.get_rank(), td.get_world_size()
+    P = impls.product()
+    d = P.build_bifurcation(4, 3, 12, 12)
+    W = 4
+    p = P.partition(d, W)
+    dig = json.dumps(cases.partition_digest(p), sort_keys=True)
+    # ranks own workers rank, rank+world, ...: their local views
+    mine = {w: dict(n=len(p.parts[w].sites), nb=p.parts[w].neighbors) for w in range(rank, W, world)}
+    objs = [None] * world
+    td.all_gather_object(objs, (dig, mine))
+    assert all(o[0] == objs[0][0] for o in objs), "ranks disagree on the decomposition"
+    views = {}
+    for o in objs:
+        views.update(o[1])
+    assert sorted(views) == list(range(W))
+    assert sum(v["n"] for v in views.values()) == d.n_sites()
+    for w, v in views.items():
+        for nb in v["nb"]:
+            assert w in views[nb]["nb"], "neighbour relation not symmetric"
+    td.barrier()
+    print("OK", rank)
+""")
+
+
+def test_gloo_two_ranks_agree_on_decomposition():
+    outs = _run_ranks(GLOO_SCRIPT, 2)
+    for rc, out in outs:
+        assert rc == 0, out
+        assert "OK" in out
+
+
+NCCL_SCRIPT = textwrap.dedent("""
+    import os
+    import numpy as np
+    import torch, torch.distributed as td
+    import cases, impls
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    torch.cuda.set_device(rank)
+    td.init_process_group("gloo")
+    P = impls.product()
+    uid = P.Simulation.nccl_unique_id() if rank == 0 else bytes(128)
+    obj = [uid]
+    td.broadcast_object_list(obj, 0)
+    run = dict(domain="bif_4_3_12_12", bcs=("bif", "smoke_inlet"), tau=0.8, dt=1e-3, W=world, steps=60,
+               noise=(11, 0.01))
+    d = cases.make_domain(P, cases.DOMAINS[run["domain"]])
+    prm = P.EngineParams(tau=0.8, dt_s=1e-3, workers=world, devices=[rank])
+    sim = P.Simulation.distributed(d, cases.make_bcs(P, run["bcs"]), prm, rank, world, obj[0])
+    cases.apply_noise(P, sim, cases.noise_for(d.n_sites(), *run["noise"]))
+    sim.run(run["steps"])
+    snap = torch.tensor(sim.snapshot_fields())
+    td.all_reduce(snap)  # disjoint site sets: the sum assembles the field
+    if rank == 0:
+        ref = P.Simulation(d, cases.make_bcs(P, run["bcs"]), P.EngineParams(tau=0.8, dt_s=1e-3, workers=world,
+                                                                             devices=[0]))
+        cases.apply_noise(P, ref, cases.noise_for(d.n_sites(), *run["noise"]))
+        ref.run(run["steps"])
+        a, b = snap.numpy(), ref.snapshot_fields()
+        assert np.array_equal(a, b), float(np.max(np.abs(a - b)))
+    td.barrier()
+    print("OK", rank)
+""")
+
+
+@pytest.mark.gpu
+def test_nccl_ranks_match_single_process():
+    import torch
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    world = 4 if n >= 4 else 2
+    outs = _run_ranks(NCCL_SCRIPT, world)
+    for rc, out in outs:
+        assert rc == 0, out
+        assert "OK" in out
