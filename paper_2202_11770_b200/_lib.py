@@ -101,7 +101,26 @@ SIGNATURES = [
 ]
 
 
+def _point_at_torch_nccl() -> None:
+    """libsplbcu binds NCCL at run time (csrc/nccl_dyn.hpp).  Point it at the
+    libnccl.so.2 PyTorch ships so both share one NCCL whatever the import
+    order (two NCCL builds cannot coexist under one soname)."""
+    if "SPLBCU_NCCL_LIB" in os.environ:
+        return
+    try:
+        import importlib.util
+        spec = importlib.util.find_spec("nvidia.nccl")
+        for base in (spec.submodule_search_locations or []) if spec else []:
+            cand = os.path.join(base, "lib", "libnccl.so.2")
+            if os.path.exists(cand):
+                os.environ["SPLBCU_NCCL_LIB"] = cand
+                return
+    except Exception:
+        pass
+
+
 def load(path: str = LIB_PATH) -> C.CDLL:
+    _point_at_torch_nccl()
     if not os.path.exists(path):
         raise ImportError(
             f"libsplbcu.so not built at {path}; run __graft_entry__.build() "

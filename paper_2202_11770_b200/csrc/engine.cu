@@ -19,6 +19,7 @@
 
 #include "engine.hpp"
 #include "kernels.cuh"
+#include "nccl_dyn.hpp"
 
 namespace splbcu {
 
@@ -34,12 +35,18 @@ namespace splbcu {
     do {                                                                                        \
         ncclResult_t r_ = (x);                                                                  \
         if (r_ != ncclSuccess)                                                                  \
-            fail(ErrKind::Comm, std::string("exchange failure: NCCL error: ") + ncclGetErrorString(r_)); \
+            fail(ErrKind::Comm, std::string("exchange failure: NCCL error: ") + nccl().GetErrorString(r_)); \
     } while (0)
+
+static const NcclApi& nccl_checked() {
+    const NcclApi& a = nccl();
+    if (!a.ok) fail(ErrKind::Comm, "exchange failure: NCCL unavailable:" + a.error);
+    return a;
+}
 
 std::string nccl_unique_id(void* out128) {
     ncclUniqueId id;
-    NK(ncclGetUniqueId(&id));
+    NK(nccl_checked().GetUniqueId(&id));
     std::memcpy(out128, &id, sizeof(id));
     return {};
 }
@@ -319,7 +326,7 @@ class Engine {
             CK(cudaSetDevice(wk.dev));
             ncclUniqueId id;
             std::memcpy(&id, nccl_id, sizeof(id));
-            NK(ncclCommInitRank(&comm, nranks, id, rank));
+            NK(nccl_checked().CommInitRank(&comm, nranks, id, rank));
         }
         if (prm.observe_iolets) init_observation();
         for (auto& wp : W)
@@ -327,7 +334,7 @@ class Engine {
     }
 
     ~Engine() {
-        if (comm) ncclCommDestroy(comm);
+        if (comm) nccl().CommDestroy(comm);
         for (auto& wp : W) {
             if (!wp) continue;
             cudaSetDevice(wp->dev);
@@ -793,12 +800,13 @@ class Engine {
     }
 
     void exchange_nccl(WorkerDev& wk) {
-        NK(ncclGroupStart());
+        const NcclApi& N = nccl();
+        NK(N.GroupStart());
         for (const Seg& sg : wk.segs) {
-            NK(ncclSend(wk.f_new() + uint64_t(kQ) * wk.P + sg.base, sg.count, ncclDouble, sg.nb, comm, wk.sE));
-            NK(ncclRecv(wk.f_old() + uint64_t(kQ) * wk.P + sg.base, sg.count, ncclDouble, sg.nb, comm, wk.sE));
+            NK(N.Send(wk.f_new() + uint64_t(kQ) * wk.P + sg.base, sg.count, ncclDouble, sg.nb, comm, wk.sE));
+            NK(N.Recv(wk.f_old() + uint64_t(kQ) * wk.P + sg.base, sg.count, ncclDouble, sg.nb, comm, wk.sE));
         }
-        NK(ncclGroupEnd());
+        NK(N.GroupEnd());
     }
 
     void post_receive(WorkerDev& wk) {
@@ -955,12 +963,12 @@ class Engine {
                 if (q == cudaSuccess) break;
                 if (q != cudaErrorNotReady) CK(q);
                 ncclResult_t ar = ncclSuccess;
-                NK(ncclCommGetAsyncError(comm, &ar));
+                NK(nccl().CommGetAsyncError(comm, &ar));
                 if (ar != ncclSuccess && ar != ncclInProgress)
-                    fail(ErrKind::Comm, std::string("exchange failure: NCCL async error: ") + ncclGetErrorString(ar));
+                    fail(ErrKind::Comm, std::string("exchange failure: NCCL async error: ") + nccl().GetErrorString(ar));
                 const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - start).count();
                 if (el > prm.exchange_timeout_s * 1000.0) {  // generous: whole run, not one take
-                    ncclCommAbort(comm);
+                    nccl().CommAbort(comm);
                     comm = nullptr;
                     const int nb = W[w]->segs.empty() ? -1 : W[w]->segs.front().nb;
                     fail(ErrKind::Comm, "exchange failure: worker " + std::to_string(w) +
