@@ -186,25 +186,29 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     name = args.workload or ("c2" if world == 1 else "c3")
-    dist = None
     if world > 1:
         import torch
         import torch.distributed as td
         torch.cuda.set_device(local)
         td.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def make_sim(params):
+        """In-process engine at N=1; at N>1 one worker per rank, joined by a
+        fresh NCCL communicator (unique id from rank 0, broadcast by torch)."""
+        if world == 1:
+            return P.Simulation(d, bcs, params)
+        import torch
+        import torch.distributed as td
+        td.barrier()
         uid = P.Simulation.nccl_unique_id() if rank == 0 else bytes(128)
         t = torch.tensor(list(uid), dtype=torch.uint8, device="cuda")
         td.broadcast(t, 0)
-        dist = (rank, world, bytes(t.cpu().tolist()))
+        return P.Simulation.distributed(d, bcs, params, rank, world, bytes(t.cpu().tolist()))
 
     t_setup = time.time()
     d, bcs, p, desc = workload(P, name, args.scale)
     n = d.n_sites()
-    params = P.EngineParams(workers=world, devices=[local], **p)
-    if dist:
-        sim = P.Simulation.distributed(d, bcs, params, *dist)
-    else:
-        sim = P.Simulation(d, bcs, params)
+    sim = make_sim(P.EngineParams(workers=world, devices=[local], **p))
     setup_s = time.time() - t_setup
 
     def barrier():
@@ -252,7 +256,7 @@ def main():
     # e2e through the public API: run(1) per step with the iolet series on
     sim.close()
     params_e = P.EngineParams(workers=world, devices=[local], observe_iolets=True, **p)
-    sim = P.Simulation.distributed(d, bcs, params_e, *dist) if dist else P.Simulation(d, bcs, params_e)
+    sim = make_sim(params_e)
     for _ in range(args.warmup):
         sim.run(1)
     barrier()

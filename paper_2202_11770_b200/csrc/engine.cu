@@ -286,15 +286,23 @@ class Engine {
         dist = nccl_id != nullptr;
         rank = rank_;
         nranks = nranks_;
-        validate_setup();
-        omega = 1.0 / prm.tau;  // RelaxationParams (lattice.hpp:83-84), dt = 1
-        part = splbcu::partition(dom, prm.workers);
-        if (dist && nranks != prm.workers) config_error("engine: dist mode needs workers == nranks");
         if (prm.devices.empty()) {
             int cur = 0;
             CK(cudaGetDevice(&cur));
             prm.devices.push_back(cur);
         }
+        if (dist) {
+            // Join the communicator first: every rank reaches this point at
+            // the same time, before the (long) per-rank table build.
+            if (nranks != prm.workers) config_error("engine: dist mode needs workers == nranks");
+            CK(cudaSetDevice(prm.devices[0]));
+            ncclUniqueId id;
+            std::memcpy(&id, nccl_id, sizeof(id));
+            NK(nccl_checked().CommInitRank(&comm, nranks, id, rank));
+        }
+        validate_setup();
+        omega = 1.0 / prm.tau;  // RelaxationParams (lattice.hpp:83-84), dt = 1
+        part = splbcu::partition(dom, prm.workers);
         for (auto& g : dom.iolets) {
             IoletDev x{};
             for (int a = 0; a < 3; ++a) x.center[a] = g.center[a], x.normal[a] = g.normal[a];
@@ -321,12 +329,6 @@ class Engine {
                                       std::to_string(w) + " <-> " + std::to_string(sg.nb));
                 }
             enable_peers();
-        } else {
-            WorkerDev& wk = *W[size_t(rank)];
-            CK(cudaSetDevice(wk.dev));
-            ncclUniqueId id;
-            std::memcpy(&id, nccl_id, sizeof(id));
-            NK(nccl_checked().CommInitRank(&comm, nranks, id, rank));
         }
         if (prm.observe_iolets) init_observation();
         for (auto& wp : W)
