@@ -745,14 +745,18 @@ class Engine {
                                                                b, e, omega);
     }
 
+    // `timed`: the bulk (mid-group) plain launch, whose CUDA-event duration
+    // feeds the roofline; the small edge launches overlap it on another stream.
     void launch_range(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, bool iolet, const double* staged,
-                      const int32_t* coords) {
+                      const int32_t* coords, bool timed) {
         if (e <= b) return;
         IoletArgs ia{wk.io_geo.get<IoletDev>(), staged, coords};
         const unsigned nb = blocks_for(e - b);
         if (iolet) {
             lbm_push<true, 256, 1><<<nb, 256, 0, s>>>(wk.f_old(), wk.f_new(), wk.tab.get<uint32_t>(), wk.P, b, e,
                                                       omega, ia);
+        } else if (!timed) {
+            launch_plain(wk, s, b, e, ia);
         } else {
             cudaEvent_t e0 = nullptr, e1 = nullptr;
             if (kernel_timing) {
@@ -779,11 +783,11 @@ class Engine {
     void advance_group(WorkerDev& wk, cudaStream_t s, bool edge, const double* staged) {
         const int32_t* ioc = wk.io_coords.get<int32_t>();
         if (edge) {
-            launch_range(wk, s, 0, wk.ep, false, staged, ioc);
-            launch_range(wk, s, wk.ep, wk.n_edge, true, staged, ioc);
+            launch_range(wk, s, 0, wk.ep, false, staged, ioc, false);
+            launch_range(wk, s, wk.ep, wk.n_edge, true, staged, ioc, false);
         } else {
-            launch_range(wk, s, wk.n_edge, wk.n_edge + wk.mp, false, staged, ioc);
-            launch_range(wk, s, wk.n_edge + wk.mp, wk.n, true, staged, ioc + 3 * uint64_t(wk.n_edge - wk.ep));
+            launch_range(wk, s, wk.n_edge, wk.n_edge + wk.mp, false, staged, ioc, true);
+            launch_range(wk, s, wk.n_edge + wk.mp, wk.n, true, staged, ioc + 3 * uint64_t(wk.n_edge - wk.ep), false);
         }
     }
 
