@@ -1,0 +1,272 @@
+// splbcu.hpp — the reference's C++ surface (namespace splb, header-only)
+// rebuilt over the C-ABI in splbcu.h.
+//
+// A C++ caller of the reference (proj/include/splb/engine.hpp:121-205) swaps
+//   #include "splb/engine.hpp"   ->   #include "splbcu.hpp"
+// and links libsplbcu.so.  Class names, argument meaning and exception types
+// follow the reference (common.hpp:11-28, geometry.hpp:64-363,
+// decomp.hpp:16-188, boundary.hpp:18-74, engine.hpp:37-205); the time step runs
+// in the B200 kernels behind the C-ABI.  Differences: SparseDomain is an
+// opaque owner of the site arrays (export() copies them out), and store(w)
+// returns a host copy (DistributionStore with f_old()/f_new() vectors) that
+// set_f_old()/set_f_new() write back, because the populations live in HBM.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "splbcu.h"
+
+namespace splb {
+
+struct Error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct DegenerateState : Error {
+    using Error::Error;
+};
+struct GeometryError : Error {
+    using Error::Error;
+};
+struct ConfigError : Error {
+    using Error::Error;
+};
+
+namespace detail {
+inline void check(int rc) {
+    if (rc == SPLBCU_OK) return;
+    const std::string m = splbcu_last_error();
+    switch (rc) {
+        case SPLBCU_ERR_CONFIG: throw ConfigError(m);
+        case SPLBCU_ERR_GEOMETRY: throw GeometryError(m);
+        case SPLBCU_ERR_DEGENERATE: throw DegenerateState(m);
+        default: throw Error(m);
+    }
+}
+}  // namespace detail
+
+using Vec3 = std::array<double, 3>;
+using Vec3i = std::array<int32_t, 3>;
+
+enum class Layout : uint8_t { AoS = 0, SoA = 1 };
+enum class Scheme : uint8_t { Push = 0, Pull = 1 };
+enum class StepSequence : uint8_t { Classic = 0, Reordered = 1 };
+
+struct Iolet {
+    enum class Kind : uint8_t { Inlet = 0, Outlet = 1 };
+    Kind kind;
+    Vec3 center;
+    Vec3 normal;
+    double radius;
+};
+
+// boundary.hpp:18-74
+struct TimeTable {
+    std::vector<std::pair<double, double>> nodes;
+    double period = 0.0;
+    static TimeTable constant(double v) { return TimeTable{{{0.0, v}}, 0.0}; }
+    double at(double t) const {
+        std::vector<double> ts, vs;
+        for (auto& n : nodes) ts.push_back(n.first), vs.push_back(n.second);
+        double out = 0.0;
+        detail::check(splbcu_timetable_at(ts.data(), vs.data(), uint32_t(ts.size()), period, t, &out));
+        return out;
+    }
+};
+
+// engine.hpp:37-44
+struct BCSet {
+    enum class Kind : uint8_t { Pressure = 0, Velocity = 1 };
+    struct Entry {
+        Kind kind = Kind::Pressure;
+        TimeTable table;
+    };
+    std::vector<Entry> entries;
+};
+
+// engine.hpp:46-57 (+ device placement)
+struct EngineParams {
+    double tau = 0.9;
+    double rho0 = 1.0;
+    double dt_s = 1.0;
+    Layout layout = Layout::AoS;
+    Scheme scheme = Scheme::Push;
+    StepSequence sequence = StepSequence::Classic;
+    int workers = 1;
+    uint64_t capture_period = 0;
+    bool observe_iolets = false;
+    double exchange_timeout_s = 30.0;
+    std::vector<int32_t> devices;  // B200: workers placed round robin
+};
+
+// geometry.hpp:64-73 (opaque; site arrays on demand)
+class SparseDomain {
+  public:
+    explicit SparseDomain(splbcu_domain* h) : h_(h, &splbcu_domain_free) {}
+    uint64_t n_sites() const { return splbcu_domain_n_sites(h_.get()); }
+    double voxel_size() const { return splbcu_domain_voxel_size(h_.get()); }
+    splbcu_domain* handle() const { return h_.get(); }
+    void validate() const { detail::check(splbcu_domain_validate(h_.get())); }
+    void write(const std::string& path) const { detail::check(splbcu_domain_write(h_.get(), path.c_str())); }
+    static SparseDomain read(const std::string& path) {
+        splbcu_domain* d = nullptr;
+        detail::check(splbcu_domain_read(path.c_str(), &d));
+        return SparseDomain(d);
+    }
+
+  private:
+    std::shared_ptr<splbcu_domain> h_;
+};
+
+inline splbcu_iolet to_c(const Iolet& io) {
+    splbcu_iolet c{};
+    c.kind = int32_t(io.kind);
+    for (int a = 0; a < 3; ++a) c.center[a] = io.center[a], c.normal[a] = io.normal[a];
+    c.radius = io.radius;
+    return c;
+}
+
+// geometry.hpp:139-208
+inline SparseDomain classify_sites(const std::vector<Vec3i>& voxels, const std::vector<Iolet>& iolets,
+                                   double voxel_size = 1.0) {
+    std::vector<splbcu_iolet> io;
+    for (auto& i : iolets) io.push_back(to_c(i));
+    splbcu_domain* d = nullptr;
+    detail::check(splbcu_domain_classify(reinterpret_cast<const int32_t*>(voxels.data()), voxels.size(), io.data(),
+                                         uint32_t(io.size()), voxel_size, &d));
+    return SparseDomain(d);
+}
+// geometry.hpp:285-308
+inline SparseDomain build_pipe(int radius, int length, double voxel_size = 1.0) {
+    splbcu_domain* d = nullptr;
+    detail::check(splbcu_domain_build_pipe(radius, length, voxel_size, &d));
+    return SparseDomain(d);
+}
+// geometry.hpp:313-363
+inline SparseDomain build_bifurcation(int tr, int br, int tl, int bl, double voxel_size = 1.0) {
+    splbcu_domain* d = nullptr;
+    detail::check(splbcu_domain_build_bifurcation(tr, br, tl, bl, voxel_size, &d));
+    return SparseDomain(d);
+}
+
+struct Capture {
+    uint64_t step = 0;
+    std::vector<double> fields;  // 4 * nSites, (rho, ux, uy, uz) in domain order
+};
+struct PropertyCache {
+    uint64_t capture_period = 0;
+    std::vector<Capture> captures;
+};
+struct IoletSeries {
+    uint64_t rows = 0;
+    std::vector<std::vector<double>> max_speed, pressure, flow;
+};
+
+// Host copy of store(w) (layout.hpp:19-62).
+struct DistributionStore {
+    Layout layout = Layout::AoS;
+    uint32_t n_sites = 0, shared_size = 0;
+    std::vector<double> old_, new_;
+    size_t idx(uint32_t s, int i) const {
+        return layout == Layout::AoS ? size_t(19) * s + size_t(i) : size_t(i) * n_sites + s;
+    }
+    size_t shared_base() const { return size_t(19) * n_sites; }
+    size_t total_size() const { return shared_base() + shared_size; }
+    double* f_old() { return old_.data(); }
+    double* f_new() { return new_.data(); }
+};
+
+// engine.hpp:121-205
+class Simulation {
+  public:
+    Simulation(const SparseDomain& domain, const BCSet& bcs, const EngineParams& p) : domain_(domain), params_(p) {
+        std::vector<std::vector<double>> keep;
+        std::vector<splbcu_bc> bc;
+        for (auto& e : bcs.entries) {
+            std::vector<double> t, v;
+            for (auto& n : e.table.nodes) t.push_back(n.first), v.push_back(n.second);
+            keep.push_back(std::move(t));
+            keep.push_back(std::move(v));
+            bc.push_back({int32_t(e.kind), keep[keep.size() - 2].data(), keep.back().data(),
+                          uint32_t(e.table.nodes.size()), e.table.period});
+        }
+        splbcu_params c;
+        splbcu_params_default(&c);
+        c.tau = p.tau, c.rho0 = p.rho0, c.dt_s = p.dt_s;
+        c.layout = int32_t(p.layout), c.scheme = int32_t(p.scheme), c.sequence = int32_t(p.sequence);
+        c.workers = p.workers, c.capture_period = p.capture_period, c.observe_iolets = p.observe_iolets;
+        c.exchange_timeout_s = p.exchange_timeout_s;
+        c.n_devices = int32_t(p.devices.size());
+        c.device_ids = p.devices.data();
+        splbcu_sim* s = nullptr;
+        detail::check(splbcu_sim_create(domain.handle(), bc.data(), uint32_t(bc.size()), &c, &s));
+        h_.reset(s);
+    }
+
+    void run(uint64_t n_steps) { detail::check(splbcu_sim_run(h_.get(), n_steps)); }
+    uint64_t steps_run() const { return splbcu_sim_steps_run(h_.get()); }
+    double step_loop_seconds() const { return splbcu_sim_step_loop_seconds(h_.get()); }
+    const SparseDomain& domain() const { return domain_; }
+
+    std::vector<double> snapshot_fields() const {
+        std::vector<double> out(4 * domain_.n_sites());
+        detail::check(splbcu_sim_snapshot(h_.get(), out.data()));
+        return out;
+    }
+
+    DistributionStore store(int w) {
+        DistributionStore st;
+        st.layout = params_.layout;
+        detail::check(splbcu_sim_store_shape(h_.get(), w, &st.n_sites, &st.shared_size));
+        st.old_.resize(st.total_size());
+        st.new_.resize(st.total_size());
+        detail::check(splbcu_sim_get_f(h_.get(), w, 0, st.old_.data()));
+        detail::check(splbcu_sim_get_f(h_.get(), w, 1, st.new_.data()));
+        return st;
+    }
+    void set_f_old(int w, const DistributionStore& st) { detail::check(splbcu_sim_set_f(h_.get(), w, 0, st.old_.data())); }
+    void set_f_new(int w, const DistributionStore& st) { detail::check(splbcu_sim_set_f(h_.get(), w, 1, st.new_.data())); }
+
+    PropertyCache cache() const {
+        PropertyCache c;
+        c.capture_period = params_.capture_period;
+        const uint64_t n = splbcu_sim_n_captures(h_.get());
+        for (uint64_t k = 0; k < n; ++k) {
+            Capture cap;
+            cap.fields.resize(4 * domain_.n_sites());
+            detail::check(splbcu_sim_capture(h_.get(), k, &cap.step, cap.fields.data()));
+            c.captures.push_back(std::move(cap));
+        }
+        return c;
+    }
+
+    IoletSeries series() const {
+        IoletSeries s;
+        s.rows = splbcu_sim_series_rows(h_.get());
+        if (!s.rows) return s;
+        const uint32_t nio = splbcu_domain_n_iolets(domain_.handle());
+        for (uint32_t k = 0; k < nio; ++k) {
+            std::vector<double> a(s.rows), b(s.rows), c(s.rows);
+            detail::check(splbcu_sim_series(h_.get(), k, a.data(), b.data(), c.data()));
+            s.max_speed.push_back(std::move(a));
+            s.pressure.push_back(std::move(b));
+            s.flow.push_back(std::move(c));
+        }
+        return s;
+    }
+
+  private:
+    struct Del {
+        void operator()(splbcu_sim* s) const { splbcu_sim_destroy(s); }
+    };
+    SparseDomain domain_;
+    EngineParams params_;
+    std::unique_ptr<splbcu_sim, Del> h_;
+};
+
+}  // namespace splb
