@@ -254,6 +254,10 @@ struct WorkerDev {
     CUtensorMap tm_f[2][2];  // [buffer][box T variant: 0 -> 128 sites, 1 -> 256 sites]
     CUtensorMap tm_t[2];
     bool tma_ok = false;  // maps encoded (planes at least one box long)
+    // compressed table of the mid-group plain range (kernels.cuh: compress_table)
+    DevMem dtab, gbase;
+    uint64_t PG = 0;
+    bool ctab_ok = false;
     size_t tev_used = 0;
 
     double* f_old() const { return fbuf[old].get<double>(); }
@@ -601,6 +605,31 @@ class Engine {
                 encode_planes(&wk.tm_f[b][v], wk.fbuf[b].get<double>(), true, kQ, wk.P, box);
             encode_planes(&wk.tm_t[v], wk.tab.get<uint32_t>(), false, kQ - 1, wk.P, box);
         }
+        // compressed table for the mid-group plain range
+        wk.ctab_ok = false;
+        if (wk.mp > 0) {
+            wk.PG = wk.P / 32 + 2;
+            int16_t* dt = wk.dtab.alloc<int16_t>(18 * wk.P + kTilePad);
+            uint32_t* gb = wk.gbase.alloc<uint32_t>(18 * wk.PG);
+            CK(cudaMemsetAsync(dt, 0, (18 * wk.P + kTilePad) * sizeof(int16_t), s));
+            CK(cudaMemsetAsync(gb, 0, 18 * wk.PG * sizeof(uint32_t), s));
+            DevMem cerr;
+            unsigned* ce = cerr.alloc<unsigned>(1);
+            CK(cudaMemsetAsync(ce, 0, sizeof(unsigned), s));
+            const uint32_t b0 = wk.n_edge, b1 = wk.n_edge + wk.mp;
+            const uint64_t groups = ((b1 + 31) >> 5) - (b0 >> 5);
+            compress_table<<<blocks_for(groups * 18 * 32), 256, 0, s>>>(wk.tab.get<uint32_t>(), wk.P, wk.PG, b0, b1,
+                                                                       dt, gb, ce);
+            CK(cudaGetLastError());
+            unsigned he = 0;
+            CK(cudaMemcpyAsync(&he, ce, sizeof(he), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            wk.ctab_ok = he == 0;
+            if (!wk.ctab_ok) {
+                wk.dtab.release();
+                wk.gbase.release();
+            }
+        }
         CK(cudaStreamSynchronize(s));
     }
 
@@ -664,7 +693,39 @@ class Engine {
         lbm_push<false, T, B><<<unsigned((e - b + T - 1) / T), T, 0, s>>>(wk.f_old(), wk.f_new(),
                                                                           wk.tab.get<uint32_t>(), wk.P, b, e, omega, ia);
     }
-    void launch_plain(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia) {
+    // Persistent TMA kernel over the compressed table (mid-group range only).
+    template <int T, int S, int B>
+    void launch_tmc(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e) {
+        using Lm = PushTmaSmem<T, S, false>;
+        static int cfg_dev = -1, resident = 0;
+        if (cfg_dev != wk.dev) {
+            CK(cudaFuncSetAttribute(lbm_push_tmc<T, S, B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(Lm::kBytes)));
+            int per_sm = 0, sms = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lbm_push_tmc<T, S, B>, T, Lm::kBytes));
+            CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, wk.dev));
+            resident = std::max(1, per_sm) * sms;
+            cfg_dev = wk.dev;
+        }
+        const uint32_t base = b & ~31u;
+        const uint32_t ntiles = (e - base + T - 1) / T;
+        const unsigned grid = unsigned(std::min<uint32_t>(ntiles, uint32_t(resident)));
+        lbm_push_tmc<T, S, B><<<grid, T, Lm::kBytes, s>>>(wk.f_old(), wk.f_new(), wk.dtab.get<int16_t>(),
+                                                           wk.gbase.get<uint32_t>(), wk.P, wk.PG, b, e, omega);
+    }
+
+    void launch_plain(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia, bool mid) {
+        if (plain_variant >= 40 && plain_variant < 50) {
+            if (mid && wk.ctab_ok) {
+                switch (plain_variant) {
+                    case 40: launch_tmc<256, 2, 2>(wk, s, b, e); return;
+                    case 41: launch_tmc<128, 2, 4>(wk, s, b, e); return;
+                    case 42: launch_tmc<128, 2, 3>(wk, s, b, e); return;
+                    default: launch_tmc<256, 2, 2>(wk, s, b, e); return;
+                }
+            }
+            return launch_tma<256, 2, 2, false>(wk, s, b, e);
+        }
         switch (plain_variant) {
             case 1: launch_plain_t<256, 1>(wk, s, b, e, ia); break;
             case 2: launch_plain_t<256, 2>(wk, s, b, e, ia); break;
@@ -756,7 +817,7 @@ class Engine {
             lbm_push<true, 256, 1><<<nb, 256, 0, s>>>(wk.f_old(), wk.f_new(), wk.tab.get<uint32_t>(), wk.P, b, e,
                                                       omega, ia);
         } else if (!timed) {
-            launch_plain(wk, s, b, e, ia);
+            launch_plain(wk, s, b, e, ia, false);
         } else {
             cudaEvent_t e0 = nullptr, e1 = nullptr;
             if (kernel_timing) {
@@ -771,7 +832,7 @@ class Engine {
                 e1 = wk.tev[wk.tev_used++];
                 CK(cudaEventRecord(e0, s));
             }
-            launch_plain(wk, s, b, e, ia);
+            launch_plain(wk, s, b, e, ia, true);
             if (kernel_timing) CK(cudaEventRecord(e1, s));
             plain_launches++;
             plain_sites += e - b;

@@ -242,6 +242,117 @@ lbm_push_tma(const double* __restrict__ fo, double* __restrict__ fn, const uint3
     }
 }
 
+// ---- compressed neighbour table (mid-group plain sites) --------------------
+// The mid-group plain range has only ToLocal and bounce-back links (shared
+// slots occur only at edge sites, iolet links only at iolet sites).  Inside a
+// warp's 32 consecutive sites (zyx order) the ToLocal targets of one direction
+// are consecutive up to small jumps at row ends, so each (direction, 32-site
+// group) stores one u32 base and every site an int16 delta:
+//     target = base + lane + delta,   delta == kDeltaBounce -> (s, inv(i)).
+// 18 x (2 + 4/32) = 38.25 B/site of index traffic instead of 72.
+constexpr int16_t kDeltaBounce = -32768;
+
+// One warp per (direction, 32-site group) over [begin, end); sets *err when a
+// delta does not fit or an unexpected op appears (caller falls back to u32).
+__global__ void compress_table(const uint32_t* __restrict__ tab, uint64_t P, uint64_t PG, uint32_t begin,
+                               uint32_t end, int16_t* __restrict__ dtab, uint32_t* __restrict__ gbase,
+                               unsigned* err) {
+    const uint64_t gw = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = int(threadIdx.x & 31);
+    const uint32_t g0 = begin >> 5, g1 = (end + 31) >> 5;
+    const uint64_t ngroups = g1 - g0;
+    if (gw >= ngroups * 18) return;  // whole warp exits together
+    const int i1 = int(gw / ngroups);  // direction - 1
+    const uint32_t g = g0 + uint32_t(gw % ngroups);
+    const uint32_t s = g * 32 + uint32_t(lane);
+    const bool live = s >= begin && s < end;
+    const uint32_t v = live ? tab[uint64_t(i1) * P + s] : kSpecial;
+    const bool local = live && v < kSpecial;
+    const unsigned m = __ballot_sync(0xffffffffu, local);
+    const int ref = m ? __ffs(int(m)) - 1 : 0;
+    const uint32_t vref = __shfl_sync(0xffffffffu, v, ref);
+    const int64_t base = m ? int64_t(vref) - ref : 0;
+    int16_t d = 0;
+    if (local) {
+        const int64_t dd = int64_t(v) - base - lane;
+        if (dd < -32767 || dd > 32767) atomicExch(err, 1u);
+        d = int16_t(dd);
+    } else if (live) {
+        if (((v >> kOpShift) & 3u) != kOpBounce) atomicExch(err, 2u);
+        d = kDeltaBounce;
+    }
+    if (live) dtab[uint64_t(i1) * P + s] = d;
+    if (lane == 0) gbase[uint64_t(i1) * PG + g] = uint32_t(base < 0 ? 0 : base);
+    if (lane == 0 && base < 0) atomicExch(err, 3u);
+}
+
+// TMA-pipelined persistent plain kernel reading the compressed table.  All
+// 32 lanes run the direction loop (bases travel by warp shuffle); only loads
+// and stores are predicated on the site being in range.
+template <int T, int S, int kMinBlocks>
+__global__ void __launch_bounds__(T, kMinBlocks)
+lbm_push_tmc(const double* __restrict__ fo, double* __restrict__ fn, const int16_t* __restrict__ dtab,
+             const uint32_t* __restrict__ gbase, uint64_t P, uint64_t PG, uint32_t begin, uint32_t end,
+             double omega) {
+    using L = PushTmaSmem<T, S, false>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S * L::kStage);
+    const uint32_t base = begin & ~31u;  // warps cover aligned 32-site groups
+    const uint32_t ntiles = (end - base + T - 1) / T;
+    const uint32_t G = gridDim.x;
+    const uint32_t tid = threadIdx.x;
+    const int lane = int(tid & 31);
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) mbar_init(&bar[s], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    const uint64_t policy = evict_first_policy();
+    auto issue = [&](uint32_t k) {
+        const uint32_t tile = blockIdx.x + k * G;
+        if (tile >= ntiles) return;
+        const int st = int(k % S);
+        unsigned char* buf = smem + st * L::kStage;
+        const uint64_t t0 = uint64_t(base) + uint64_t(tile) * T;
+        mbar_expect_tx(&bar[st], L::kStage);
+#pragma unroll 1
+        for (int i = 0; i < kQ; ++i) bulk_g2s(buf + i * T * 8, fo + uint64_t(i) * P + t0, T * 8, &bar[st], policy);
+    };
+    if (tid == 0)
+        for (uint32_t k = 0; k + 1 < uint32_t(S); ++k) issue(k);
+    for (uint32_t k = 0;; ++k) {
+        const uint32_t tile = blockIdx.x + k * G;
+        if (tile >= ntiles) break;
+        if (tid == 0) issue(k + S - 1);
+        const int st = int(k % S);
+        const uint32_t s = base + tile * T + tid;
+        const bool live = s >= begin && s < end;
+        int16_t dl[kQ - 1];
+#pragma unroll
+        for (int i = 0; i < kQ - 1; ++i) dl[i] = live ? __ldcs(dtab + uint64_t(i) * P + s) : int16_t(0);
+        const uint32_t breg = (lane < kQ - 1) ? __ldcs(gbase + uint64_t(lane) * PG + (s >> 5)) : 0u;
+        mbar_wait(&bar[st], (k / S) & 1u);
+        const double* fs = reinterpret_cast<const double*>(smem + st * L::kStage);
+        double f[kQ];
+#pragma unroll
+        for (int i = 0; i < kQ; ++i) f[i] = fs[i * T + tid];
+        const Macro m = macro_of(f);
+        double feq[kQ];
+        feq_all(m.rho, m.ux, m.uy, m.uz, feq);
+        if (live) fn[s] = relax(f[0], feq[0], omega);
+#pragma unroll
+        for (int i = 1; i < kQ; ++i) {
+            const double fpost = relax(f[i], feq[i], omega);
+            const uint32_t b = __shfl_sync(0xffffffffu, breg, i - 1);
+            const int d = dl[i - 1];
+            const uint64_t dst = d == kDeltaBounce ? uint64_t(inv(i)) * P + s
+                                                   : uint64_t(i) * P + uint64_t(int64_t(b) + lane + d);
+            if (live) fn[dst] = fpost;
+        }
+        __syncthreads();  // stage st is free for the copy issued next iteration
+    }
+}
+
 // ---- warp-specialised 2-D TMA variant --------------------------------------
 // One TMA instruction per tile moves the whole [19 planes x T sites] f box
 // (and, optionally, the [18 x T] table box) described by a CUtensorMap over
