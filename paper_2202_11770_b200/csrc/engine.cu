@@ -9,8 +9,9 @@
 #include <nccl.h>
 
 #include <algorithm>
-#include <cstdlib>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <thread>
@@ -625,6 +626,9 @@ class Engine {
             CK(cudaMemcpyAsync(&he, ce, sizeof(he), cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
             wk.ctab_ok = he == 0;
+            if (std::getenv("SPLBCU_VERBOSE"))
+                std::fprintf(stderr, "[splbcu] worker %d: compressed table %s (code %u)\n", wk.w,
+                             wk.ctab_ok ? "on" : "off", he);
             if (!wk.ctab_ok) {
                 wk.dtab.release();
                 wk.gbase.release();

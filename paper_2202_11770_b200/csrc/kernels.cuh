@@ -282,8 +282,9 @@ __global__ void compress_table(const uint32_t* __restrict__ tab, uint64_t P, uin
         d = kDeltaBounce;
     }
     if (live) dtab[uint64_t(i1) * P + s] = d;
-    if (lane == 0) gbase[uint64_t(i1) * PG + g] = uint32_t(base < 0 ? 0 : base);
-    if (lane == 0 && base < 0) atomicExch(err, 3u);
+    // the base may be "negative" (target of lane 0 below index 0): stored
+    // modulo 2^32, the kernel adds lane + delta in the same arithmetic
+    if (lane == 0) gbase[uint64_t(i1) * PG + g] = uint32_t(uint64_t(base));
 }
 
 // TMA-pipelined persistent plain kernel reading the compressed table.  All
@@ -346,7 +347,7 @@ lbm_push_tmc(const double* __restrict__ fo, double* __restrict__ fn, const int16
             const uint32_t b = __shfl_sync(0xffffffffu, breg, i - 1);
             const int d = dl[i - 1];
             const uint64_t dst = d == kDeltaBounce ? uint64_t(inv(i)) * P + s
-                                                   : uint64_t(i) * P + uint64_t(int64_t(b) + lane + d);
+                                                   : uint64_t(i) * P + uint32_t(b + uint32_t(lane) + uint32_t(d));
             if (live) fn[dst] = fpost;
         }
         __syncthreads();  // stage st is free for the copy issued next iteration
