@@ -715,7 +715,8 @@ class Engine {
         const uint32_t ntiles = (e - base + T - 1) / T;
         const unsigned grid = unsigned(std::min<uint32_t>(ntiles, uint32_t(resident)));
         lbm_push_tmc<T, S, B><<<grid, T, Lm::kBytes, s>>>(wk.f_old(), wk.f_new(), wk.dtab.get<int16_t>(),
-                                                           wk.gbase.get<uint32_t>(), wk.P, wk.PG, b, e, omega);
+                                                           wk.gbase.get<uint32_t>(), wk.tab.get<uint32_t>(), wk.P,
+                                                           wk.PG, b, e, omega);
     }
 
     void launch_plain(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia, bool mid) {

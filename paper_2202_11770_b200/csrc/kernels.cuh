@@ -251,6 +251,7 @@ lbm_push_tma(const double* __restrict__ fo, double* __restrict__ fn, const uint3
 //     target = base + lane + delta,   delta == kDeltaBounce -> (s, inv(i)).
 // 18 x (2 + 4/32) = 38.25 B/site of index traffic instead of 72.
 constexpr int16_t kDeltaBounce = -32768;
+constexpr int16_t kDeltaEscape = -32767;
 
 // One warp per (direction, 32-site group) over [begin, end); sets *err when a
 // delta does not fit or an unexpected op appears (caller falls back to u32).
@@ -275,8 +276,9 @@ __global__ void compress_table(const uint32_t* __restrict__ tab, uint64_t P, uin
     int16_t d = 0;
     if (local) {
         const int64_t dd = int64_t(v) - base - lane;
-        if (dd < -32767 || dd > 32767) atomicExch(err, 1u);
-        d = int16_t(dd);
+        // far targets (e.g. the iolet sites stored after the plain range) take
+        // the escape code and are read from the u32 table
+        d = (dd < -32766 || dd > 32767) ? kDeltaEscape : int16_t(dd);
     } else if (live) {
         if (((v >> kOpShift) & 3u) != kOpBounce) atomicExch(err, 2u);
         d = kDeltaBounce;
@@ -293,8 +295,8 @@ __global__ void compress_table(const uint32_t* __restrict__ tab, uint64_t P, uin
 template <int T, int S, int kMinBlocks>
 __global__ void __launch_bounds__(T, kMinBlocks)
 lbm_push_tmc(const double* __restrict__ fo, double* __restrict__ fn, const int16_t* __restrict__ dtab,
-             const uint32_t* __restrict__ gbase, uint64_t P, uint64_t PG, uint32_t begin, uint32_t end,
-             double omega) {
+             const uint32_t* __restrict__ gbase, const uint32_t* __restrict__ tab, uint64_t P, uint64_t PG,
+             uint32_t begin, uint32_t end, double omega) {
     using L = PushTmaSmem<T, S, false>;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S * L::kStage);
@@ -346,8 +348,10 @@ lbm_push_tmc(const double* __restrict__ fo, double* __restrict__ fn, const int16
             const double fpost = relax(f[i], feq[i], omega);
             const uint32_t b = __shfl_sync(0xffffffffu, breg, i - 1);
             const int d = dl[i - 1];
-            const uint64_t dst = d == kDeltaBounce ? uint64_t(inv(i)) * P + s
-                                                   : uint64_t(i) * P + uint32_t(b + uint32_t(lane) + uint32_t(d));
+            uint64_t dst;
+            if (d == kDeltaBounce) dst = uint64_t(inv(i)) * P + s;
+            else if (d == kDeltaEscape) dst = uint64_t(i) * P + (live ? tab[uint64_t(i - 1) * P + s] : 0u);
+            else dst = uint64_t(i) * P + uint32_t(b + uint32_t(lane) + uint32_t(d));
             if (live) fn[dst] = fpost;
         }
         __syncthreads();  // stage st is free for the copy issued next iteration
