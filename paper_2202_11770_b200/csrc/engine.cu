@@ -751,6 +751,11 @@ class Engine {
             case 20: launch_tma<128, 2, 4, false>(wk, s, b, e); break;
             case 21: launch_tma<256, 2, 2, false>(wk, s, b, e); break;
             case 22: launch_tma<64, 2, 10, false>(wk, s, b, e); break;
+            case 23: launch_tma<256, 2, 2, false, 1>(wk, s, b, e); break;
+            case 24: launch_tma<256, 2, 2, false, 2>(wk, s, b, e); break;
+            case 25: launch_tma<256, 2, 2, false, 3>(wk, s, b, e); break;
+            case 26: launch_tma<256, 3, 1, false>(wk, s, b, e); break;
+            case 27: launch_tma<192, 2, 2, false>(wk, s, b, e); break;
             case 30: launch_ws<128, 2, 3, true>(wk, s, b, e); break;
             case 31: launch_ws<128, 3, 2, true>(wk, s, b, e); break;
             case 32: launch_ws<256, 2, 1, true>(wk, s, b, e); break;
@@ -791,15 +796,15 @@ class Engine {
     }
 
     // Persistent TMA-pipelined launch: grid = resident CTAs (occupancy x SMs).
-    template <int T, int S, int B, bool TS = true>
+    template <int T, int S, int B, bool TS = true, int H = 0>
     void launch_tma(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e) {
         using Lm = PushTmaSmem<T, S, TS>;
         static int cfg_dev = -1, resident = 0;
         if (cfg_dev != wk.dev) {
-            CK(cudaFuncSetAttribute(lbm_push_tma<T, S, B, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            CK(cudaFuncSetAttribute(lbm_push_tma<T, S, B, TS, H>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     int(Lm::kBytes)));
             int per_sm = 0, sms = 0;
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lbm_push_tma<T, S, B, TS>, T, Lm::kBytes));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lbm_push_tma<T, S, B, TS, H>, T, Lm::kBytes));
             CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, wk.dev));
             resident = std::max(1, per_sm) * sms;
             cfg_dev = wk.dev;
@@ -807,7 +812,7 @@ class Engine {
         const uint32_t base = b & ~3u;
         const uint32_t ntiles = (e - base + T - 1) / T;
         const unsigned grid = unsigned(std::min<uint32_t>(ntiles, uint32_t(resident)));
-        lbm_push_tma<T, S, B, TS><<<grid, T, Lm::kBytes, s>>>(wk.f_old(), wk.f_new(), wk.tab.get<uint32_t>(), wk.P,
+        lbm_push_tma<T, S, B, TS, H><<<grid, T, Lm::kBytes, s>>>(wk.f_old(), wk.f_new(), wk.tab.get<uint32_t>(), wk.P,
                                                                b, e, omega);
     }
 

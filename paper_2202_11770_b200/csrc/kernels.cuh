@@ -152,6 +152,11 @@ __device__ __forceinline__ uint64_t evict_first_policy() {
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
+__device__ __forceinline__ uint64_t evict_normal_policy() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
 
 template <int T, int S, bool kTabSmem = true>
 struct PushTmaSmem {
@@ -165,7 +170,9 @@ struct PushTmaSmem {
 // begin rounded down to 4 sites (16-byte bulk-copy alignment); sites outside
 // the range are loaded but neither computed nor stored.  Buffers carry a
 // tail pad of T elements so the last tile's copies stay in bounds.
-template <int T, int S, int kMinBlocks, bool kTabSmem = true>
+// kHints: bit0 = streaming (.cs) stores, bit1 = no L2 evict-first on the
+// bulk loads (tuning knobs; default 0).
+template <int T, int S, int kMinBlocks, bool kTabSmem = true, int kHints = 0>
 __global__ void __launch_bounds__(T, kMinBlocks)
 lbm_push_tma(const double* __restrict__ fo, double* __restrict__ fn, const uint32_t* __restrict__ tab,
              uint64_t P, uint32_t begin, uint32_t end, double omega) {
@@ -181,7 +188,7 @@ lbm_push_tma(const double* __restrict__ fo, double* __restrict__ fn, const uint3
         mbar_fence_init();
     }
     __syncthreads();
-    const uint64_t policy = evict_first_policy();
+    const uint64_t policy = (kHints & 2) ? evict_normal_policy() : evict_first_policy();
     auto issue = [&](uint32_t k) {
         const uint32_t tile = blockIdx.x + k * G;
         if (tile >= ntiles) return;
@@ -235,7 +242,8 @@ lbm_push_tma(const double* __restrict__ fo, double* __restrict__ fn, const uint3
                 if (v < kSpecial) dst = uint64_t(i) * P + v;
                 else if (((v >> kOpShift) & 3u) == kOpShared) dst = uint64_t(kQ) * P + (v & kPayload);
                 else dst = uint64_t(inv(i)) * P + s;
-                fn[dst] = fpost;
+                if constexpr ((kHints & 1) != 0) __stcs(fn + dst, fpost);
+                else fn[dst] = fpost;
             }
         }
         __syncthreads();  // stage st is free for the copy issued next iteration
