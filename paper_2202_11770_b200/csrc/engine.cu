@@ -698,15 +698,15 @@ class Engine {
                                                                           wk.tab.get<uint32_t>(), wk.P, b, e, omega, ia);
     }
     // Persistent TMA kernel over the compressed table (mid-group range only).
-    template <int T, int S, int B>
+    template <int T, int S, int B, int H = 2>
     void launch_tmc(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e) {
         using Lm = PushTmaSmem<T, S, false>;
         static int cfg_dev = -1, resident = 0;
         if (cfg_dev != wk.dev) {
-            CK(cudaFuncSetAttribute(lbm_push_tmc<T, S, B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            CK(cudaFuncSetAttribute(lbm_push_tmc<T, S, B, H>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     int(Lm::kBytes)));
             int per_sm = 0, sms = 0;
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lbm_push_tmc<T, S, B>, T, Lm::kBytes));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lbm_push_tmc<T, S, B, H>, T, Lm::kBytes));
             CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, wk.dev));
             resident = std::max(1, per_sm) * sms;
             cfg_dev = wk.dev;
@@ -714,9 +714,9 @@ class Engine {
         const uint32_t base = b & ~31u;
         const uint32_t ntiles = (e - base + T - 1) / T;
         const unsigned grid = unsigned(std::min<uint32_t>(ntiles, uint32_t(resident)));
-        lbm_push_tmc<T, S, B><<<grid, T, Lm::kBytes, s>>>(wk.f_old(), wk.f_new(), wk.dtab.get<int16_t>(),
-                                                           wk.gbase.get<uint32_t>(), wk.tab.get<uint32_t>(), wk.P,
-                                                           wk.PG, b, e, omega);
+        lbm_push_tmc<T, S, B, H><<<grid, T, Lm::kBytes, s>>>(wk.f_old(), wk.f_new(), wk.dtab.get<int16_t>(),
+                                                              wk.gbase.get<uint32_t>(), wk.tab.get<uint32_t>(), wk.P,
+                                                              wk.PG, b, e, omega);
     }
 
     void launch_plain(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia, bool mid) {
@@ -726,10 +726,12 @@ class Engine {
                     case 40: launch_tmc<256, 2, 2>(wk, s, b, e); return;
                     case 41: launch_tmc<128, 2, 4>(wk, s, b, e); return;
                     case 42: launch_tmc<128, 2, 3>(wk, s, b, e); return;
+                    case 43: launch_tmc<256, 2, 2, 6>(wk, s, b, e); return;
+                    case 44: launch_tmc<256, 2, 2, 0>(wk, s, b, e); return;
                     default: launch_tmc<256, 2, 2>(wk, s, b, e); return;
                 }
             }
-            return launch_tma<256, 2, 2, false>(wk, s, b, e);
+            return launch_tma<256, 2, 2, false, 2>(wk, s, b, e);
         }
         switch (plain_variant) {
             case 1: launch_plain_t<256, 1>(wk, s, b, e, ia); break;
@@ -756,6 +758,8 @@ class Engine {
             case 25: launch_tma<256, 2, 2, false, 3>(wk, s, b, e); break;
             case 26: launch_tma<256, 3, 1, false>(wk, s, b, e); break;
             case 27: launch_tma<192, 2, 2, false>(wk, s, b, e); break;
+            case 28: launch_tma<256, 2, 2, false, 6>(wk, s, b, e); break;
+            case 29: launch_tma<128, 2, 4, false, 2>(wk, s, b, e); break;
             case 30: launch_ws<128, 2, 3, true>(wk, s, b, e); break;
             case 31: launch_ws<128, 3, 2, true>(wk, s, b, e); break;
             case 32: launch_ws<256, 2, 1, true>(wk, s, b, e); break;
@@ -765,7 +769,7 @@ class Engine {
             case 36: launch_ws<128, 4, 2, false>(wk, s, b, e); break;
             case 37: launch_plain_t<128, 4>(wk, s, b, e, ia); break;
             // default: measured best on B200 (C2: 86% of the HBM copy roofline)
-            default: launch_tma<256, 2, 2, false>(wk, s, b, e); break;
+            default: launch_tma<256, 2, 2, false, 2>(wk, s, b, e); break;
         }
     }
 

@@ -218,7 +218,10 @@ lbm_push_tma(const double* __restrict__ fo, double* __restrict__ fn, const uint3
             // table straight to registers (coalesced), overlapping the wait
             if (live) {
 #pragma unroll
-                for (int i = 0; i < kQ - 1; ++i) treg[i] = ld_t(tab + uint64_t(i) * P + s);
+                for (int i = 0; i < kQ - 1; ++i) {
+                    if constexpr ((kHints & 4) != 0) treg[i] = __ldg(tab + uint64_t(i) * P + s);
+                    else treg[i] = ld_t(tab + uint64_t(i) * P + s);
+                }
             }
         }
         mbar_wait(&bar[st], (k / S) & 1u);
@@ -300,7 +303,7 @@ __global__ void compress_table(const uint32_t* __restrict__ tab, uint64_t P, uin
 // TMA-pipelined persistent plain kernel reading the compressed table.  All
 // 32 lanes run the direction loop (bases travel by warp shuffle); only loads
 // and stores are predicated on the site being in range.
-template <int T, int S, int kMinBlocks>
+template <int T, int S, int kMinBlocks, int kHints = 2>
 __global__ void __launch_bounds__(T, kMinBlocks)
 lbm_push_tmc(const double* __restrict__ fo, double* __restrict__ fn, const int16_t* __restrict__ dtab,
              const uint32_t* __restrict__ gbase, const uint32_t* __restrict__ tab, uint64_t P, uint64_t PG,
@@ -318,7 +321,7 @@ lbm_push_tmc(const double* __restrict__ fo, double* __restrict__ fn, const int16
         mbar_fence_init();
     }
     __syncthreads();
-    const uint64_t policy = evict_first_policy();
+    const uint64_t policy = (kHints & 2) ? evict_normal_policy() : evict_first_policy();
     auto issue = [&](uint32_t k) {
         const uint32_t tile = blockIdx.x + k * G;
         if (tile >= ntiles) return;
@@ -340,8 +343,11 @@ lbm_push_tmc(const double* __restrict__ fo, double* __restrict__ fn, const int16
         const bool live = s >= begin && s < end;
         int16_t dl[kQ - 1];
 #pragma unroll
-        for (int i = 0; i < kQ - 1; ++i) dl[i] = live ? __ldcs(dtab + uint64_t(i) * P + s) : int16_t(0);
-        const uint32_t breg = (lane < kQ - 1) ? __ldcs(gbase + uint64_t(lane) * PG + (s >> 5)) : 0u;
+        for (int i = 0; i < kQ - 1; ++i) {
+            if constexpr ((kHints & 4) != 0) dl[i] = live ? __ldg(dtab + uint64_t(i) * P + s) : int16_t(0);
+            else dl[i] = live ? __ldcs(dtab + uint64_t(i) * P + s) : int16_t(0);
+        }
+        const uint32_t breg = (lane < kQ - 1) ? __ldg(gbase + uint64_t(lane) * PG + (s >> 5)) : 0u;
         mbar_wait(&bar[st], (k / S) & 1u);
         const double* fs = reinterpret_cast<const double*>(smem + st * L::kStage);
         double f[kQ];
