@@ -769,7 +769,13 @@ class Engine {
             case 36: launch_ws<128, 4, 2, false>(wk, s, b, e); break;
             case 37: launch_plain_t<128, 4>(wk, s, b, e, ia); break;
             // default: measured best on B200 (C2: 86% of the HBM copy roofline)
-            default: launch_tma<256, 2, 2, false, 2>(wk, s, b, e); break;
+            // default: measured best on B200 — compressed table for the bulk
+            // (mid) range, u32 table elsewhere; L2 evict-normal bulk loads and
+            // read-only-path table loads (C2 ~93 %, C3 ~89 % of the copy roofline)
+            default:
+                if (mid && wk.ctab_ok) launch_tmc<256, 2, 2, 6>(wk, s, b, e);
+                else launch_tma<256, 2, 2, false, 6>(wk, s, b, e);
+                break;
         }
     }
 
