@@ -176,6 +176,8 @@ def main():
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--quick", action="store_true", help="kernel-only number (tuning runs)")
+    ap.add_argument("--halo", default="nccl", choices=["nccl", "p2p"],
+                    help="N>1 halo exchange: NCCL send/recv + PostReceive, or fused NVLink P2P stores")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -209,7 +211,8 @@ def main():
     t_setup = time.time()
     d, bcs, p, desc = workload(P, name, args.scale)
     n = d.n_sites()
-    sim = make_sim(P.EngineParams(workers=world, devices=[local], **p))
+    halo_mode = 1 if args.halo == "p2p" else 0
+    sim = make_sim(P.EngineParams(workers=world, devices=[local], halo_mode=halo_mode, **p))
     setup_s = time.time() - t_setup
 
     def barrier():
@@ -265,7 +268,7 @@ def main():
         return
     # e2e through the public API: run(1) per step with the iolet series on
     sim.close()
-    params_e = P.EngineParams(workers=world, devices=[local], observe_iolets=True, **p)
+    params_e = P.EngineParams(workers=world, devices=[local], observe_iolets=True, halo_mode=halo_mode, **p)
     sim = make_sim(params_e)
     for _ in range(args.warmup):
         sim.run(1)
@@ -304,6 +307,8 @@ def main():
                 "warmup": args.warmup, "ms_per_step": dev_s / args.steps * 1e3, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": desc, "sites": n, "parallelism": f"slab decomposition x{world}",
+                           "halo": (("NCCL send/recv + PostReceive" if halo_mode == 0 else "fused NVLink P2P stores")
+                                    if world > 1 else "none"),
                            "l2": "inputs (f, table) 3.8 GB per step >> 126 MB L2; no flush needed",
                            "setup_s": round(setup_s, 2)},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,

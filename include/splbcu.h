@@ -92,6 +92,11 @@ typedef struct splbcu_params {
      * n_devices == 0 means {current device}. */
     int32_t n_devices;
     const int32_t* device_ids;
+    /* B200 extension: halo exchange between workers.  0 = NCCL send/recv of
+     * the shared tail (one process per GPU) or peer copies (in-process), then
+     * PostReceive; 1 = fused NVLink P2P: the edge kernels store cut-crossing
+     * links straight into the neighbour's f_new (§8f.4 of SURVEY.md). */
+    int32_t halo_mode;
 } splbcu_params;
 
 typedef struct splbcu_domain splbcu_domain;       /* splb::SparseDomain */

@@ -102,6 +102,7 @@ struct EngineParams {
     bool observe_iolets = false;
     double exchange_timeout_s = 30.0;
     std::vector<int32_t> devices;  // B200: workers placed round robin
+    int32_t halo_mode = 0;         // B200: 0 NCCL/peer copies, 1 fused NVLink P2P stores
 };
 
 // geometry.hpp:64-73 (opaque; site arrays on demand)
@@ -201,6 +202,7 @@ class Simulation {
         c.layout = int32_t(p.layout), c.scheme = int32_t(p.scheme), c.sequence = int32_t(p.sequence);
         c.workers = p.workers, c.capture_period = p.capture_period, c.observe_iolets = p.observe_iolets;
         c.exchange_timeout_s = p.exchange_timeout_s;
+        c.halo_mode = p.halo_mode;
         c.n_devices = int32_t(p.devices.size());
         c.device_ids = p.devices.data();
         splbcu_sim* s = nullptr;

@@ -9,6 +9,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -69,6 +70,41 @@ static EncodeTiledFn encode_fn() {
         fn = reinterpret_cast<EncodeTiledFn>(p);
     }
     return fn;
+}
+
+// Stream memory operations (driver API) for the P2P halo's step flags.
+using StreamValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+struct StreamMemOps {
+    StreamValueFn wait = nullptr, write = nullptr;
+};
+static const StreamMemOps& stream_mem_ops() {
+    static StreamMemOps ops = [] {
+        StreamMemOps o;
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPointByVersion("cuStreamWaitValue32", &p, 12000, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            o.wait = reinterpret_cast<StreamValueFn>(p);
+        p = nullptr;
+        if (cudaGetDriverEntryPointByVersion("cuStreamWriteValue32", &p, 12000, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            o.write = reinterpret_cast<StreamValueFn>(p);
+        return o;
+    }();
+    if (!ops.wait || !ops.write) fail(ErrKind::Cuda, "stream memory operations unavailable");
+    return ops;
+}
+static void wait_geq(cudaStream_t s, const uint32_t* addr, uint32_t v) {
+    const CUresult r = stream_mem_ops().wait(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(addr), v,
+                                             CU_STREAM_WAIT_VALUE_GEQ);
+    if (r != CUDA_SUCCESS) fail(ErrKind::Cuda, "cuStreamWaitValue32 failed (" + std::to_string(int(r)) + ")");
+}
+static void write_flag(cudaStream_t s, uint32_t* addr, uint32_t v) {
+    // default flags: the write is ordered after the stream's prior work and
+    // preceded by a memory barrier, so the halo stores are visible first
+    const CUresult r = stream_mem_ops().write(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(addr), v,
+                                              CU_STREAM_WRITE_VALUE_DEFAULT);
+    if (r != CUDA_SUCCESS) fail(ErrKind::Cuda, "cuStreamWriteValue32 failed (" + std::to_string(int(r)) + ")");
 }
 
 // 2-D map over `planes` direction planes of pitch P: dim0 = site, dim1 = plane;
@@ -259,6 +295,12 @@ struct WorkerDev {
     DevMem dtab, gbase;
     uint64_t PG = 0;
     bool ctab_ok = false;
+    // fused P2P halo: per shared slot the neighbour index and final flat
+    // destination; neighbours' f buffers and flag words (peer-mapped)
+    DevMem slot_peer, slot_dst, flags;  // flags: [0,W) halo_in from v, [W,2W) peer_done of v
+    std::vector<std::array<double*, 2>> peer_f;  // by segment index
+    std::vector<uint32_t*> peer_flags;           // by segment index
+    std::vector<void*> ipc_opened;               // dist mode: handles to close
     size_t tev_used = 0;
 
     double* f_old() const { return fbuf[old].get<double>(); }
@@ -284,6 +326,7 @@ class Engine {
     double loop_s = 0.0, dev_loop_s = 0.0, plain_s = 0.0;
     uint64_t plain_launches = 0, plain_sites = 0, launches = 0;
     bool kernel_timing = false;
+    bool p2p_mode = false;
     std::vector<IoletDev> io_host;
 
     Engine(const Domain& d, std::vector<BCEntry> b, Params p, int rank_, int nranks_, const void* nccl_id)
@@ -335,12 +378,122 @@ class Engine {
                 }
             enable_peers();
         }
+        p2p_mode = prm.halo_mode == 1;
+        if (p2p_mode) setup_p2p();
         if (prm.observe_iolets) init_observation();
         for (auto& wp : W)
             if (wp) CK(cudaStreamSynchronize(wp->sM));
     }
 
+    // NCCL all-reduce of one int on the local worker's stream: a barrier.
+    void dist_barrier() {
+        WorkerDev& wk = *W[size_t(rank)];
+        CK(cudaSetDevice(wk.dev));
+        DevMem one;
+        int* d = one.alloc<int>(1);
+        CK(cudaMemsetAsync(d, 0, sizeof(int), wk.sE));
+        NK(nccl().AllReduce(d, d, 1, ncclInt, ncclSum, comm, wk.sE));
+        CK(cudaStreamSynchronize(wk.sE));
+    }
+
+    // Fused P2P halo (§8f.4): map the neighbours' f buffers and flag words,
+    // and give every outgoing shared slot its final destination in the
+    // neighbour's f_new (the neighbour's recv_dest for that slot,
+    // ExchangePlan::final_dest, exchange.hpp:20).
+    void setup_p2p() {
+        if (dist && !nccl().AllReduce) fail(ErrKind::Comm, "exchange failure: NCCL all-reduce unavailable");
+        for (auto& wp : W) {
+            if (!wp) continue;
+            WorkerDev& wk = *wp;
+            CK(cudaSetDevice(wk.dev));
+            if (wk.segs.size() > size_t(kMaxPeers))
+                config_error("engine: fused P2P halo supports at most " + std::to_string(kMaxPeers) + " neighbours");
+            uint32_t* fl = wk.flags.alloc<uint32_t>(2 * size_t(prm.workers));
+            CK(cudaMemset(fl, 0, 2 * size_t(prm.workers) * sizeof(uint32_t)));
+        }
+        if (!dist) {
+            for (auto& wp : W) {
+                WorkerDev& wk = *wp;
+                std::vector<uint8_t> sp(std::max<uint32_t>(wk.shared, 1), 0);
+                std::vector<uint64_t> sd(std::max<uint32_t>(wk.shared, 1), 0);
+                wk.peer_f.clear();
+                wk.peer_flags.clear();
+                for (size_t k = 0; k < wk.segs.size(); ++k) {
+                    const Seg& sg = wk.segs[k];
+                    WorkerDev& peer = *W[size_t(sg.nb)];
+                    const Seg* ps = find_seg(peer, wk.w);
+                    std::vector<uint64_t> prf(sg.count);
+                    CK(cudaSetDevice(peer.dev));
+                    if (sg.count)
+                        CK(cudaMemcpy(prf.data(), peer.recv_flat.get<uint64_t>() + ps->base, sg.count * 8,
+                                      cudaMemcpyDeviceToHost));
+                    for (uint32_t j = 0; j < sg.count; ++j) sp[sg.base + j] = uint8_t(k), sd[sg.base + j] = prf[j];
+                    wk.peer_f.push_back({peer.fbuf[0].get<double>(), peer.fbuf[1].get<double>()});
+                    wk.peer_flags.push_back(peer.flags.get<uint32_t>());
+                }
+                CK(cudaSetDevice(wk.dev));
+                upload(wk.slot_peer, sp, wk.sM);
+                upload(wk.slot_dst, sd, wk.sM);
+                CK(cudaStreamSynchronize(wk.sM));
+            }
+            return;
+        }
+        // one process per GPU: IPC handles all-gathered over NCCL
+        WorkerDev& wk = *W[size_t(rank)];
+        CK(cudaSetDevice(wk.dev));
+        constexpr size_t H = sizeof(cudaIpcMemHandle_t);
+        std::vector<cudaIpcMemHandle_t> mine(3);
+        CK(cudaIpcGetMemHandle(&mine[0], wk.fbuf[0].p));
+        CK(cudaIpcGetMemHandle(&mine[1], wk.fbuf[1].p));
+        CK(cudaIpcGetMemHandle(&mine[2], wk.flags.p));
+        DevMem dsend, drecv;
+        char* ds = dsend.alloc<char>(3 * H);
+        char* dr = drecv.alloc<char>(3 * H * size_t(nranks));
+        CK(cudaMemcpy(ds, mine.data(), 3 * H, cudaMemcpyHostToDevice));
+        NK(nccl().AllGather(ds, dr, 3 * H, ncclChar, comm, wk.sE));
+        std::vector<cudaIpcMemHandle_t> all(3 * size_t(nranks));
+        CK(cudaMemcpyAsync(all.data(), dr, 3 * H * size_t(nranks), cudaMemcpyDeviceToHost, wk.sE));
+        CK(cudaStreamSynchronize(wk.sE));
+        wk.peer_f.clear();
+        wk.peer_flags.clear();
+        for (const Seg& sg : wk.segs) {
+            std::array<double*, 2> pf{};
+            for (int b = 0; b < 3; ++b) {
+                void* p = nullptr;
+                CK(cudaIpcOpenMemHandle(&p, all[3 * size_t(sg.nb) + size_t(b)], cudaIpcMemLazyEnablePeerAccess));
+                wk.ipc_opened.push_back(p);
+                if (b < 2) pf[size_t(b)] = static_cast<double*>(p);
+                else wk.peer_flags.push_back(static_cast<uint32_t*>(p));
+            }
+            wk.peer_f.push_back(pf);
+        }
+        // final destinations: each side sends its recv_dest slice for the pair
+        uint64_t* sd = wk.slot_dst.alloc<uint64_t>(std::max<uint32_t>(wk.shared, 1));
+        std::vector<uint8_t> sp(std::max<uint32_t>(wk.shared, 1), 0);
+        for (size_t k = 0; k < wk.segs.size(); ++k)
+            for (uint32_t j = 0; j < wk.segs[k].count; ++j) sp[wk.segs[k].base + j] = uint8_t(k);
+        upload(wk.slot_peer, sp, wk.sE);
+        const NcclApi& N = nccl();
+        NK(N.GroupStart());
+        for (const Seg& sg : wk.segs) {
+            NK(N.Send(wk.recv_flat.get<uint64_t>() + sg.base, sg.count, ncclUint64, sg.nb, comm, wk.sE));
+            NK(N.Recv(sd + sg.base, sg.count, ncclUint64, sg.nb, comm, wk.sE));
+        }
+        NK(N.GroupEnd());
+        CK(cudaStreamSynchronize(wk.sE));
+        dist_barrier();
+    }
+
     ~Engine() {
+        if (p2p_mode && dist && comm) {
+            try {
+                dist_barrier();  // no neighbour still stores into our buffers
+            } catch (...) {
+            }
+        }
+        for (auto& wp : W)
+            if (wp)
+                for (void* p : wp->ipc_opened) cudaIpcCloseMemHandle(p);
         if (comm) nccl().CommDestroy(comm);
         for (auto& wp : W) {
             if (!wp) continue;
@@ -694,8 +847,8 @@ class Engine {
     }();
     template <int T, int B>
     void launch_plain_t(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia) {
-        lbm_push<false, T, B><<<unsigned((e - b + T - 1) / T), T, 0, s>>>(wk.f_old(), wk.f_new(),
-                                                                          wk.tab.get<uint32_t>(), wk.P, b, e, omega, ia);
+        lbm_push<false, T, B><<<unsigned((e - b + T - 1) / T), T, 0, s>>>(
+            wk.f_old(), wk.f_new(), wk.tab.get<uint32_t>(), wk.P, b, e, omega, ia, HaloArgs{});
     }
     // Persistent TMA kernel over the compressed table (mid-group range only).
     template <int T, int S, int B, int H = 2>
@@ -806,15 +959,16 @@ class Engine {
     }
 
     // Persistent TMA-pipelined launch: grid = resident CTAs (occupancy x SMs).
-    template <int T, int S, int B, bool TS = true, int H = 0>
-    void launch_tma(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e) {
+    template <int T, int S, int B, bool TS = true, int H = 0, bool P2 = false>
+    void launch_tma(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const HaloArgs& halo = HaloArgs{}) {
         using Lm = PushTmaSmem<T, S, TS>;
         static int cfg_dev = -1, resident = 0;
         if (cfg_dev != wk.dev) {
-            CK(cudaFuncSetAttribute(lbm_push_tma<T, S, B, TS, H>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            CK(cudaFuncSetAttribute(lbm_push_tma<T, S, B, TS, H, P2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     int(Lm::kBytes)));
             int per_sm = 0, sms = 0;
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lbm_push_tma<T, S, B, TS, H>, T, Lm::kBytes));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lbm_push_tma<T, S, B, TS, H, P2>, T,
+                                                             Lm::kBytes));
             CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, wk.dev));
             resident = std::max(1, per_sm) * sms;
             cfg_dev = wk.dev;
@@ -822,20 +976,41 @@ class Engine {
         const uint32_t base = b & ~3u;
         const uint32_t ntiles = (e - base + T - 1) / T;
         const unsigned grid = unsigned(std::min<uint32_t>(ntiles, uint32_t(resident)));
-        lbm_push_tma<T, S, B, TS, H><<<grid, T, Lm::kBytes, s>>>(wk.f_old(), wk.f_new(), wk.tab.get<uint32_t>(), wk.P,
-                                                               b, e, omega);
+        lbm_push_tma<T, S, B, TS, H, P2><<<grid, T, Lm::kBytes, s>>>(wk.f_old(), wk.f_new(), wk.tab.get<uint32_t>(),
+                                                                   wk.P, b, e, omega, halo);
+    }
+
+    // Halo arguments of this step for the fused P2P path: the neighbours'
+    // current f_new (all workers swap in lockstep, so the parity is ours).
+    HaloArgs halo_args(const WorkerDev& wk) const {
+        HaloArgs h{};
+        for (size_t k = 0; k < wk.peer_f.size(); ++k) h.peer_fn[k] = wk.peer_f[k][1 - wk.old];
+        h.slot_peer = wk.slot_peer.get<uint8_t>();
+        h.slot_dst = wk.slot_dst.get<uint64_t>();
+        return h;
     }
 
     // `timed`: the bulk (mid-group) plain launch, whose CUDA-event duration
     // feeds the roofline; the small edge launches overlap it on another stream.
+    // `edge` launches store cut-crossing links to the neighbours in P2P mode.
     void launch_range(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, bool iolet, const double* staged,
-                      const int32_t* coords, bool timed) {
+                      const int32_t* coords, bool timed, bool edge = false) {
         if (e <= b) return;
         IoletArgs ia{wk.io_geo.get<IoletDev>(), staged, coords};
         const unsigned nb = blocks_for(e - b);
+        const bool p2p = edge && p2p_mode && wk.shared > 0;
         if (iolet) {
-            lbm_push<true, 256, 1><<<nb, 256, 0, s>>>(wk.f_old(), wk.f_new(), wk.tab.get<uint32_t>(), wk.P, b, e,
-                                                      omega, ia);
+            if (p2p)
+                lbm_push<true, 256, 1, true><<<nb, 256, 0, s>>>(wk.f_old(), wk.f_new(), wk.tab.get<uint32_t>(), wk.P, b,
+                                                                e, omega, ia, halo_args(wk));
+            else
+                lbm_push<true, 256, 1><<<nb, 256, 0, s>>>(wk.f_old(), wk.f_new(), wk.tab.get<uint32_t>(), wk.P, b, e,
+                                                          omega, ia, HaloArgs{});
+        } else if (p2p) {
+            if (wk.tma_ok) launch_tma<256, 2, 2, false, 6, true>(wk, s, b, e, halo_args(wk));
+            else
+                lbm_push<false, 128, 4, true><<<unsigned((e - b + 127) / 128), 128, 0, s>>>(
+                    wk.f_old(), wk.f_new(), wk.tab.get<uint32_t>(), wk.P, b, e, omega, ia, halo_args(wk));
         } else if (!timed) {
             launch_plain(wk, s, b, e, ia, false);
         } else {
@@ -864,8 +1039,8 @@ class Engine {
     void advance_group(WorkerDev& wk, cudaStream_t s, bool edge, const double* staged) {
         const int32_t* ioc = wk.io_coords.get<int32_t>();
         if (edge) {
-            launch_range(wk, s, 0, wk.ep, false, staged, ioc, false);
-            launch_range(wk, s, wk.ep, wk.n_edge, true, staged, ioc, false);
+            launch_range(wk, s, 0, wk.ep, false, staged, ioc, false, true);
+            launch_range(wk, s, wk.ep, wk.n_edge, true, staged, ioc, false, true);
         } else {
             launch_range(wk, s, wk.n_edge, wk.n_edge + wk.mp, false, staged, ioc, true);
             launch_range(wk, s, wk.n_edge + wk.mp, wk.n, true, staged, ioc + 3 * uint64_t(wk.n_edge - wk.ep), false);
@@ -1067,7 +1242,52 @@ class Engine {
     }
 
     // advance_one (engine.hpp:330-363) for every local worker.
+    // Fused P2P step: the edge kernels store cut-crossing links straight into
+    // the neighbours' f_new over NVLink; stream-ordered flag words replace
+    // send/recv: wait until a neighbour is done reading the buffer we write
+    // (its previous step), publish "halo delivered" after the edge kernels,
+    // and wait for every neighbour's delivery before the step ends.
+    void step_once_p2p(uint64_t k, uint64_t staged_off) {
+        const uint32_t g = uint32_t(steps_run + k);  // global step index
+        const size_t Wn = size_t(prm.workers);
+        for (auto& wp : W) {
+            if (!wp) continue;
+            WorkerDev& wk = *wp;
+            CK(cudaSetDevice(wk.dev));
+            const uint32_t* fl = wk.flags.get<uint32_t>();
+            for (const Seg& sg : wk.segs) wait_geq(wk.sE, fl + Wn + size_t(sg.nb), g);  // peer_done
+            advance_group(wk, wk.sE, true, wk.staged.get<double>() + staged_off);
+            for (size_t j = 0; j < wk.segs.size(); ++j) write_flag(wk.sE, wk.peer_flags[j] + wk.w, g + 1);  // halo_in
+        }
+        for (auto& wp : W) {
+            if (!wp) continue;
+            WorkerDev& wk = *wp;
+            CK(cudaSetDevice(wk.dev));
+            advance_group(wk, wk.sM, false, wk.staged.get<double>() + staged_off);
+            CK(cudaEventRecord(wk.evMid, wk.sM));
+        }
+        const uint64_t done = steps_run + k + 1;
+        for (auto& wp : W) {
+            if (!wp) continue;
+            WorkerDev& wk = *wp;
+            CK(cudaSetDevice(wk.dev));
+            CK(cudaStreamWaitEvent(wk.sE, wk.evMid, 0));
+            const uint32_t* fl = wk.flags.get<uint32_t>();
+            for (const Seg& sg : wk.segs) wait_geq(wk.sE, fl + size_t(sg.nb), g + 1);  // halos landed
+            if (prm.capture_period > 0 && done % prm.capture_period == 0)
+                record_state(wk, wk.sE, done, wk.f_new());
+            else if (prm.observe_iolets)
+                observe(wk, wk.sE, wk.f_new(), done);
+            for (size_t j = 0; j < wk.segs.size(); ++j)
+                write_flag(wk.sE, wk.peer_flags[j] + Wn + size_t(wk.w), g + 1);  // done reading f_old(g)
+            CK(cudaEventRecord(wk.evEnd, wk.sE));
+            CK(cudaStreamWaitEvent(wk.sM, wk.evEnd, 0));
+            wk.old = 1 - wk.old;
+        }
+    }
+
     void step_once(uint64_t k, uint64_t staged_off) {
+        if (p2p_mode) return step_once_p2p(k, staged_off);
         const bool classic = prm.sequence == 0;
         // PreSend: edge sites
         for (auto& wp : W) {

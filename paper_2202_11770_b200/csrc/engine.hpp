@@ -21,6 +21,7 @@ struct Params {
     uint64_t capture_period = 0;
     bool observe_iolets = false;
     double exchange_timeout_s = 30.0;
+    int halo_mode = 0;  // 0: NCCL send/recv (dist) or peer copies; 1: fused P2P stores
     std::vector<int> devices;
 };
 

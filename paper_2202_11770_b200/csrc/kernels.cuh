@@ -62,12 +62,29 @@ struct IoletArgs {
     const int32_t* coords;   // 3 ints per site of this launch's range, [s - begin]
 };
 
+// Fused halo (NVLink P2P): a cut-crossing link's post-collision value is
+// stored straight into the neighbour GPU's f_new at its final destination
+// (ExchangePlan::final_dest, exchange.hpp:20) instead of the local shared
+// tail, so no send/recv and no PostReceive pass is needed.
+constexpr int kMaxPeers = 8;
+struct HaloArgs {
+    double* peer_fn[kMaxPeers];  // neighbours' f_new this step (peer-mapped)
+    const uint8_t* slot_peer;    // per shared slot: index into peer_fn
+    const uint64_t* slot_dst;    // per shared slot: flat index in that f_new
+};
+
+template <bool kP2P>
+__device__ __forceinline__ void store_shared(double* fn, uint64_t P, uint32_t slot, double v, const HaloArgs& h) {
+    if constexpr (kP2P) h.peer_fn[h.slot_peer[slot]][h.slot_dst[slot]] = v;
+    else fn[uint64_t(kQ) * P + slot] = v;
+}
+
 // Fused collide + push-stream over sites [begin, end) (update_push,
 // engine.hpp:404-433).  One thread per site.
-template <bool kIolets, int kThreads, int kMinBlocks>
+template <bool kIolets, int kThreads, int kMinBlocks, bool kP2P = false>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
 lbm_push(const double* __restrict__ fo, double* __restrict__ fn, const uint32_t* __restrict__ tab,
-         uint64_t P, uint32_t begin, uint32_t end, double omega, IoletArgs ia) {
+         uint64_t P, uint32_t begin, uint32_t end, double omega, IoletArgs ia, HaloArgs halo) {
     const uint32_t s = begin + blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= end) return;
     double f[kQ];
@@ -91,6 +108,10 @@ lbm_push(const double* __restrict__ fo, double* __restrict__ fn, const uint32_t*
         } else {
             const uint32_t op = (v >> kOpShift) & 3u;
             if (op == kOpShared) {
+                if constexpr (kP2P) {
+                    store_shared<true>(fn, P, v & kPayload, fpost, halo);
+                    continue;
+                }
                 dst = uint64_t(kQ) * P + (v & kPayload);
             } else {
                 dst = uint64_t(inv(i)) * P + s;
@@ -172,10 +193,10 @@ struct PushTmaSmem {
 // tail pad of T elements so the last tile's copies stay in bounds.
 // kHints: bit0 = streaming (.cs) stores, bit1 = no L2 evict-first on the
 // bulk loads (tuning knobs; default 0).
-template <int T, int S, int kMinBlocks, bool kTabSmem = true, int kHints = 0>
+template <int T, int S, int kMinBlocks, bool kTabSmem = true, int kHints = 0, bool kP2P = false>
 __global__ void __launch_bounds__(T, kMinBlocks)
 lbm_push_tma(const double* __restrict__ fo, double* __restrict__ fn, const uint32_t* __restrict__ tab,
-             uint64_t P, uint32_t begin, uint32_t end, double omega) {
+             uint64_t P, uint32_t begin, uint32_t end, double omega, HaloArgs halo = HaloArgs{}) {
     using L = PushTmaSmem<T, S, kTabSmem>;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S * L::kStage);
@@ -243,8 +264,13 @@ lbm_push_tma(const double* __restrict__ fo, double* __restrict__ fn, const uint3
                 else v = treg[i - 1];
                 uint64_t dst;
                 if (v < kSpecial) dst = uint64_t(i) * P + v;
-                else if (((v >> kOpShift) & 3u) == kOpShared) dst = uint64_t(kQ) * P + (v & kPayload);
-                else dst = uint64_t(inv(i)) * P + s;
+                else if (((v >> kOpShift) & 3u) == kOpShared) {
+                    if constexpr (kP2P) {
+                        store_shared<true>(fn, P, v & kPayload, fpost, halo);
+                        continue;
+                    }
+                    dst = uint64_t(kQ) * P + (v & kPayload);
+                } else dst = uint64_t(inv(i)) * P + s;
                 if constexpr ((kHints & 1) != 0) __stcs(fn + dst, fpost);
                 else fn[dst] = fpost;
             }

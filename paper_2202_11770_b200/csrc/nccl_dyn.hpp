@@ -24,6 +24,9 @@ struct NcclApi {
     ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
     ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*GroupStart)() = nullptr;
     ncclResult_t (*GroupEnd)() = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
@@ -62,6 +65,8 @@ inline const NcclApi& nccl() {
         sym(a.CommGetAsyncError, "ncclCommGetAsyncError");
         sym(a.Send, "ncclSend");
         sym(a.Recv, "ncclRecv");
+        sym(a.AllReduce, "ncclAllReduce");
+        sym(a.AllGather, "ncclAllGather");
         sym(a.GroupStart, "ncclGroupStart");
         sym(a.GroupEnd, "ncclGroupEnd");
         sym(a.GetErrorString, "ncclGetErrorString");

@@ -159,6 +159,7 @@ class EngineParams:
     observe_iolets: bool = False
     exchange_timeout_s: float = 30.0
     devices: Optional[List[int]] = None
+    halo_mode: int = 0  # B200: 0 NCCL / peer copies + PostReceive, 1 fused NVLink P2P stores
 
 
 # ---- domain -----------------------------------------------------------------------
@@ -401,6 +402,7 @@ def _params_c(p: EngineParams):
     c.capture_period = p.capture_period
     c.observe_iolets = 1 if p.observe_iolets else 0
     c.exchange_timeout_s = p.exchange_timeout_s
+    c.halo_mode = p.halo_mode
     devs = None
     if p.devices:
         devs = np.array(p.devices, np.int32)

@@ -191,13 +191,15 @@ def total_mass(M, sim):
     return m
 
 
-def execute_run(M, run, devices=None):
+def execute_run(M, run, devices=None, halo_mode=None):
     d = make_domain(M, DOMAINS[run["domain"]])
     p = M.EngineParams(tau=run.get("tau", 0.9), dt_s=run.get("dt", 1.0), workers=run["W"],
                        layout=run.get("layout", 0), sequence=run.get("sequence", 0),
                        capture_period=run.get("capture", 0), observe_iolets=run.get("observe", False))
     if devices is not None:
         p.devices = devices
+    if halo_mode is not None:
+        p.halo_mode = halo_mode
     sim = M.Simulation(d, make_bcs(M, run["bcs"]), p)
     if "noise" in run:
         apply_noise(M, sim, noise_for(d.n_sites(), *run["noise"]))

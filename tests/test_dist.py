@@ -103,7 +103,7 @@ NCCL_SCRIPT = textwrap.dedent("""
     run = dict(domain="bif_4_3_12_12", bcs=("bif", "smoke_inlet"), tau=0.8, dt=1e-3, W=world, steps=60,
                noise=(11, 0.01))
     d = cases.make_domain(P, cases.DOMAINS[run["domain"]])
-    prm = P.EngineParams(tau=0.8, dt_s=1e-3, workers=world, devices=[rank])
+    prm = P.EngineParams(tau=0.8, dt_s=1e-3, workers=world, devices=[rank], halo_mode=int(os.environ["HALO"]))
     sim = P.Simulation.distributed(d, cases.make_bcs(P, run["bcs"]), prm, rank, world, obj[0])
     cases.apply_noise(P, sim, cases.noise_for(d.n_sites(), *run["noise"]))
     sim.run(run["steps"])
@@ -122,13 +122,16 @@ NCCL_SCRIPT = textwrap.dedent("""
 
 
 @pytest.mark.gpu
-def test_nccl_ranks_match_single_process():
+@pytest.mark.parametrize("halo", ["0", "1"])
+def test_nccl_ranks_match_single_process(halo):
+    """halo 0: NCCL send/recv + PostReceive; halo 1: fused NVLink P2P stores
+    into IPC-mapped neighbour buffers, flag-synchronised."""
     import torch
     n = torch.cuda.device_count()
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
     world = 4 if n >= 4 else 2
-    outs = _run_ranks(NCCL_SCRIPT, world)
+    outs = _run_ranks(NCCL_SCRIPT, world, env_extra={"HALO": halo})
     for rc, out in outs:
         assert rc == 0, out
         assert "OK" in out

@@ -47,6 +47,27 @@ def test_kernel_variants_bit_exact(product, golden, variant, monkeypatch):
         assert cases.run_digest(res) == golden["runs"][key], key
 
 
+@pytest.mark.parametrize("key", ["bif_W3_soa_reordered", "bif_W4_noise", "pipe_4_20_W4", "pipe_3_8_obs_W2",
+                                 "blob0_noise_W5", "pipe_beat_6_30", "box8_noise_W2_1000"])
+def test_fused_p2p_halo_bit_exact(product, golden, key):
+    """halo_mode=1: edge kernels store cut-crossing links straight into the
+    neighbour's f_new (no shared tail, no PostReceive), flag-synchronised.
+    Same bits as the reference."""
+    res = cases.execute_run(product, cases.RUNS[key], halo_mode=1)
+    assert cases.run_digest(res) == golden["runs"][key]
+
+
+def test_fused_p2p_multi_gpu_in_process(product, golden):
+    import torch
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    for key in ("bif_W4_noise", "pipe_4_20_W4"):
+        for mode in (0, 1):
+            res = cases.execute_run(product, cases.RUNS[key], devices=list(range(n)), halo_mode=mode)
+            assert cases.run_digest(res) == golden["runs"][key], (key, mode)
+
+
 def test_live_reference_random_case(product, reference):
     """A case outside the golden set, against the reference run live."""
     run = dict(domain="bif_3_2_6_8", bcs=("bif", "bif_inlet"), tau=0.7, dt=2e-3, W=3, layout=1, steps=30,
