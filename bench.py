@@ -176,7 +176,7 @@ def main():
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--quick", action="store_true", help="kernel-only number (tuning runs)")
-    ap.add_argument("--halo", default="nccl", choices=["nccl", "p2p"],
+    ap.add_argument("--halo", default="p2p", choices=["nccl", "p2p"],
                     help="N>1 halo exchange: NCCL send/recv + PostReceive, or fused NVLink P2P stores")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

@@ -379,22 +379,50 @@ class Engine {
             enable_peers();
         }
         p2p_mode = prm.halo_mode == 1;
-        if (p2p_mode) setup_p2p();
+        if (p2p_mode) {
+            // If peer mapping fails anywhere, every rank falls back to the
+            // NCCL / peer-copy exchange (ranks agree through an all-reduce).
+            int ok = 1;
+            std::string why;
+            try {
+                setup_p2p();  // dist mode: collective, fails on all ranks together
+            } catch (const Error& e) {
+                if (e.kind == ErrKind::Comm) throw;
+                ok = 0;
+                why = e.what();
+                cudaGetLastError();
+            }
+            if (!ok) {
+                std::fprintf(stderr, "[splbcu] fused P2P halo unavailable (%s); using %s\n",
+                             why.empty() ? "another rank failed" : why.c_str(),
+                             dist ? "NCCL send/recv" : "peer copies");
+                for (auto& wp : W)
+                    if (wp) {
+                        for (void* p : wp->ipc_opened) cudaIpcCloseMemHandle(p);
+                        wp->ipc_opened.clear();
+                    }
+                p2p_mode = false;
+            }
+        }
         if (prm.observe_iolets) init_observation();
         for (auto& wp : W)
             if (wp) CK(cudaStreamSynchronize(wp->sM));
     }
 
-    // NCCL all-reduce of one int on the local worker's stream: a barrier.
-    void dist_barrier() {
+    // NCCL all-reduce (min) of one int on the local worker's stream; also a barrier.
+    int agree_min(int v) {
         WorkerDev& wk = *W[size_t(rank)];
         CK(cudaSetDevice(wk.dev));
         DevMem one;
         int* d = one.alloc<int>(1);
-        CK(cudaMemsetAsync(d, 0, sizeof(int), wk.sE));
-        NK(nccl().AllReduce(d, d, 1, ncclInt, ncclSum, comm, wk.sE));
+        CK(cudaMemcpyAsync(d, &v, sizeof(int), cudaMemcpyHostToDevice, wk.sE));
+        NK(nccl().AllReduce(d, d, 1, ncclInt, ncclMin, comm, wk.sE));
+        int out = 0;
+        CK(cudaMemcpyAsync(&out, d, sizeof(int), cudaMemcpyDeviceToHost, wk.sE));
         CK(cudaStreamSynchronize(wk.sE));
+        return out;
     }
+    void dist_barrier() { (void)agree_min(1); }
 
     // Fused P2P halo (§8f.4): map the neighbours' f buffers and flag words,
     // and give every outgoing shared slot its final destination in the
@@ -422,6 +450,13 @@ class Engine {
                     const Seg& sg = wk.segs[k];
                     WorkerDev& peer = *W[size_t(sg.nb)];
                     const Seg* ps = find_seg(peer, wk.w);
+                    if (peer.dev != wk.dev) {
+                        int can = 0;
+                        CK(cudaDeviceCanAccessPeer(&can, wk.dev, peer.dev));
+                        if (!can)
+                            fail(ErrKind::Cuda, "no peer access between devices " + std::to_string(wk.dev) + " and " +
+                                                    std::to_string(peer.dev));
+                    }
                     std::vector<uint64_t> prf(sg.count);
                     CK(cudaSetDevice(peer.dev));
                     if (sg.count)
@@ -456,17 +491,25 @@ class Engine {
         CK(cudaStreamSynchronize(wk.sE));
         wk.peer_f.clear();
         wk.peer_flags.clear();
+        int opened = 1;
         for (const Seg& sg : wk.segs) {
             std::array<double*, 2> pf{};
-            for (int b = 0; b < 3; ++b) {
+            for (int b = 0; b < 3 && opened; ++b) {
                 void* p = nullptr;
-                CK(cudaIpcOpenMemHandle(&p, all[3 * size_t(sg.nb) + size_t(b)], cudaIpcMemLazyEnablePeerAccess));
+                if (cudaIpcOpenMemHandle(&p, all[3 * size_t(sg.nb) + size_t(b)], cudaIpcMemLazyEnablePeerAccess) !=
+                    cudaSuccess) {
+                    cudaGetLastError();
+                    opened = 0;
+                    break;
+                }
                 wk.ipc_opened.push_back(p);
                 if (b < 2) pf[size_t(b)] = static_cast<double*>(p);
                 else wk.peer_flags.push_back(static_cast<uint32_t*>(p));
             }
             wk.peer_f.push_back(pf);
         }
+        // every rank must have mapped its neighbours before anyone proceeds
+        if (!agree_min(opened)) fail(ErrKind::Cuda, "cudaIpcOpenMemHandle failed on some rank");
         // final destinations: each side sends its recv_dest slice for the pair
         uint64_t* sd = wk.slot_dst.alloc<uint64_t>(std::max<uint32_t>(wk.shared, 1));
         std::vector<uint8_t> sp(std::max<uint32_t>(wk.shared, 1), 0);
