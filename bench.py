@@ -127,7 +127,27 @@ def cpu_reference_run(name, steps_cap, seconds, scale):
     """The unmodified reference (oracle/_ref) on all host cores."""
     import impls
     R = impls.reference()
-    d, bcs, p, desc = workload(R, name, scale)
+    if name in ("c3", "c4"):
+        # The reference has no tree/channel generator: the product's
+        # generator makes the (bounded) sample, handed over as plain arrays
+        # (SparseDomain fields) — the reference's own engine runs it.
+        import paper_2202_11770_b200 as Pm
+        if name == "c3":
+            dp = Pm.build_tree(32, 160, 6, 0.8, 0.8)
+            desc = "C3-shaped tree sample R0=32 L0=160, 6 levels (product generator -> reference SparseDomain)"
+        else:
+            dp = Pm.build_channel(128, 128, 200)
+            desc = "C4-shaped channel sample 128x128x200 (product generator -> reference SparseDomain)"
+        e = dp.export()
+        d = R.SparseDomain.from_arrays(e["coords"], e["types"], e["link_kind"], e["link_iolet"],
+                                       [R.Iolet(i.kind, i.center, i.normal, i.radius) for i in e["iolets"]],
+                                       e["type_ranges"])
+        ents = [R.BCEntry(R.PRESSURE, R.TimeTable.constant(CS2 * 1.001))]
+        ents += [R.BCEntry(R.PRESSURE, R.TimeTable.constant(CS2 * 0.999)) for _ in e["iolets"][1:]]
+        bcs, p = R.BCSet(ents), dict(tau=0.8, dt_s=1.0)
+        del dp, e
+    else:
+        d, bcs, p, desc = workload(R, name, scale)
     cores = os.cpu_count() or 1
     sim = R.Simulation(d, bcs, R.EngineParams(workers=cores, layout=R.SOA, **p))
     sim.run(1)  # warm-up

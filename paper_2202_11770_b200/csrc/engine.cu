@@ -924,6 +924,10 @@ class Engine {
                     case 42: launch_tmc<128, 2, 3>(wk, s, b, e); return;
                     case 43: launch_tmc<256, 2, 2, 6>(wk, s, b, e); return;
                     case 44: launch_tmc<256, 2, 2, 0>(wk, s, b, e); return;
+                    case 45: launch_tmc<192, 2, 3, 6>(wk, s, b, e); return;
+                    case 46: launch_tmc<128, 2, 4, 6>(wk, s, b, e); return;
+                    case 47: launch_tmc<128, 3, 3, 6>(wk, s, b, e); return;
+                    case 48: launch_tmc<96, 2, 5, 6>(wk, s, b, e); return;
                     default: launch_tmc<256, 2, 2>(wk, s, b, e); return;
                 }
             }
