@@ -238,6 +238,13 @@ int splbcu_sim_capture(const splbcu_sim* s, uint64_t k, uint64_t* step,
 uint64_t splbcu_sim_series_rows(const splbcu_sim* s);
 int splbcu_sim_series(const splbcu_sim* s, uint32_t iolet, double* max_speed,
                       double* pressure, double* flow);
+/* Output formats (snapshot.hpp:12-82): the captures as the reference's
+ * snapshots.bin (per capture: u64 step, then 4*n f64 in domain order) and the
+ * iolet series as its timeseries.csv text.  series_csv writes at most cap
+ * bytes (NUL-terminated when room) and always reports the full length. */
+int splbcu_sim_write_snapshots(const splbcu_sim* s, const char* path);
+int splbcu_sim_series_csv(const splbcu_sim* s, double dt_s, char* buf, size_t cap,
+                          size_t* len);
 /* B200 instrumentation (no reference equivalent): CUDA-event timing of every
  * fused plain-site collide+stream launch, on the stream it is launched on. */
 int splbcu_sim_set_kernel_timing(splbcu_sim* s, int32_t on);

@@ -14,6 +14,7 @@
 
 #include "splb/engine.hpp"
 #include "splb/geometry_io.hpp"
+#include "splb/snapshot.hpp"
 #include "splbcu.h"
 
 using namespace splb;
@@ -375,6 +376,20 @@ int splbcu_sim_series(const splbcu_sim* s, uint32_t k, double* a, double* b, dou
         if (a) std::memcpy(a, sr.max_speed.at(k).data(), sr.rows * 8);
         if (b) std::memcpy(b, sr.pressure.at(k).data(), sr.rows * 8);
         if (c) std::memcpy(c, sr.flow.at(k).data(), sr.rows * 8);
+    });
+}
+int splbcu_sim_write_snapshots(const splbcu_sim* s, const char* path) {
+    return guard([&] { write_snapshots(s->s->cache(), std::string(path)); });
+}
+int splbcu_sim_series_csv(const splbcu_sim* s, double dt_s, char* buf, size_t cap, size_t* len) {
+    return guard([&] {
+        const std::string out = series_csv(s->s->series(), dt_s);
+        if (len) *len = out.size();
+        if (buf && cap) {
+            const size_t n = std::min(cap - 1, out.size());
+            std::memcpy(buf, out.data(), n);
+            buf[n] = '\0';
+        }
     });
 }
 int splbcu_sim_set_kernel_timing(splbcu_sim*, int32_t) { return 0; }

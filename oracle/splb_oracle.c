@@ -1191,6 +1191,56 @@ int splbcu_sim_series(const splbcu_sim* S, uint32_t k, double* a, double* b, dou
     if (c) memcpy(c, S->sq[k], 8 * S->rows);
     return 0;
 }
+/* write_snapshots (snapshot.hpp:15-29) */
+int splbcu_sim_write_snapshots(const splbcu_sim* S, const char* path) {
+    FILE* f = fopen(path, "wb");
+    if (!f) return set_err(SPLBCU_ERR_RUNTIME, "snapshot write: cannot open %s", path);
+    int ok = 1;
+    for (uint64_t c = 0; c < S->ncap; ++c) {
+        ok &= fwrite(&S->cap_step[c], 8, 1, f) == 1;
+        ok &= fwrite(S->cap_f[c], 8, 4 * S->dom->n, f) == 4 * S->dom->n;
+    }
+    ok &= fclose(f) == 0;
+    return ok ? 0 : set_err(SPLBCU_ERR_RUNTIME, "snapshot write: stream failure");
+}
+/* series_csv (snapshot.hpp:59-82) */
+int splbcu_sim_series_csv(const splbcu_sim* S, double dt_s, char* buf, size_t cap, size_t* len) {
+    size_t n = 0, sz = 1024;
+    char* out = malloc(sz);
+    char b[256];
+#define APPEND(str)                                          \
+    do {                                                     \
+        size_t l_ = strlen(str);                             \
+        while (n + l_ + 1 > sz) out = realloc(out, sz *= 2); \
+        memcpy(out + n, str, l_);                            \
+        n += l_;                                             \
+    } while (0)
+    APPEND("step,time_s");
+    const uint32_t nio = S->rows ? S->dom->nio : 0;
+    for (uint32_t k = 0; k < nio; ++k) {
+        snprintf(b, sizeof b, ",iolet%u_max_speed,iolet%u_pressure,iolet%u_flow", k, k, k);
+        APPEND(b);
+    }
+    APPEND("\n");
+    for (uint64_t row = 0; row < S->rows; ++row) {
+        snprintf(b, sizeof b, "%llu,%.17g", (unsigned long long)row, (double)row * dt_s);
+        APPEND(b);
+        for (uint32_t k = 0; k < nio; ++k) {
+            snprintf(b, sizeof b, ",%.17g,%.17g,%.17g", S->smax[k][row], S->sp[k][row], S->sq[k][row]);
+            APPEND(b);
+        }
+        APPEND("\n");
+    }
+#undef APPEND
+    if (len) *len = n;
+    if (buf && cap) {
+        const size_t m = n < cap - 1 ? n : cap - 1;
+        memcpy(buf, out, m);
+        buf[m] = '\0';
+    }
+    free(out);
+    return 0;
+}
 int splbcu_sim_set_kernel_timing(splbcu_sim* S, int32_t on) {
     (void)S, (void)on;
     return 0;

@@ -94,6 +94,8 @@ SIGNATURES = [
     ("splbcu_sim_capture", c_int, [_P, C.c_uint64, c_u64p, c_dp]),
     ("splbcu_sim_series_rows", C.c_uint64, [_P]),
     ("splbcu_sim_series", c_int, [_P, C.c_uint32, c_dp, c_dp, c_dp]),
+    ("splbcu_sim_write_snapshots", c_int, [_P, C.c_char_p]),
+    ("splbcu_sim_series_csv", c_int, [_P, C.c_double, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
     ("splbcu_sim_set_kernel_timing", c_int, [_P, c_int]),
     ("splbcu_sim_kernel_stats", c_int, [_P, c_dp, c_u64p, c_u64p]),
     ("splbcu_sim_launch_count", C.c_uint64, [_P]),

@@ -2,7 +2,9 @@
 // engine's exceptions and maps them to the reference's taxonomy.
 #include "splbcu.h"
 
+#include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -431,6 +433,53 @@ int splbcu_sim_series(const splbcu_sim* s, uint32_t k, double* max_speed, double
         if (max_speed) std::memcpy(max_speed, sr.max_speed[k].data(), sr.max_speed[k].size() * 8);
         if (pressure) std::memcpy(pressure, sr.pressure[k].data(), sr.pressure[k].size() * 8);
         if (flow) std::memcpy(flow, sr.flow[k].data(), sr.flow[k].size() * 8);
+    });
+}
+
+// write_snapshots (snapshot.hpp:15-29)
+int splbcu_sim_write_snapshots(const splbcu_sim* s, const char* path) {
+    return guard([&] {
+        check_ptr(s, "simulation");
+        std::FILE* f = std::fopen(path, "wb");
+        if (!f) runtime_error(std::string("snapshot write: cannot open ") + path);
+        bool ok = true;
+        for (const Capture& c : s->s->captures()) {
+            ok &= std::fwrite(&c.step, sizeof(uint64_t), 1, f) == 1;
+            ok &= std::fwrite(c.fields.data(), sizeof(double), c.fields.size(), f) == c.fields.size();
+        }
+        ok &= std::fclose(f) == 0;
+        if (!ok) runtime_error("snapshot write: stream failure");
+    });
+}
+
+// series_csv (snapshot.hpp:59-82)
+int splbcu_sim_series_csv(const splbcu_sim* s, double dt_s, char* buf, size_t cap, size_t* len) {
+    return guard([&] {
+        check_ptr(s, "simulation");
+        const Series& sr = s->s->series();
+        std::string out = "step,time_s";
+        char b[256];
+        for (size_t k = 0; k < sr.max_speed.size(); ++k) {
+            std::snprintf(b, sizeof b, ",iolet%zu_max_speed,iolet%zu_pressure,iolet%zu_flow", k, k, k);
+            out += b;
+        }
+        out += '\n';
+        for (uint64_t row = 0; row < sr.rows; ++row) {
+            std::snprintf(b, sizeof b, "%llu,%.17g", (unsigned long long)row, double(row) * dt_s);
+            out += b;
+            for (size_t k = 0; k < sr.max_speed.size(); ++k) {
+                std::snprintf(b, sizeof b, ",%.17g,%.17g,%.17g", sr.max_speed[k][row], sr.pressure[k][row],
+                              sr.flow[k][row]);
+                out += b;
+            }
+            out += '\n';
+        }
+        if (len) *len = out.size();
+        if (buf && cap) {
+            const size_t n = std::min(cap - 1, out.size());
+            std::memcpy(buf, out.data(), n);
+            buf[n] = '\0';
+        }
     });
 }
 

@@ -478,6 +478,18 @@ class Simulation:
         _check(lib.splbcu_sim_kernel_stats(self._h, C.byref(s), C.byref(n), C.byref(sites)))
         return s.value, n.value, sites.value
 
+    def write_snapshots(self, path: str) -> None:
+        """write_snapshots (snapshot.hpp:15-29): snapshots.bin."""
+        _check(lib.splbcu_sim_write_snapshots(self._h, path.encode()))
+
+    def series_csv(self, dt_s: float) -> str:
+        """series_csv (snapshot.hpp:59-82): timeseries.csv text."""
+        n = C.c_size_t()
+        _check(lib.splbcu_sim_series_csv(self._h, dt_s, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value + 1)
+        _check(lib.splbcu_sim_series_csv(self._h, dt_s, buf, n.value + 1, C.byref(n)))
+        return buf.value.decode()
+
     def launch_count(self) -> int:
         return int(lib.splbcu_sim_launch_count(self._h))
 

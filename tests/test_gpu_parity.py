@@ -221,3 +221,18 @@ def test_kernel_timing_counts(product):
     assert launches == 10 and secs > 0.0
     e = d.export()["type_ranges"]
     assert sites == 10 * int(e[1][1])  # Inner + Wall sites per step
+
+
+def test_output_files_match_reference(product, reference, tmp_path):
+    """snapshots.bin and timeseries.csv written from the B200 engine are
+    byte-identical to the reference's writers (snapshot.hpp:15-82)."""
+    outs = []
+    for M in (product, reference):
+        run = dict(domain="bif_3_2_6_8", bcs=("bif", "bif_inlet"), tau=0.8, dt=1e-3, W=3, steps=40, capture=10,
+                   observe=True)
+        res = cases.execute_run(M, run)
+        p = str(tmp_path / f"{M.__name__}.bin")
+        res["sim"].write_snapshots(p)
+        outs.append((open(p, "rb").read(), res["sim"].series_csv(1e-3)))
+    assert outs[0][0] == outs[1][0]
+    assert outs[0][1] == outs[1][1]

@@ -89,3 +89,17 @@ def test_errors_match_reference(port, reference):
             M.Simulation(d, M.BCSet([M.BCEntry(M.PRESSURE, M.TimeTable.constant(cases.CS2))]), M.EngineParams())
         with pytest.raises(M.Error, match="exceeds site count"):
             M.partition(M.classify_sites(cases.closed_box(2), []), 9)
+
+
+def test_output_files_match_reference(port, reference, tmp_path):
+    """snapshots.bin and timeseries.csv (snapshot.hpp:15-82) byte-identical."""
+    outs = []
+    for M in (port, reference):
+        run = dict(domain="pipe_3_8", bcs=("pressure", 0.34, cases.CS2), tau=0.8, dt=1e-3, W=2, steps=25,
+                   capture=10, observe=True)
+        res = cases.execute_run(M, run)
+        p = str(tmp_path / f"{M.__name__}.bin")
+        res["sim"].write_snapshots(p)
+        outs.append((open(p, "rb").read(), res["sim"].series_csv(1e-3)))
+    assert outs[0] == outs[1]
+    assert outs[0][1].count("\n") == 27 and "iolet1_flow" in outs[0][1]
