@@ -322,6 +322,7 @@ class Engine {
     std::vector<Capture> caps;
     Series series;
     std::vector<std::vector<std::pair<int, uint32_t>>> obs_order;  // per iolet: (worker, pos)
+    std::vector<std::vector<uint32_t>> obs_off_all;  // per worker: per-iolet offsets (+ total), all workers
     uint64_t steps_run = 0;
     double loop_s = 0.0, dev_loop_s = 0.0, plain_s = 0.0;
     uint64_t plain_launches = 0, plain_sites = 0, launches = 0;
@@ -423,6 +424,33 @@ class Engine {
         return out;
     }
     void dist_barrier() { (void)agree_min(1); }
+
+    // Host-buffer collectives over the engine's NCCL communicator (dist mode).
+    std::vector<double> allgather_host(const std::vector<double>& mine) {
+        WorkerDev& wk = *W[size_t(rank)];
+        CK(cudaSetDevice(wk.dev));
+        DevMem s, r;
+        double* ds = s.alloc<double>(mine.size());
+        double* dr = r.alloc<double>(mine.size() * size_t(nranks));
+        CK(cudaMemcpyAsync(ds, mine.data(), mine.size() * 8, cudaMemcpyHostToDevice, wk.sE));
+        NK(nccl().AllGather(ds, dr, mine.size(), ncclDouble, comm, wk.sE));
+        std::vector<double> all(mine.size() * size_t(nranks));
+        CK(cudaMemcpyAsync(all.data(), dr, all.size() * 8, cudaMemcpyDeviceToHost, wk.sE));
+        CK(cudaStreamSynchronize(wk.sE));
+        return all;
+    }
+    // Sum over ranks of arrays that are disjoint (each rank's sites, zero
+    // elsewhere): x + 0 == x exactly, so this assembles the global field.
+    void allreduce_host_sum(double* x, size_t n) {
+        WorkerDev& wk = *W[size_t(rank)];
+        CK(cudaSetDevice(wk.dev));
+        DevMem b;
+        double* d = b.alloc<double>(n);
+        CK(cudaMemcpyAsync(d, x, n * 8, cudaMemcpyHostToDevice, wk.sE));
+        NK(nccl().AllReduce(d, d, n, ncclDouble, ncclSum, comm, wk.sE));
+        CK(cudaMemcpyAsync(x, d, n * 8, cudaMemcpyDeviceToHost, wk.sE));
+        CK(cudaStreamSynchronize(wk.sE));
+    }
 
     // Fused P2P halo (§8f.4): map the neighbours' f buffers and flag words,
     // and give every outgoing shared slot its final destination in the
@@ -859,6 +887,9 @@ class Engine {
                 }
             }
         }
+        obs_off_all.assign(size_t(prm.workers), std::vector<uint32_t>(n_io + 1, 0));
+        for (size_t w = 0; w < size_t(prm.workers); ++w)
+            for (size_t k = 0; k < n_io; ++k) obs_off_all[w][k + 1] = obs_off_all[w][k] + per_w_count[w][k];
         for (auto& wp : W) {
             if (!wp) continue;
             WorkerDev& wk = *wp;
@@ -1184,6 +1215,8 @@ class Engine {
     }
 
     void run(uint64_t n) {
+        const size_t caps_before = caps.size();
+        const bool first_run = steps_run == 0;
         prepare_records(n);
         if (steps_run == 0)
             for (auto& wp : W)
@@ -1254,6 +1287,12 @@ class Engine {
         loop_s += std::chrono::duration<double>(h1 - h0).count();
         steps_run += n;
         assemble_series();
+        if (dist) {
+            // captures of this run hold this rank's sites only: assemble them
+            for (size_t c = 0; c < caps.size(); ++c)
+                if (c >= caps_before || (first_run && caps[c].step == 0))
+                    allreduce_host_sum(caps[c].fields.data(), caps[c].fields.size());
+        }
     }
 
     // Waits for the step loop; in NCCL mode polls for async comm errors and
@@ -1401,6 +1440,21 @@ class Engine {
         }
         const uint64_t first_row = series.rows;
         const uint64_t rows = steps_run + 1;
+        uint64_t row_base = 0, nrows = 0;
+        for (auto& wp : W)
+            if (wp) row_base = wp->obs_row_base, nrows = wp->obs_rows;
+        if (dist) {
+            // every rank needs every worker's rows: all-gather (padded)
+            uint64_t maxn = 0;
+            for (auto& o : obs_off_all) maxn = std::max<uint64_t>(maxn, o[n_io]);
+            const uint64_t per = 3 * nrows * std::max<uint64_t>(maxn, 1);
+            std::vector<double> mine(per, 0.0);
+            std::copy(hb[size_t(rank)].begin(), hb[size_t(rank)].end(), mine.begin());
+            const std::vector<double> all = allgather_host(mine);
+            for (int w = 0; w < prm.workers; ++w)
+                hb[size_t(w)].assign(all.begin() + int64_t(per) * w,
+                                     all.begin() + int64_t(per) * w + int64_t(3 * nrows * obs_off_all[size_t(w)][n_io]));
+        }
         series.max_speed.resize(n_io);
         series.pressure.resize(n_io);
         series.flow.resize(n_io);
@@ -1408,9 +1462,8 @@ class Engine {
             for (uint64_t row = first_row; row < rows; ++row) {
                 double vmax = 0.0, psum = 0.0, qsum = 0.0;
                 for (const auto& [w, pos] : obs_order[k]) {
-                    if (!W[size_t(w)]) continue;  // dist mode: other ranks' sites
-                    const WorkerDev& wk = *W[size_t(w)];
-                    const double* v = &hb[size_t(w)][3 * ((row - wk.obs_row_base) * wk.n_obs + wk.obs_off[k] + pos)];
+                    const std::vector<uint32_t>& off = obs_off_all[size_t(w)];
+                    const double* v = &hb[size_t(w)][3 * ((row - row_base) * off[n_io] + off[k] + pos)];
                     vmax = std::max(vmax, v[0]);
                     psum += v[1];
                     qsum += v[2];
@@ -1431,6 +1484,7 @@ class Engine {
     }
 
     void snapshot(double* out) {
+        if (dist) std::fill(out, out + 4 * dom.n, 0.0);
         for (auto& wp : W) {
             if (!wp) continue;
             WorkerDev& wk = *wp;
@@ -1444,6 +1498,7 @@ class Engine {
             for (uint32_t j = 0; j < wk.n; ++j)
                 std::memcpy(&out[4 * uint64_t(wk.global_of_int[j])], &h[4 * uint64_t(j)], 32);
         }
+        if (dist) allreduce_host_sum(out, 4 * dom.n);  // every rank returns the whole domain
     }
 
     uint64_t ref_idx(const WorkerDev& wk, uint32_t r, int i) const {

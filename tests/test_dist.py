@@ -103,19 +103,22 @@ NCCL_SCRIPT = textwrap.dedent("""
     run = dict(domain="bif_4_3_12_12", bcs=("bif", "smoke_inlet"), tau=0.8, dt=1e-3, W=world, steps=60,
                noise=(11, 0.01))
     d = cases.make_domain(P, cases.DOMAINS[run["domain"]])
-    prm = P.EngineParams(tau=0.8, dt_s=1e-3, workers=world, devices=[rank], halo_mode=int(os.environ["HALO"]))
+    kw = dict(tau=0.8, dt_s=1e-3, workers=world, capture_period=20, observe_iolets=True)
+    prm = P.EngineParams(devices=[rank], halo_mode=int(os.environ["HALO"]), **kw)
     sim = P.Simulation.distributed(d, cases.make_bcs(P, run["bcs"]), prm, rank, world, obj[0])
     cases.apply_noise(P, sim, cases.noise_for(d.n_sites(), *run["noise"]))
-    sim.run(run["steps"])
-    snap = torch.tensor(sim.snapshot_fields())
-    td.all_reduce(snap)  # disjoint site sets: the sum assembles the field
-    if rank == 0:
-        ref = P.Simulation(d, cases.make_bcs(P, run["bcs"]), P.EngineParams(tau=0.8, dt_s=1e-3, workers=world,
-                                                                             devices=[0]))
-        cases.apply_noise(P, ref, cases.noise_for(d.n_sites(), *run["noise"]))
-        ref.run(run["steps"])
-        a, b = snap.numpy(), ref.snapshot_fields()
-        assert np.array_equal(a, b), float(np.max(np.abs(a - b)))
+    sim.run(25)
+    sim.run(run["steps"] - 25)
+    # snapshot, captures and iolet series are assembled across ranks
+    got = (cases.h(sim.snapshot_fields()), [(c.step, cases.h(c.fields)) for c in sim.cache()],
+           {k: [cases.h(a) for a in v] for k, v in sim.series().items() if k != "rows"})
+    ref = P.Simulation(d, cases.make_bcs(P, run["bcs"]), P.EngineParams(devices=[rank], **kw))
+    cases.apply_noise(P, ref, cases.noise_for(d.n_sites(), *run["noise"]))
+    ref.run(25)
+    ref.run(run["steps"] - 25)
+    want = (cases.h(ref.snapshot_fields()), [(c.step, cases.h(c.fields)) for c in ref.cache()],
+            {k: [cases.h(a) for a in v] for k, v in ref.series().items() if k != "rows"})
+    assert got == want, (got[1], want[1])
     td.barrier()
     print("OK", rank)
 """)
