@@ -97,6 +97,11 @@ typedef struct splbcu_params {
      * PostReceive; 1 = fused NVLink P2P: the edge kernels store cut-crossing
      * links straight into the neighbour's f_new (§8f.4 of SURVEY.md). */
     int32_t halo_mode;
+    /* B200 extension: distribution storage.  0 = two buffers, push step
+     * (f_old -> f_new, reference layout.hpp:19-62); 1 = one buffer updated in
+     * place with the AA pattern (even steps local, odd steps gather/scatter;
+     * §8f.3): half the HBM, identical bits. */
+    int32_t storage;
 } splbcu_params;
 
 typedef struct splbcu_domain splbcu_domain;       /* splb::SparseDomain */

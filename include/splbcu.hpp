@@ -103,6 +103,7 @@ struct EngineParams {
     double exchange_timeout_s = 30.0;
     std::vector<int32_t> devices;  // B200: workers placed round robin
     int32_t halo_mode = 0;         // B200: 0 NCCL/peer copies, 1 fused NVLink P2P stores
+    int32_t storage = 0;           // B200: 0 two buffers (push), 1 single buffer (AA pattern)
 };
 
 // geometry.hpp:64-73 (opaque; site arrays on demand)
@@ -203,6 +204,7 @@ class Simulation {
         c.workers = p.workers, c.capture_period = p.capture_period, c.observe_iolets = p.observe_iolets;
         c.exchange_timeout_s = p.exchange_timeout_s;
         c.halo_mode = p.halo_mode;
+        c.storage = p.storage;
         c.n_devices = int32_t(p.devices.size());
         c.device_ids = p.devices.data();
         splbcu_sim* s = nullptr;

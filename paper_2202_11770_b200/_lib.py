@@ -36,7 +36,8 @@ class Params(C.Structure):
                 ("layout", C.c_int32), ("scheme", C.c_int32), ("sequence", C.c_int32),
                 ("workers", C.c_int32), ("capture_period", C.c_uint64),
                 ("observe_iolets", C.c_int32), ("exchange_timeout_s", C.c_double),
-                ("n_devices", C.c_int32), ("device_ids", c_i32p), ("halo_mode", C.c_int32)]
+                ("n_devices", C.c_int32), ("device_ids", c_i32p), ("halo_mode", C.c_int32),
+                ("storage", C.c_int32)]
 
 
 # (name, restype, argtypes) for every symbol include/splbcu.h declares.

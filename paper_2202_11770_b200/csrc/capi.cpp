@@ -69,6 +69,7 @@ Params to_params(const splbcu_params* p) {
     q.exchange_timeout_s = p->exchange_timeout_s;
     for (int k = 0; k < p->n_devices; ++k) q.devices.push_back(p->device_ids[k]);
     q.halo_mode = p->halo_mode;
+    q.storage = p->storage;
     return q;
 }
 

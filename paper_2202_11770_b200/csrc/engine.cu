@@ -328,6 +328,7 @@ class Engine {
     uint64_t plain_launches = 0, plain_sites = 0, launches = 0;
     bool kernel_timing = false;
     bool p2p_mode = false;
+    bool aa_mode = false;  // single-buffer AA storage (params.storage == 1)
     std::vector<IoletDev> io_host;
 
     Engine(const Domain& d, std::vector<BCEntry> b, Params p, int rank_, int nranks_, const void* nccl_id)
@@ -335,6 +336,7 @@ class Engine {
         dist = nccl_id != nullptr;
         rank = rank_;
         nranks = nranks_;
+        aa_mode = prm.storage == 1;
         if (prm.devices.empty()) {
             int cur = 0;
             CK(cudaGetDevice(&cur));
@@ -379,8 +381,10 @@ class Engine {
                 }
             enable_peers();
         }
-        p2p_mode = prm.halo_mode == 1;
-        if (p2p_mode) {
+        p2p_mode = prm.halo_mode == 1 || (aa_mode && prm.workers > 1);
+        if (aa_mode && p2p_mode) {
+            setup_p2p();  // the AA scheme's odd steps read/write neighbours in place: no fallback
+        } else if (p2p_mode) {
             // If peer mapping fails anywhere, every rank falls back to the
             // NCCL / peer-copy exchange (ranks agree through an all-reduce).
             int ok = 1;
@@ -491,7 +495,8 @@ class Engine {
                         CK(cudaMemcpy(prf.data(), peer.recv_flat.get<uint64_t>() + ps->base, sg.count * 8,
                                       cudaMemcpyDeviceToHost));
                     for (uint32_t j = 0; j < sg.count; ++j) sp[sg.base + j] = uint8_t(k), sd[sg.base + j] = prf[j];
-                    wk.peer_f.push_back({peer.fbuf[0].get<double>(), peer.fbuf[1].get<double>()});
+                    wk.peer_f.push_back({peer.fbuf[0].get<double>(),
+                                         peer.fbuf[aa_mode ? 0 : 1].get<double>()});
                     wk.peer_flags.push_back(peer.flags.get<uint32_t>());
                 }
                 CK(cudaSetDevice(wk.dev));
@@ -534,6 +539,7 @@ class Engine {
                 if (b < 2) pf[size_t(b)] = static_cast<double*>(p);
                 else wk.peer_flags.push_back(static_cast<uint32_t*>(p));
             }
+            if (aa_mode) pf[1] = pf[0];  // single buffer
             wk.peer_f.push_back(pf);
         }
         // every rank must have mapped its neighbours before anyone proceeds
@@ -802,11 +808,13 @@ class Engine {
             assign_slots<<<blocks_for(wk.shared), 256, 0, s>>>(ovals2, ivals2, wk.shared, tab, rf, sp);
         CK(cudaGetLastError());
 
-        // distribution store, f_old = equilibrium(rho0, 0) (engine.hpp:243-260)
-        for (int b = 0; b < 2; ++b) {
+        // distribution store, f_old = equilibrium(rho0, 0) (engine.hpp:243-260);
+        // the AA scheme keeps a single buffer
+        for (int b = 0; b < (aa_mode ? 1 : 2); ++b) {
             double* f = wk.fbuf[b].alloc<double>(wk.fsize() + kTilePad);
             CK(cudaMemsetAsync(f, 0, (wk.fsize() + kTilePad) * sizeof(double), s));
         }
+        if (aa_mode) wk.fbuf[1].alloc<double>(1);
         wk.old = 0;
         Eq19 eq;
         feq_all(prm.rho0, 0.0, 0.0, 0.0, eq.v);
@@ -1160,10 +1168,40 @@ class Engine {
     void observe(WorkerDev& wk, cudaStream_t s, const double* f, uint64_t row) {
         if (!wk.n_obs) return;
         double* out = wk.obs_buf.get<double>() + 3 * (row - wk.obs_row_base) * wk.n_obs;
-        lbm_iolet_observe<<<blocks_for(wk.n_obs), 256, 0, s>>>(f, wk.P, wk.n_obs, wk.obs_site.get<uint32_t>(),
-                                                               wk.obs_iolet.get<uint16_t>(), wk.io_geo.get<IoletDev>(), out);
+        if (aa_mode) {
+            const int st = int(row & 1);  // AA state after `row` steps: S when odd
+            if (p2p_mode)
+                lbm_aa_observe<true><<<blocks_for(wk.n_obs), 256, 0, s>>>(
+                    f, wk.tab.get<uint32_t>(), wk.P, wk.n_obs, st, halo_args(wk), wk.obs_site.get<uint32_t>(),
+                    wk.obs_iolet.get<uint16_t>(), wk.io_geo.get<IoletDev>(), out);
+            else
+                lbm_aa_observe<false><<<blocks_for(wk.n_obs), 256, 0, s>>>(
+                    f, wk.tab.get<uint32_t>(), wk.P, wk.n_obs, st, HaloArgs{}, wk.obs_site.get<uint32_t>(),
+                    wk.obs_iolet.get<uint16_t>(), wk.io_geo.get<IoletDev>(), out);
+        } else {
+            lbm_iolet_observe<<<blocks_for(wk.n_obs), 256, 0, s>>>(f, wk.P, wk.n_obs, wk.obs_site.get<uint32_t>(),
+                                                                   wk.obs_iolet.get<uint16_t>(),
+                                                                   wk.io_geo.get<IoletDev>(), out);
+        }
         launches++;
         CK(cudaGetLastError());
+    }
+
+    // Moments of every local site into wk.cap4 (internal order), either
+    // storage scheme; `steps` = steps completed (AA state parity).
+    void moments_to_cap4(WorkerDev& wk, cudaStream_t s, const double* f, uint64_t steps) {
+        if (!wk.n) return;
+        if (aa_mode) {
+            const int st = int(steps & 1);
+            if (p2p_mode)
+                lbm_aa_capture<true><<<blocks_for(wk.n), 256, 0, s>>>(f, wk.tab.get<uint32_t>(), wk.P, wk.n, st,
+                                                                      halo_args(wk), wk.cap4.get<double>());
+            else
+                lbm_aa_capture<false><<<blocks_for(wk.n), 256, 0, s>>>(f, wk.tab.get<uint32_t>(), wk.P, wk.n, st,
+                                                                       HaloArgs{}, wk.cap4.get<double>());
+        } else {
+            lbm_capture_moments<<<blocks_for(wk.n), 256, 0, s>>>(f, wk.P, wk.n, wk.cap4.get<double>());
+        }
     }
 
     void capture(WorkerDev& wk, cudaStream_t s, const double* f, uint64_t step) {
@@ -1171,8 +1209,7 @@ class Engine {
         for (Capture& x : caps)
             if (x.step == step) c = &x;
         if (!c) return;
-        if (wk.n)
-            lbm_capture_moments<<<blocks_for(wk.n), 256, 0, s>>>(f, wk.P, wk.n, wk.cap4.get<double>());
+        moments_to_cap4(wk, s, f, step);
         launches++;
         CK(cudaGetLastError());
         std::vector<double> h(4 * uint64_t(wk.n));
@@ -1328,6 +1365,124 @@ class Engine {
     }
 
     // advance_one (engine.hpp:330-363) for every local worker.
+    // ---- AA single-buffer scheme ------------------------------------------------
+    template <int T, int S, int B>
+    void launch_aa_even_tma(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e) {
+        using Lm = PushTmaSmem<T, S, false>;
+        static int cfg_dev = -1, resident = 0;
+        if (cfg_dev != wk.dev) {
+            CK(cudaFuncSetAttribute(lbm_aa_even_tma<T, S, B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(Lm::kBytes)));
+            int per_sm = 0, sms = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lbm_aa_even_tma<T, S, B>, T, Lm::kBytes));
+            CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, wk.dev));
+            resident = std::max(1, per_sm) * sms;
+            cfg_dev = wk.dev;
+        }
+        const uint32_t base = b & ~3u;
+        const uint32_t ntiles = (e - base + T - 1) / T;
+        const unsigned grid = unsigned(std::min<uint32_t>(ntiles, uint32_t(resident)));
+        lbm_aa_even_tma<T, S, B><<<grid, T, Lm::kBytes, s>>>(wk.f_old(), wk.P, b, e, omega);
+    }
+
+    void launch_aa_range(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, bool iolet, const double* staged,
+                         const int32_t* coords, bool timed, bool edge, bool odd) {
+        if (e <= b) return;
+        IoletArgs ia{wk.io_geo.get<IoletDev>(), staged, coords};
+        const bool remote = edge && p2p_mode && wk.shared > 0;
+        const HaloArgs h = remote ? halo_args(wk) : HaloArgs{};
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (timed && kernel_timing) {
+            if (wk.tev_used + 2 > wk.tev.size())
+                for (int k = 0; k < 2; ++k) {
+                    cudaEvent_t ev;
+                    CK(cudaEventCreate(&ev));
+                    wk.tev.push_back(ev);
+                }
+            e0 = wk.tev[wk.tev_used++];
+            e1 = wk.tev[wk.tev_used++];
+            CK(cudaEventRecord(e0, s));
+        }
+        double* F = wk.f_old();
+        const uint32_t* tab = wk.tab.get<uint32_t>();
+        const unsigned nb = blocks_for(e - b, 128);
+        if (!odd) {
+            if (iolet) lbm_aa_even<true><<<blocks_for(e - b), 256, 0, s>>>(F, tab, wk.P, b, e, omega, ia);
+            else if (wk.tma_ok) launch_aa_even_tma<256, 2, 2>(wk, s, b, e);
+            else lbm_aa_even<false><<<blocks_for(e - b), 256, 0, s>>>(F, tab, wk.P, b, e, omega, ia);
+        } else if (remote) {
+            if (iolet) lbm_aa_odd<true, true, 128, 4><<<nb, 128, 0, s>>>(F, tab, wk.P, b, e, omega, ia, h);
+            else lbm_aa_odd<false, true, 128, 4><<<nb, 128, 0, s>>>(F, tab, wk.P, b, e, omega, ia, h);
+        } else {
+            if (iolet) lbm_aa_odd<true, false, 128, 4><<<nb, 128, 0, s>>>(F, tab, wk.P, b, e, omega, ia, h);
+            else lbm_aa_odd<false, false, 128, 4><<<nb, 128, 0, s>>>(F, tab, wk.P, b, e, omega, ia, h);
+        }
+        if (timed) {
+            if (kernel_timing) CK(cudaEventRecord(e1, s));
+            plain_launches++;
+            plain_sites += e - b;
+        }
+        launches++;
+        CK(cudaGetLastError());
+    }
+
+    void advance_group_aa(WorkerDev& wk, cudaStream_t s, bool edge, const double* staged, bool odd) {
+        const int32_t* ioc = wk.io_coords.get<int32_t>();
+        if (edge) {
+            launch_aa_range(wk, s, 0, wk.ep, false, staged, ioc, false, true, odd);
+            launch_aa_range(wk, s, wk.ep, wk.n_edge, true, staged, ioc, false, true, odd);
+        } else {
+            launch_aa_range(wk, s, wk.n_edge, wk.n_edge + wk.mp, false, staged, ioc, true, false, odd);
+            launch_aa_range(wk, s, wk.n_edge + wk.mp, wk.n, true, staged, ioc + 3 * uint64_t(wk.n_edge - wk.ep),
+                            false, false, odd);
+        }
+    }
+
+    // One AA step for every local worker.  Only the odd steps' edge kernels
+    // touch a neighbour (remote gathers and stores, in place); a neighbour
+    // may start its next edge kernel once ours is done (flag word), while
+    // the interior kernels never conflict across workers.
+    void step_once_aa(uint64_t k, uint64_t staged_off) {
+        const uint32_t g = uint32_t(steps_run + k);
+        const bool odd = (g & 1u) != 0;
+        for (auto& wp : W) {
+            if (!wp) continue;
+            WorkerDev& wk = *wp;
+            CK(cudaSetDevice(wk.dev));
+            const uint32_t* fl = wk.flags.get<uint32_t>();
+            if (p2p_mode)
+                for (const Seg& sg : wk.segs) wait_geq(wk.sE, fl + size_t(sg.nb), g);
+            advance_group_aa(wk, wk.sE, true, wk.staged.get<double>() + staged_off, odd);
+            if (p2p_mode)
+                for (size_t j = 0; j < wk.segs.size(); ++j) write_flag(wk.sE, wk.peer_flags[j] + wk.w, g + 1);
+        }
+        for (auto& wp : W) {
+            if (!wp) continue;
+            WorkerDev& wk = *wp;
+            CK(cudaSetDevice(wk.dev));
+            advance_group_aa(wk, wk.sM, false, wk.staged.get<double>() + staged_off, odd);
+            CK(cudaEventRecord(wk.evMid, wk.sM));
+        }
+        const uint64_t done = steps_run + k + 1;
+        for (auto& wp : W) {
+            if (!wp) continue;
+            WorkerDev& wk = *wp;
+            CK(cudaSetDevice(wk.dev));
+            CK(cudaStreamWaitEvent(wk.sE, wk.evMid, 0));
+            const bool rec = (prm.capture_period > 0 && done % prm.capture_period == 0) || prm.observe_iolets;
+            if (rec && p2p_mode) {  // state-S gathers read the neighbours' edge slots of this step
+                const uint32_t* fl = wk.flags.get<uint32_t>();
+                for (const Seg& sg : wk.segs) wait_geq(wk.sE, fl + size_t(sg.nb), g + 1);
+            }
+            if (prm.capture_period > 0 && done % prm.capture_period == 0)
+                record_state(wk, wk.sE, done, wk.f_old());
+            else if (prm.observe_iolets)
+                observe(wk, wk.sE, wk.f_old(), done);
+            CK(cudaEventRecord(wk.evEnd, wk.sE));
+            CK(cudaStreamWaitEvent(wk.sM, wk.evEnd, 0));
+        }
+    }
+
     // Fused P2P step: the edge kernels store cut-crossing links straight into
     // the neighbours' f_new over NVLink; stream-ordered flag words replace
     // send/recv: wait until a neighbour is done reading the buffer we write
@@ -1373,6 +1528,7 @@ class Engine {
     }
 
     void step_once(uint64_t k, uint64_t staged_off) {
+        if (aa_mode) return step_once_aa(k, staged_off);
         if (p2p_mode) return step_once_p2p(k, staged_off);
         const bool classic = prm.sequence == 0;
         // PreSend: edge sites
@@ -1489,8 +1645,7 @@ class Engine {
             if (!wp) continue;
             WorkerDev& wk = *wp;
             CK(cudaSetDevice(wk.dev));
-            if (wk.n)
-                lbm_capture_moments<<<blocks_for(wk.n), 256, 0, wk.sM>>>(wk.f_old(), wk.P, wk.n, wk.cap4.get<double>());
+            moments_to_cap4(wk, wk.sM, wk.f_old(), steps_run);
             CK(cudaGetLastError());
             std::vector<double> h(4 * uint64_t(wk.n));
             if (wk.n) CK(cudaMemcpyAsync(h.data(), wk.cap4.get<double>(), h.size() * 8, cudaMemcpyDeviceToHost, wk.sM));
@@ -1501,6 +1656,26 @@ class Engine {
         if (dist) allreduce_host_sum(out, 4 * dom.n);  // every rank returns the whole domain
     }
 
+    // AA storage: f in the reference meaning, as 19 planes of P (internal order).
+    std::vector<double> aa_planes(WorkerDev& wk) {
+        DevMem tmp;
+        double* d = tmp.alloc<double>(uint64_t(kQ) * wk.P);
+        if (wk.n) {
+            const int st = int(steps_run & 1);
+            if (p2p_mode)
+                lbm_aa_export<true><<<blocks_for(wk.n), 256, 0, wk.sM>>>(wk.f_old(), wk.tab.get<uint32_t>(), wk.P,
+                                                                         wk.n, st, halo_args(wk), d);
+            else
+                lbm_aa_export<false><<<blocks_for(wk.n), 256, 0, wk.sM>>>(wk.f_old(), wk.tab.get<uint32_t>(), wk.P,
+                                                                          wk.n, st, HaloArgs{}, d);
+            CK(cudaGetLastError());
+        }
+        std::vector<double> h(uint64_t(kQ) * wk.P);
+        CK(cudaMemcpyAsync(h.data(), d, h.size() * 8, cudaMemcpyDeviceToHost, wk.sM));
+        CK(cudaStreamSynchronize(wk.sM));
+        return h;
+    }
+
     uint64_t ref_idx(const WorkerDev& wk, uint32_t r, int i) const {
         return prm.layout == 0 ? uint64_t(kQ) * r + uint64_t(i) : uint64_t(i) * wk.n + r;
     }
@@ -1509,6 +1684,18 @@ class Engine {
         WorkerDev& wk = local(w);
         CK(cudaSetDevice(wk.dev));
         CK(cudaDeviceSynchronize());
+        if (aa_mode) {
+            // one buffer: f_old is the current state (gathered by the AA rule);
+            // f_new has no storage of its own (zeros); no shared tail
+            std::fill(host, host + uint64_t(kQ) * wk.n + wk.shared, 0.0);
+            if (which != 0) return;
+            const std::vector<double> h = aa_planes(wk);
+            for (uint32_t r = 0; r < wk.n; ++r) {
+                const uint32_t j = wk.int_of_ref[r];
+                for (int i = 0; i < kQ; ++i) host[ref_idx(wk, r, i)] = h[uint64_t(i) * wk.P + j];
+            }
+            return;
+        }
         std::vector<double> h(wk.fsize());
         const double* src = which == 0 ? wk.f_old() : wk.f_new();
         CK(cudaMemcpy(h.data(), src, h.size() * 8, cudaMemcpyDeviceToHost));
@@ -1523,6 +1710,25 @@ class Engine {
         WorkerDev& wk = local(w);
         CK(cudaSetDevice(wk.dev));
         CK(cudaDeviceSynchronize());
+        if (aa_mode) {
+            if (which != 0) return;  // no separate f_new in the single-buffer scheme
+            if ((steps_run & 1) && prm.workers > 1)
+                config_error("store(w): the AA scheme accepts f_old writes across workers after an even step count");
+            std::vector<double> h(uint64_t(kQ) * wk.P, 0.0);
+            for (uint32_t r = 0; r < wk.n; ++r) {
+                const uint32_t j = wk.int_of_ref[r];
+                for (int i = 0; i < kQ; ++i) h[uint64_t(i) * wk.P + j] = host[ref_idx(wk, r, i)];
+            }
+            DevMem tmp;
+            double* d = tmp.alloc<double>(h.size());
+            CK(cudaMemcpy(d, h.data(), h.size() * 8, cudaMemcpyHostToDevice));
+            if (wk.n)
+                lbm_aa_import<<<blocks_for(wk.n), 256, 0, wk.sM>>>(wk.f_old(), wk.tab.get<uint32_t>(), wk.P, wk.n,
+                                                                   int(steps_run & 1), d);
+            CK(cudaGetLastError());
+            CK(cudaStreamSynchronize(wk.sM));
+            return;
+        }
         std::vector<double> h(wk.fsize(), 0.0);
         for (uint32_t r = 0; r < wk.n; ++r) {
             const uint32_t j = wk.int_of_ref[r];

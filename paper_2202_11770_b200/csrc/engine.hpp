@@ -22,6 +22,7 @@ struct Params {
     bool observe_iolets = false;
     double exchange_timeout_s = 30.0;
     int halo_mode = 0;  // 0: NCCL send/recv (dist) or peer copies; 1: fused P2P stores
+    int storage = 0;    // 0: two buffers (push); 1: one buffer, AA pattern in place
     std::vector<int> devices;
 };
 

@@ -516,6 +516,243 @@ lbm_push_ws(const __grid_constant__ CUtensorMap tm_f, const __grid_constant__ CU
     }
 }
 
+// ---- AA pattern: one distribution buffer, in place ---------
+// State N ("natural", after an even number of steps): F[i][x] = f(x, i).
+// Even step (N -> S), purely local: collide at x, store the post-collision
+//   g_m(x) (or its iolet BC value) at F[inv(m)][x].
+// State S: f(y, i) lives at F[inv(i)][y - c_i] when link inv(i) of y is a
+//   fluid link (the source site's swapped slot), else at F[i][y] (the value
+//   bounced back / reconstructed at y itself).
+// Odd step (S -> N): gather f(y, .) by that rule, collide, store h_i(y) where
+//   the push step would (F[i][y + c_i]; bounce-back / iolet -> F[inv(i)][y]).
+// Every location is read and written by exactly one site per step, so the
+// update is in place; the arithmetic is the push step's, so the bits are the
+// reference's.  Cut-crossing links read/write the neighbour GPU's buffer
+// (peer-mapped) at the location the P2P push would store to.
+
+// Location of f(y, i) in state S, from the table entry of direction inv(i).
+template <bool kP2P>
+__device__ __forceinline__ const double* aa_src(const double* F, uint64_t P, uint32_t y, int i, uint32_t vinv,
+                                                const HaloArgs& h) {
+    if (vinv < kSpecial) return F + uint64_t(inv(i)) * P + vinv;
+    if (((vinv >> kOpShift) & 3u) == kOpShared) {
+        if constexpr (kP2P) {
+            const uint32_t slot = vinv & kPayload;
+            return h.peer_fn[h.slot_peer[slot]] + h.slot_dst[slot];
+        }
+    }
+    return F + uint64_t(i) * P + y;  // bounce-back / iolet: reconstructed at y
+}
+
+// Even step over sites [begin, end): plain sites need no table at all.
+template <bool kIolets>
+__global__ void __launch_bounds__(256)
+lbm_aa_even(double* __restrict__ F, const uint32_t* __restrict__ tab, uint64_t P, uint32_t begin, uint32_t end,
+            double omega, IoletArgs ia) {
+    const uint32_t s = begin + blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= end) return;
+    double f[kQ];
+#pragma unroll
+    for (int i = 0; i < kQ; ++i) f[i] = F[uint64_t(i) * P + s];
+    const Macro m = macro_of(f);
+    double feq[kQ];
+    feq_all(m.rho, m.ux, m.uy, m.uz, feq);
+    F[s] = relax(f[0], feq[0], omega);
+#pragma unroll
+    for (int i = 1; i < kQ; ++i) {
+        double g = relax(f[i], feq[i], omega);
+        if constexpr (kIolets) {
+            const uint32_t v = tab[uint64_t(i - 1) * P + s];
+            if (v >= kSpecial && ((v >> kOpShift) & 3u) == kOpIolet) {
+                const uint32_t k = v & kPayload;
+                const int32_t* c = ia.coords + 3 * uint64_t(s - begin);
+                g = iolet_link_value(i, g, m, ia.io[k], ia.staged[k], c[0], c[1], c[2]);
+            }
+        }
+        F[uint64_t(inv(i)) * P + s] = g;
+    }
+}
+
+// Even step, plain sites, TMA-staged loads (the bulk kernel): streaming in,
+// streaming out, 304 B/site.
+template <int T, int S, int kMinBlocks>
+__global__ void __launch_bounds__(T, kMinBlocks)
+lbm_aa_even_tma(double* __restrict__ F, uint64_t P, uint32_t begin, uint32_t end, double omega) {
+    using L = PushTmaSmem<T, S, false>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S * L::kStage);
+    const uint32_t base = begin & ~3u;
+    const uint32_t ntiles = (end - base + T - 1) / T;
+    const uint32_t G = gridDim.x;
+    const uint32_t tid = threadIdx.x;
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) mbar_init(&bar[s], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    const uint64_t policy = evict_normal_policy();
+    auto issue = [&](uint32_t k) {
+        const uint32_t tile = blockIdx.x + k * G;
+        if (tile >= ntiles) return;
+        const int st = int(k % S);
+        unsigned char* buf = smem + st * L::kStage;
+        const uint64_t t0 = uint64_t(base) + uint64_t(tile) * T;
+        mbar_expect_tx(&bar[st], L::kStage);
+#pragma unroll 1
+        for (int i = 0; i < kQ; ++i) bulk_g2s(buf + i * T * 8, F + uint64_t(i) * P + t0, T * 8, &bar[st], policy);
+    };
+    if (tid == 0)
+        for (uint32_t k = 0; k + 1 < uint32_t(S); ++k) issue(k);
+    for (uint32_t k = 0;; ++k) {
+        const uint32_t tile = blockIdx.x + k * G;
+        if (tile >= ntiles) break;
+        if (tid == 0) issue(k + S - 1);
+        const int st = int(k % S);
+        const uint32_t s = base + tile * T + tid;
+        mbar_wait(&bar[st], (k / S) & 1u);
+        const double* fs = reinterpret_cast<const double*>(smem + st * L::kStage);
+        if (s >= begin && s < end) {
+            double f[kQ];
+#pragma unroll
+            for (int i = 0; i < kQ; ++i) f[i] = fs[i * T + tid];
+            const Macro m = macro_of(f);
+            double feq[kQ];
+            feq_all(m.rho, m.ux, m.uy, m.uz, feq);
+#pragma unroll
+            for (int i = 0; i < kQ; ++i) F[uint64_t(inv(i)) * P + s] = relax(f[i], feq[i], omega);
+        }
+        __syncthreads();
+    }
+}
+
+// Odd step over sites [begin, end): gather by the state-S rule, collide, store
+// like the push step.  One thread per site.
+template <bool kIolets, bool kP2P, int kThreads, int kMinBlocks>
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
+lbm_aa_odd(double* __restrict__ F, const uint32_t* __restrict__ tab, uint64_t P, uint32_t begin, uint32_t end,
+           double omega, IoletArgs ia, HaloArgs halo) {
+    const uint32_t s = begin + blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= end) return;
+    uint32_t t[kQ - 1];
+#pragma unroll
+    for (int i = 0; i < kQ - 1; ++i) t[i] = __ldg(tab + uint64_t(i) * P + s);
+    double f[kQ];
+    f[0] = F[s];
+#pragma unroll
+    for (int i = 1; i < kQ; ++i) f[i] = *aa_src<kP2P>(F, P, s, i, t[inv(i) - 1], halo);
+    const Macro m = macro_of(f);
+    double feq[kQ];
+    feq_all(m.rho, m.ux, m.uy, m.uz, feq);
+    F[s] = relax(f[0], feq[0], omega);
+#pragma unroll
+    for (int i = 1; i < kQ; ++i) {
+        double fpost = relax(f[i], feq[i], omega);
+        const uint32_t v = t[i - 1];
+        double* dst;
+        if (v < kSpecial) {
+            dst = F + uint64_t(i) * P + v;
+        } else {
+            const uint32_t op = (v >> kOpShift) & 3u;
+            if (op == kOpShared) {
+                if constexpr (kP2P) {
+                    const uint32_t slot = v & kPayload;
+                    dst = halo.peer_fn[halo.slot_peer[slot]] + halo.slot_dst[slot];
+                } else {
+                    dst = F + uint64_t(kQ) * P + (v & kPayload);  // unreachable: AA needs P2P across workers
+                }
+            } else {
+                dst = F + uint64_t(inv(i)) * P + s;
+                if constexpr (kIolets) {
+                    if (op == kOpIolet) {
+                        const uint32_t k = v & kPayload;
+                        const int32_t* c = ia.coords + 3 * uint64_t(s - begin);
+                        fpost = iolet_link_value(i, fpost, m, ia.io[k], ia.staged[k], c[0], c[1], c[2]);
+                    }
+                }
+            }
+        }
+        *dst = fpost;
+    }
+}
+
+// Gather the 19 populations of site s in the current AA state (state N:
+// plain reads; state S: the rule above).
+template <bool kP2P>
+__device__ __forceinline__ void aa_gather(const double* F, const uint32_t* tab, uint64_t P, uint32_t s, bool state_s,
+                                          const HaloArgs& h, double f[kQ]) {
+    if (!state_s) {
+#pragma unroll
+        for (int i = 0; i < kQ; ++i) f[i] = F[uint64_t(i) * P + s];
+        return;
+    }
+    f[0] = F[s];
+#pragma unroll
+    for (int i = 1; i < kQ; ++i) f[i] = *aa_src<kP2P>(F, P, s, i, tab[uint64_t(inv(i) - 1) * P + s], h);
+}
+
+template <bool kP2P>
+__global__ void lbm_aa_capture(const double* __restrict__ F, const uint32_t* __restrict__ tab, uint64_t P,
+                               uint32_t n, int state_s, HaloArgs h, double* __restrict__ out4) {
+    const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    double fl[kQ];
+    aa_gather<kP2P>(F, tab, P, s, state_s != 0, h, fl);
+    const Macro m = macro_of(fl);
+    double* o = out4 + 4 * uint64_t(s);
+    o[0] = m.rho;
+    o[1] = m.ux;
+    o[2] = m.uy;
+    o[3] = m.uz;
+}
+
+// f in the reference's meaning for every (site, direction): 19 planes of n.
+template <bool kP2P>
+__global__ void lbm_aa_export(const double* __restrict__ F, const uint32_t* __restrict__ tab, uint64_t P, uint32_t n,
+                              int state_s, HaloArgs h, double* __restrict__ out) {
+    const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    double fl[kQ];
+    aa_gather<kP2P>(F, tab, P, s, state_s != 0, h, fl);
+#pragma unroll
+    for (int i = 0; i < kQ; ++i) out[uint64_t(i) * P + s] = fl[i];
+}
+
+// Inverse of lbm_aa_export: scatter f(s, i) to its location in the current
+// state (own sites only; a cut-crossing source lives on the neighbour).
+__global__ void lbm_aa_import(double* __restrict__ F, const uint32_t* __restrict__ tab, uint64_t P, uint32_t n,
+                              int state_s, const double* __restrict__ in) {
+    const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    if (!state_s) {
+        for (int i = 0; i < kQ; ++i) F[uint64_t(i) * P + s] = in[uint64_t(i) * P + s];
+        return;
+    }
+    F[s] = in[s];
+    for (int i = 1; i < kQ; ++i) {
+        const uint32_t vinv = tab[uint64_t(inv(i) - 1) * P + s];
+        if (vinv < kSpecial) F[uint64_t(inv(i)) * P + vinv] = in[uint64_t(i) * P + s];
+        else if (((vinv >> kOpShift) & 3u) != kOpShared) F[uint64_t(i) * P + s] = in[uint64_t(i) * P + s];
+    }
+}
+
+template <bool kP2P>
+__global__ void lbm_aa_observe(const double* __restrict__ F, const uint32_t* __restrict__ tab, uint64_t P,
+                               uint32_t n_obs, int state_s, HaloArgs h, const uint32_t* __restrict__ obs_site,
+                               const uint16_t* __restrict__ obs_iolet, const IoletDev* __restrict__ io,
+                               double* __restrict__ out_row) {
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n_obs) return;
+    const uint32_t s = obs_site[j];
+    double fl[kQ];
+    aa_gather<kP2P>(F, tab, P, s, state_s != 0, h, fl);
+    const Macro m = macro_of(fl);
+    const IoletDev& g = io[obs_iolet[j]];
+    double* o = out_row + 3 * uint64_t(j);
+    o[0] = sqrt((m.ux * m.ux + m.uy * m.uy) + m.uz * m.uz);
+    o[1] = kCs2 * m.rho;
+    o[2] = (m.ux * g.normal[0] + m.uy * g.normal[1]) + m.uz * g.normal[2];
+}
+
 // PostReceive re-allocation (engine.hpp:534-542): fn[recv_dest[k]] = fo[tail + k].
 __global__ void lbm_post_receive(const double* __restrict__ fo_tail, double* __restrict__ fn,
                                  const uint64_t* __restrict__ recv_flat, uint32_t n) {

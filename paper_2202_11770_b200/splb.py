@@ -160,6 +160,7 @@ class EngineParams:
     exchange_timeout_s: float = 30.0
     devices: Optional[List[int]] = None
     halo_mode: int = 0  # B200: 0 NCCL / peer copies + PostReceive, 1 fused NVLink P2P stores
+    storage: int = 0  # B200: 0 two buffers (push), 1 single buffer (AA pattern, in place)
 
 
 # ---- domain -----------------------------------------------------------------------
@@ -403,6 +404,7 @@ def _params_c(p: EngineParams):
     c.observe_iolets = 1 if p.observe_iolets else 0
     c.exchange_timeout_s = p.exchange_timeout_s
     c.halo_mode = p.halo_mode
+    c.storage = p.storage
     devs = None
     if p.devices:
         devs = np.array(p.devices, np.int32)

@@ -191,7 +191,7 @@ def total_mass(M, sim):
     return m
 
 
-def execute_run(M, run, devices=None, halo_mode=None):
+def execute_run(M, run, devices=None, halo_mode=None, storage=None):
     d = make_domain(M, DOMAINS[run["domain"]])
     p = M.EngineParams(tau=run.get("tau", 0.9), dt_s=run.get("dt", 1.0), workers=run["W"],
                        layout=run.get("layout", 0), sequence=run.get("sequence", 0),
@@ -200,6 +200,8 @@ def execute_run(M, run, devices=None, halo_mode=None):
         p.devices = devices
     if halo_mode is not None:
         p.halo_mode = halo_mode
+    if storage is not None:
+        p.storage = storage
     sim = M.Simulation(d, make_bcs(M, run["bcs"]), p)
     if "noise" in run:
         apply_noise(M, sim, noise_for(d.n_sites(), *run["noise"]))

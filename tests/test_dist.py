@@ -104,7 +104,8 @@ NCCL_SCRIPT = textwrap.dedent("""
                noise=(11, 0.01))
     d = cases.make_domain(P, cases.DOMAINS[run["domain"]])
     kw = dict(tau=0.8, dt_s=1e-3, workers=world, capture_period=20, observe_iolets=True)
-    prm = P.EngineParams(devices=[rank], halo_mode=int(os.environ["HALO"]), **kw)
+    mode = int(os.environ["HALO"])  # 0 NCCL, 1 fused P2P, 2 AA single buffer (P2P in place)
+    prm = P.EngineParams(devices=[rank], halo_mode=min(mode, 1), storage=1 if mode == 2 else 0, **kw)
     sim = P.Simulation.distributed(d, cases.make_bcs(P, run["bcs"]), prm, rank, world, obj[0])
     cases.apply_noise(P, sim, cases.noise_for(d.n_sites(), *run["noise"]))
     sim.run(25)
@@ -125,7 +126,7 @@ NCCL_SCRIPT = textwrap.dedent("""
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("halo", ["0", "1"])
+@pytest.mark.parametrize("halo", ["0", "1", "2"])
 def test_nccl_ranks_match_single_process(halo):
     """halo 0: NCCL send/recv + PostReceive; halo 1: fused NVLink P2P stores
     into IPC-mapped neighbour buffers, flag-synchronised."""

@@ -57,6 +57,35 @@ def test_fused_p2p_halo_bit_exact(product, golden, key):
     assert cases.run_digest(res) == golden["runs"][key]
 
 
+@pytest.mark.parametrize("key", sorted(cases.RUNS))
+def test_aa_single_buffer_bit_exact(product, golden, key):
+    """storage=1: one buffer updated in place with the AA pattern (even steps
+    local, odd steps gather/scatter, cut links read/written in the
+    neighbour's buffer).  Same bits as the reference for every golden run —
+    captures and series are taken in both AA states."""
+    res = cases.execute_run(product, cases.RUNS[key], storage=1)
+    assert cases.run_digest(res) == golden["runs"][key]
+
+
+def test_aa_store_views_odd_and_even(product):
+    """store(w).f_old() in the AA scheme equals the push engine's after odd
+    and even step counts (the state-S gather), for several workers."""
+    d = product.build_bifurcation(3, 2, 6, 8)
+    bcs = cases.make_bcs(product, ("bif", "bif_inlet"))
+    for W in (1, 3):
+        a = product.Simulation(d, bcs, product.EngineParams(tau=0.8, dt_s=1e-3, workers=W, layout=product.SOA))
+        b = product.Simulation(d, bcs, product.EngineParams(tau=0.8, dt_s=1e-3, workers=W, layout=product.SOA,
+                                                            storage=1))
+        for n in (7, 6):
+            a.run(n)
+            b.run(n)
+            for w in range(W):
+                fa, fb = a.store(w).f_old(), b.store(w).f_old()
+                n19 = 19 * a.store(w).n_sites
+                assert np.array_equal(fa[:n19], fb[:n19]), (W, n, w)
+            assert np.array_equal(a.snapshot_fields(), b.snapshot_fields())
+
+
 def test_fused_p2p_multi_gpu_in_process(product, golden):
     import torch
     n = torch.cuda.device_count()
@@ -66,6 +95,8 @@ def test_fused_p2p_multi_gpu_in_process(product, golden):
         for mode in (0, 1):
             res = cases.execute_run(product, cases.RUNS[key], devices=list(range(n)), halo_mode=mode)
             assert cases.run_digest(res) == golden["runs"][key], (key, mode)
+        res = cases.execute_run(product, cases.RUNS[key], devices=list(range(n)), storage=1)
+        assert cases.run_digest(res) == golden["runs"][key], (key, "aa")
 
 
 def test_live_reference_random_case(product, reference):
