@@ -196,6 +196,8 @@ def main():
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--quick", action="store_true", help="kernel-only number (tuning runs)")
+    ap.add_argument("--storage", default="two", choices=["two", "aa"],
+                    help="two buffers (push) or one buffer in place (AA pattern)")
     ap.add_argument("--halo", default="p2p", choices=["nccl", "p2p"],
                     help="N>1 halo exchange: NCCL send/recv + PostReceive, or fused NVLink P2P stores")
     args = ap.parse_args()
@@ -232,7 +234,8 @@ def main():
     d, bcs, p, desc = workload(P, name, args.scale)
     n = d.n_sites()
     halo_mode = 1 if args.halo == "p2p" else 0
-    sim = make_sim(P.EngineParams(workers=world, devices=[local], halo_mode=halo_mode, **p))
+    storage = 1 if args.storage == "aa" else 0
+    sim = make_sim(P.EngineParams(workers=world, devices=[local], halo_mode=halo_mode, storage=storage, **p))
     setup_s = time.time() - t_setup
 
     def barrier():
@@ -288,7 +291,8 @@ def main():
         return
     # e2e through the public API: run(1) per step with the iolet series on
     sim.close()
-    params_e = P.EngineParams(workers=world, devices=[local], observe_iolets=True, halo_mode=halo_mode, **p)
+    params_e = P.EngineParams(workers=world, devices=[local], observe_iolets=True, halo_mode=halo_mode,
+                              storage=storage, **p)
     sim = make_sim(params_e)
     for _ in range(args.warmup):
         sim.run(1)
