@@ -841,10 +841,12 @@ class Engine {
         // compressed table for the mid-group plain range
         wk.ctab_ok = false;
         if (wk.mp > 0) {
-            wk.PG = wk.P / 32 + 2;
-            int16_t* dt = wk.dtab.alloc<int16_t>(18 * wk.P + kTilePad);
+            // pitch of the group bases: a multiple of 4 (16-byte bulk copies) with
+            // room for the last tile's overhang; deltas padded likewise
+            wk.PG = (wk.P / 32 + 32 + 3) / 4 * 4;
+            int16_t* dt = wk.dtab.alloc<int16_t>(18 * wk.P + 4 * kTilePad);
             uint32_t* gb = wk.gbase.alloc<uint32_t>(18 * wk.PG);
-            CK(cudaMemsetAsync(dt, 0, (18 * wk.P + kTilePad) * sizeof(int16_t), s));
+            CK(cudaMemsetAsync(dt, 0, (18 * wk.P + 4 * kTilePad) * sizeof(int16_t), s));
             CK(cudaMemsetAsync(gb, 0, 18 * wk.PG * sizeof(uint32_t), s));
             DevMem cerr;
             unsigned* ce = cerr.alloc<unsigned>(1);
@@ -1385,6 +1387,26 @@ class Engine {
         lbm_aa_even_tma<T, S, B><<<grid, T, Lm::kBytes, s>>>(wk.f_old(), wk.P, b, e, omega);
     }
 
+    template <int T, int S, int B>
+    void launch_aa_odd_tmc(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e) {
+        using Lm = AaOddSmem<T, S, B>;
+        static int cfg_dev = -1, resident = 0;
+        if (cfg_dev != wk.dev) {
+            CK(cudaFuncSetAttribute(lbm_aa_odd_tmc<T, S, B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(Lm::kBytes)));
+            int per_sm = 0, sms = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lbm_aa_odd_tmc<T, S, B>, T, Lm::kBytes));
+            CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, wk.dev));
+            resident = std::max(1, per_sm) * sms;
+            cfg_dev = wk.dev;
+        }
+        const uint32_t base = b & ~127u;
+        const uint32_t ntiles = (e - base + T - 1) / T;
+        const unsigned grid = unsigned(std::min<uint32_t>(ntiles, uint32_t(resident)));
+        lbm_aa_odd_tmc<T, S, B><<<grid, T, Lm::kBytes, s>>>(wk.f_old(), wk.dtab.get<int16_t>(), wk.gbase.get<uint32_t>(),
+                                                             wk.tab.get<uint32_t>(), wk.P, wk.PG, b, e, omega);
+    }
+
     void launch_aa_range(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, bool iolet, const double* staged,
                          const int32_t* coords, bool timed, bool edge, bool odd) {
         if (e <= b) return;
@@ -1414,8 +1436,13 @@ class Engine {
             if (iolet) lbm_aa_odd<true, true, 128, 4><<<nb, 128, 0, s>>>(F, tab, wk.P, b, e, omega, ia, h);
             else lbm_aa_odd<false, true, 128, 4><<<nb, 128, 0, s>>>(F, tab, wk.P, b, e, omega, ia, h);
         } else {
+            const int v = plain_variant;
             if (iolet) lbm_aa_odd<true, false, 128, 4><<<nb, 128, 0, s>>>(F, tab, wk.P, b, e, omega, ia, h);
-            else lbm_aa_odd<false, false, 128, 4><<<nb, 128, 0, s>>>(F, tab, wk.P, b, e, omega, ia, h);
+            else if (timed && wk.ctab_ok && v != 60) {
+                if (v == 61) launch_aa_odd_tmc<128, 2, 4>(wk, s, b, e);
+                else if (v == 62) launch_aa_odd_tmc<256, 3, 2>(wk, s, b, e);
+                else launch_aa_odd_tmc<256, 2, 2>(wk, s, b, e);
+            } else lbm_aa_odd<false, false, 128, 4><<<nb, 128, 0, s>>>(F, tab, wk.P, b, e, omega, ia, h);
         }
         if (timed) {
             if (kernel_timing) CK(cudaEventRecord(e1, s));

@@ -675,6 +675,102 @@ lbm_aa_odd(double* __restrict__ F, const uint32_t* __restrict__ tab, uint64_t P,
     }
 }
 
+// Odd step over the mid-group plain range with the compressed table: a
+// persistent CTA streams each tile's int16 deltas and group bases into shared
+// memory with bulk async copies (2 stages) while the previous tile gathers,
+// collides and scatters; a table entry serves twice (direction inv(i) for the
+// gather of f_i, direction i for the store of h_i).
+template <int T, int S, int kMinBlocks>
+struct AaOddSmem {
+    static constexpr uint32_t kD = uint32_t(kQ - 1) * T * 2;          // deltas
+    static constexpr uint32_t kB = uint32_t(kQ - 1) * (T / 32) * 4;   // group bases
+    static constexpr uint32_t kStage = (kD + kB + 127) / 128 * 128;
+    static constexpr uint32_t kBytes = S * kStage + S * 8;
+};
+
+template <int T, int S, int kMinBlocks>
+__global__ void __launch_bounds__(T, kMinBlocks)
+lbm_aa_odd_tmc(double* __restrict__ F, const int16_t* __restrict__ dtab, const uint32_t* __restrict__ gbase,
+               const uint32_t* __restrict__ tab, uint64_t P, uint64_t PG, uint32_t begin, uint32_t end, double omega) {
+    using L = AaOddSmem<T, S, kMinBlocks>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S * L::kStage);
+    const uint32_t base = begin & ~127u;  // 16-byte aligned group-base copies (PG is a multiple of 4)
+    const uint32_t ntiles = (end - base + T - 1) / T;
+    const uint32_t G = gridDim.x;
+    const uint32_t tid = threadIdx.x;
+    const int lane = int(tid & 31), warp = int(tid >> 5);
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) mbar_init(&bar[s], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    const uint64_t policy = evict_normal_policy();
+    auto issue = [&](uint32_t k) {
+        const uint32_t tile = blockIdx.x + k * G;
+        if (tile >= ntiles) return;
+        const int st = int(k % S);
+        unsigned char* buf = smem + st * L::kStage;
+        const uint64_t t0 = uint64_t(base) + uint64_t(tile) * T;
+        mbar_expect_tx(&bar[st], L::kD + L::kB);
+#pragma unroll 1
+        for (int i = 0; i < kQ - 1; ++i) {
+            bulk_g2s(buf + i * T * 2, dtab + uint64_t(i) * P + t0, T * 2, &bar[st], policy);
+            bulk_g2s(buf + L::kD + i * (T / 32) * 4, gbase + uint64_t(i) * PG + (t0 >> 5), (T / 32) * 4, &bar[st],
+                     policy);
+        }
+    };
+    if (tid == 0)
+        for (uint32_t k = 0; k + 1 < uint32_t(S); ++k) issue(k);
+    for (uint32_t k = 0;; ++k) {
+        const uint32_t tile = blockIdx.x + k * G;
+        if (tile >= ntiles) break;
+        if (tid == 0) issue(k + S - 1);
+        const int st = int(k % S);
+        const uint32_t s = base + tile * T + tid;
+        mbar_wait(&bar[st], (k / S) & 1u);
+        const int16_t* ds = reinterpret_cast<const int16_t*>(smem + st * L::kStage);
+        const uint32_t* bs = reinterpret_cast<const uint32_t*>(smem + st * L::kStage + L::kD);
+        if (s >= begin && s < end) {
+            // target of direction j (1..18) from the compressed entry
+            auto target = [&](int j, uint64_t& addr, bool& special) {
+                const int d = ds[(j - 1) * T + tid];
+                if (d == kDeltaBounce) {
+                    special = true;
+                    addr = 0;
+                } else if (d == kDeltaEscape) {
+                    special = false;
+                    addr = tab[uint64_t(j - 1) * P + s];
+                } else {
+                    special = false;
+                    addr = uint32_t(bs[(j - 1) * (T / 32) + warp] + uint32_t(lane) + uint32_t(d));
+                }
+            };
+            double f[kQ];
+            f[0] = F[s];
+#pragma unroll
+            for (int i = 1; i < kQ; ++i) {
+                uint64_t a;
+                bool sp;
+                target(inv(i), a, sp);
+                f[i] = sp ? F[uint64_t(i) * P + s] : F[uint64_t(inv(i)) * P + a];
+            }
+            const Macro m = macro_of(f);
+            double feq[kQ];
+            feq_all(m.rho, m.ux, m.uy, m.uz, feq);
+            F[s] = relax(f[0], feq[0], omega);
+#pragma unroll
+            for (int i = 1; i < kQ; ++i) {
+                uint64_t a;
+                bool sp;
+                target(i, a, sp);
+                F[sp ? uint64_t(inv(i)) * P + s : uint64_t(i) * P + a] = relax(f[i], feq[i], omega);
+            }
+        }
+        __syncthreads();
+    }
+}
+
 // Gather the 19 populations of site s in the current AA state (state N:
 // plain reads; state S: the rule above).
 template <bool kP2P>

@@ -67,6 +67,16 @@ def test_aa_single_buffer_bit_exact(product, golden, key):
     assert cases.run_digest(res) == golden["runs"][key]
 
 
+@pytest.mark.parametrize("variant", ["60", "61", "62"])
+def test_aa_odd_kernel_variants(product, golden, variant, monkeypatch):
+    """Odd-step kernels: register gather (60) and TMA-staged compressed-table
+    shapes (61, 62; default = 256x2x2) give the reference's bits."""
+    monkeypatch.setenv("SPLBCU_PLAIN_VARIANT", variant)
+    for key in ("bif_W3_soa_reordered", "pipe_beat_6_30", "C1_pipe_16_128"):
+        res = cases.execute_run(product, cases.RUNS[key], storage=1)
+        assert cases.run_digest(res) == golden["runs"][key], key
+
+
 def test_aa_store_views_odd_and_even(product):
     """store(w).f_old() in the AA scheme equals the push engine's after odd
     and even step counts (the state-S gather), for several workers."""
