@@ -1438,10 +1438,19 @@ class Engine {
         } else {
             const int v = plain_variant;
             if (iolet) lbm_aa_odd<true, false, 128, 4><<<nb, 128, 0, s>>>(F, tab, wk.P, b, e, omega, ia, h);
-            else if (timed && wk.ctab_ok && v != 60) {
+            else if (timed && wk.ctab_ok && v >= 61 && v <= 63) {
                 if (v == 61) launch_aa_odd_tmc<128, 2, 4>(wk, s, b, e);
                 else if (v == 62) launch_aa_odd_tmc<256, 3, 2>(wk, s, b, e);
                 else launch_aa_odd_tmc<256, 2, 2>(wk, s, b, e);
+            } else if (timed && wk.ctab_ok && v != 60) {
+                // default: compressed table, one thread per site
+                const uint32_t b0 = b & ~31u;
+                if (v == 64)
+                    lbm_aa_odd_c<256, 2><<<unsigned((e - b0 + 255) / 256), 256, 0, s>>>(
+                        F, wk.dtab.get<int16_t>(), wk.gbase.get<uint32_t>(), tab, wk.P, wk.PG, b, e, omega);
+                else
+                    lbm_aa_odd_c<128, 4><<<unsigned((e - b0 + 127) / 128), 128, 0, s>>>(
+                        F, wk.dtab.get<int16_t>(), wk.gbase.get<uint32_t>(), tab, wk.P, wk.PG, b, e, omega);
             } else lbm_aa_odd<false, false, 128, 4><<<nb, 128, 0, s>>>(F, tab, wk.P, b, e, omega, ia, h);
         }
         if (timed) {

@@ -771,6 +771,47 @@ lbm_aa_odd_tmc(double* __restrict__ F, const int16_t* __restrict__ dtab, const u
     }
 }
 
+// Odd step, mid-group plain range, compressed table, one thread per site (no
+// CTA barrier: gathers of different CTAs overlap freely).  Bases travel by
+// warp shuffle; warps cover aligned 32-site groups.
+template <int kThreads, int kMinBlocks>
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
+lbm_aa_odd_c(double* __restrict__ F, const int16_t* __restrict__ dtab, const uint32_t* __restrict__ gbase,
+             const uint32_t* __restrict__ tab, uint64_t P, uint64_t PG, uint32_t begin, uint32_t end, double omega) {
+    const uint32_t s = (begin & ~31u) + blockIdx.x * kThreads + threadIdx.x;
+    const int lane = int(threadIdx.x & 31);
+    const bool live = s >= begin && s < end;
+    if (__all_sync(0xffffffffu, !live)) return;  // whole warp outside the range
+    int d[kQ - 1];
+#pragma unroll
+    for (int i = 0; i < kQ - 1; ++i) d[i] = live ? int(__ldg(dtab + uint64_t(i) * P + s)) : int(kDeltaBounce);
+    const uint32_t breg = lane < kQ - 1 ? __ldg(gbase + uint64_t(lane) * PG + (s >> 5)) : 0u;
+    // direction j's target site (or UINT32_MAX for bounce-back)
+    auto target = [&](int j) -> uint32_t {
+        const uint32_t b = __shfl_sync(0xffffffffu, breg, j - 1);
+        const int dj = d[j - 1];
+        if (dj == kDeltaBounce) return 0xffffffffu;
+        if (dj == kDeltaEscape) return live ? tab[uint64_t(j - 1) * P + s] : 0u;
+        return b + uint32_t(lane) + uint32_t(dj);
+    };
+    double f[kQ];
+    f[0] = live ? F[s] : 1.0;
+#pragma unroll
+    for (int i = 1; i < kQ; ++i) {
+        const uint32_t t = target(inv(i));
+        f[i] = !live ? 0.0 : (t == 0xffffffffu ? F[uint64_t(i) * P + s] : F[uint64_t(inv(i)) * P + t]);
+    }
+    const Macro m = macro_of(f);
+    double feq[kQ];
+    feq_all(m.rho, m.ux, m.uy, m.uz, feq);
+    if (live) F[s] = relax(f[0], feq[0], omega);
+#pragma unroll
+    for (int i = 1; i < kQ; ++i) {
+        const uint32_t t = target(i);
+        if (live) F[t == 0xffffffffu ? uint64_t(inv(i)) * P + s : uint64_t(i) * P + t] = relax(f[i], feq[i], omega);
+    }
+}
+
 // Gather the 19 populations of site s in the current AA state (state N:
 // plain reads; state S: the rule above).
 template <bool kP2P>
