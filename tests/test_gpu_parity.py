@@ -67,7 +67,7 @@ def test_aa_single_buffer_bit_exact(product, golden, key):
     assert cases.run_digest(res) == golden["runs"][key]
 
 
-@pytest.mark.parametrize("variant", ["0", "60", "61", "62", "63", "64"])
+@pytest.mark.parametrize("variant", ["0", "60", "61", "62", "63", "64", "65"])
 def test_aa_odd_kernel_variants(product, golden, variant, monkeypatch):
     """Odd-step kernels: register gather (60) and TMA-staged compressed-table
     shapes (61, 62; default = 256x2x2) give the reference's bits."""
