@@ -388,10 +388,12 @@ lbm_push_tmc(const double* __restrict__ fo, double* __restrict__ fn, const int16
             const double fpost = relax(f[i], feq[i], omega);
             const uint32_t b = __shfl_sync(0xffffffffu, breg, i - 1);
             const int d = dl[i - 1];
-            uint64_t dst;
-            if (d == kDeltaBounce) dst = uint64_t(inv(i)) * P + s;
-            else if (d == kDeltaEscape) dst = uint64_t(i) * P + (live ? tab[uint64_t(i - 1) * P + s] : 0u);
-            else dst = uint64_t(i) * P + uint32_t(b + uint32_t(lane) + uint32_t(d));
+            // branch-free address select; the rare escape is a predicated load
+            uint32_t t = b + uint32_t(lane) + uint32_t(d);
+            if ((kHints & 8) == 0 || d == kDeltaEscape) {
+                if (d == kDeltaEscape && live) t = tab[uint64_t(i - 1) * P + s];
+            }
+            const uint64_t dst = d == kDeltaBounce ? uint64_t(inv(i)) * P + s : uint64_t(i) * P + t;
             if (live) fn[dst] = fpost;
         }
         __syncthreads();  // stage st is free for the copy issued next iteration
