@@ -951,9 +951,11 @@ class Engine {
         const uint32_t base = b & ~31u;
         const uint32_t ntiles = (e - base + T - 1) / T;
         const unsigned grid = unsigned(std::min<uint32_t>(ntiles, uint32_t(resident)));
+        Planes19 pl;
+        for (int i = 0; i < kQ; ++i) pl.p[i] = wk.f_new() + uint64_t(i) * wk.P;
         lbm_push_tmc<T, S, B, H><<<grid, T, Lm::kBytes, s>>>(wk.f_old(), wk.f_new(), wk.dtab.get<int16_t>(),
                                                               wk.gbase.get<uint32_t>(), wk.tab.get<uint32_t>(), wk.P,
-                                                              wk.PG, b, e, omega);
+                                                              wk.PG, b, e, omega, pl);
     }
 
     void launch_plain(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia, bool mid) {

@@ -279,6 +279,13 @@ lbm_push_tma(const double* __restrict__ fo, double* __restrict__ fn, const uint3
     }
 }
 
+// Base address of each direction plane of f_new (fn + i*P), passed by value
+// so per-store address math reads the constant bank instead of recomputing
+// 64-bit plane offsets.
+struct Planes19 {
+    double* p[kQ];
+};
+
 // ---- compressed neighbour table (mid-group plain sites) --------------------
 // The mid-group plain range has only ToLocal and bounce-back links (shared
 // slots occur only at edge sites, iolet links only at iolet sites).  Inside a
@@ -333,7 +340,7 @@ template <int T, int S, int kMinBlocks, int kHints = 2>
 __global__ void __launch_bounds__(T, kMinBlocks)
 lbm_push_tmc(const double* __restrict__ fo, double* __restrict__ fn, const int16_t* __restrict__ dtab,
              const uint32_t* __restrict__ gbase, const uint32_t* __restrict__ tab, uint64_t P, uint64_t PG,
-             uint32_t begin, uint32_t end, double omega) {
+             uint32_t begin, uint32_t end, double omega, const __grid_constant__ Planes19 planes) {
     using L = PushTmaSmem<T, S, false>;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S * L::kStage);
@@ -393,8 +400,9 @@ lbm_push_tmc(const double* __restrict__ fo, double* __restrict__ fn, const int16
             if ((kHints & 8) == 0 || d == kDeltaEscape) {
                 if (d == kDeltaEscape && live) t = tab[uint64_t(i - 1) * P + s];
             }
-            const uint64_t dst = d == kDeltaBounce ? uint64_t(inv(i)) * P + s : uint64_t(i) * P + t;
-            if (live) fn[dst] = fpost;
+            // plane base addresses come from the constant bank (kernel params)
+            double* dst = d == kDeltaBounce ? planes.p[inv(i)] + s : planes.p[i] + t;
+            if (live) *dst = fpost;
         }
         __syncthreads();  // stage st is free for the copy issued next iteration
     }
