@@ -395,13 +395,17 @@ lbm_push_tmc(const double* __restrict__ fo, double* __restrict__ fn, const int16
             const double fpost = relax(f[i], feq[i], omega);
             const uint32_t b = __shfl_sync(0xffffffffu, breg, i - 1);
             const int d = dl[i - 1];
-            // branch-free address select; the rare escape is a predicated load
+            // branch-free: the rare escape is a predicated load (inline PTX so
+            // no divergent block is formed), the bounce case a select; plane
+            // base addresses come from the constant bank (kernel params)
             uint32_t t = b + uint32_t(lane) + uint32_t(d);
-            if ((kHints & 8) == 0 || d == kDeltaEscape) {
-                if (d == kDeltaEscape && live) t = tab[uint64_t(i - 1) * P + s];
-            }
-            // plane base addresses come from the constant bank (kernel params)
-            double* dst = d == kDeltaBounce ? planes.p[inv(i)] + s : planes.p[i] + t;
+            const uint32_t esc = (d == kDeltaEscape) && live;
+            asm("{\n .reg .pred p;\n setp.ne.u32 p, %1, 0;\n @p ld.global.nc.u32 %0, [%2];\n}"
+                : "+r"(t)
+                : "r"(esc), "l"(tab + uint64_t(i - 1) * P + s));
+            const bool bb = d == kDeltaBounce;
+            const uintptr_t pb = reinterpret_cast<uintptr_t>(bb ? planes.p[inv(i)] : planes.p[i]);
+            double* dst = reinterpret_cast<double*>(pb) + (bb ? s : t);
             if (live) *dst = fpost;
         }
         __syncthreads();  // stage st is free for the copy issued next iteration
