@@ -268,20 +268,23 @@ def main():
     value = n * args.steps / dev_s / 1e6
     ks, kl, kn = k1[0] - k0[0], k1[1] - k0[1], k1[2] - k0[2]
     hbm, src = peaks()
-    achieved = (kn / kl) * BYTES_PER_SITE / (ks / kl) / 1e9 if kl else None
     traffic = load_profile_traffic()
     # The default kernel reads a compressed table (int16 deltas + a u32 base per
-    # 32 sites): its own algorithmic bytes are 304 + 18*(2 + 4/32) = 342.25
-    # B/site.  `achieved`/`frac` use SURVEY §8d's 376 B/site (the reference
-    # data layout's bytes, so the number is comparable across layouts);
-    # `achieved_design` is the DRAM rate the kernel's own bytes imply.
-    achieved_design = (kn / kl) * DESIGN_BYTES_PER_SITE / (ks / kl) / 1e9 if kl else None
+    # 32 sites): its algorithmic bytes are 304 + 18*(2 + 4/32) = 342.25 B/site
+    # (AA storage: even steps 304, odd steps 376 -> 340 on average).
+    # `achieved`/`frac` use those bytes (the DRAM rate the kernel really
+    # sustains); `achieved_376`/`frac_376` restate it in SURVEY §8d's
+    # 376 B/site (the reference data layout), which can exceed 1.0 because the
+    # kernel moves fewer bytes than that layout.
+    bps = 340.0 if args.storage == "aa" else DESIGN_BYTES_PER_SITE
+    achieved = (kn / kl) * bps / (ks / kl) / 1e9 if kl else None
+    achieved_376 = (kn / kl) * BYTES_PER_SITE / (ks / kl) / 1e9 if kl else None
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
             "frac": achieved / hbm if achieved else None,
             "traffic": (traffic * kn / kl) if (traffic and kl) else None,
             "peak_source": src, "kernel": "lbm_push_tmc (Inner+Wall fused collide+stream, TMA-pipelined)",
-            "bytes_per_site": BYTES_PER_SITE, "design_bytes_per_site": DESIGN_BYTES_PER_SITE,
-            "achieved_design": achieved_design, "frac_design": achieved_design / hbm if achieved_design else None,
+            "bytes_per_site": bps, "achieved_376": achieved_376,
+            "frac_376": achieved_376 / hbm if achieved_376 else None,
             "sites_per_launch": kn / kl if kl else None, "avg_launch_ms": ks / kl * 1e3 if kl else None,
             "kernel_share": ks / dev_s if dev_s else None}
 

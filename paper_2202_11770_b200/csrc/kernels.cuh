@@ -800,20 +800,27 @@ lbm_aa_odd_c(double* __restrict__ F, const int16_t* __restrict__ dtab, const uin
 #pragma unroll
     for (int i = 0; i < kQ - 1; ++i) d[i] = live ? int(__ldg(dtab + uint64_t(i) * P + s)) : int(kDeltaBounce);
     const uint32_t breg = lane < kQ - 1 ? __ldg(gbase + uint64_t(lane) * PG + (s >> 5)) : 0u;
-    // direction j's target site (or UINT32_MAX for bounce-back)
-    auto target = [&](int j) -> uint32_t {
+    // direction j's target site; bounce-back -> (s, mirrored plane).  Branch-free:
+    // the escape is a predicated load, the bounce a select.
+    auto target = [&](int j, bool& bb) -> uint32_t {
         const uint32_t b = __shfl_sync(0xffffffffu, breg, j - 1);
         const int dj = d[j - 1];
-        if (dj == kDeltaBounce) return 0xffffffffu;
-        if (dj == kDeltaEscape) return live ? tab[uint64_t(j - 1) * P + s] : 0u;
-        return b + uint32_t(lane) + uint32_t(dj);
+        uint32_t t = b + uint32_t(lane) + uint32_t(dj);
+        const uint32_t esc = (dj == kDeltaEscape) && live;
+        asm("{\n .reg .pred p;\n setp.ne.u32 p, %1, 0;\n @p ld.global.nc.u32 %0, [%2];\n}"
+            : "+r"(t)
+            : "r"(esc), "l"(tab + uint64_t(j - 1) * P + s));
+        bb = dj == kDeltaBounce;
+        return bb ? s : t;
     };
     double f[kQ];
     f[0] = live ? F[s] : 1.0;
 #pragma unroll
     for (int i = 1; i < kQ; ++i) {
-        const uint32_t t = target(inv(i));
-        f[i] = !live ? 0.0 : (t == 0xffffffffu ? F[uint64_t(i) * P + s] : F[uint64_t(inv(i)) * P + t]);
+        bool bb;
+        const uint32_t t = target(inv(i), bb);
+        const double* src = (bb ? F + uint64_t(i) * P : F + uint64_t(inv(i)) * P) + t;
+        f[i] = live ? *src : 0.0;
     }
     const Macro m = macro_of(f);
     double feq[kQ];
@@ -821,8 +828,10 @@ lbm_aa_odd_c(double* __restrict__ F, const int16_t* __restrict__ dtab, const uin
     if (live) F[s] = relax(f[0], feq[0], omega);
 #pragma unroll
     for (int i = 1; i < kQ; ++i) {
-        const uint32_t t = target(i);
-        if (live) F[t == 0xffffffffu ? uint64_t(inv(i)) * P + s : uint64_t(i) * P + t] = relax(f[i], feq[i], omega);
+        bool bb;
+        const uint32_t t = target(i, bb);
+        double* dst = (bb ? F + uint64_t(inv(i)) * P : F + uint64_t(i) * P) + t;
+        if (live) *dst = relax(f[i], feq[i], omega);
     }
 }
 
