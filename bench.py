@@ -308,11 +308,13 @@ def main():
     e2e_s = max_over_ranks(time.perf_counter() - t0)
     ser = sim.series()
     n_obs = sum(1 for _ in ser["flow"])
-    e = d.export() if n < 2e7 else None
+    # observed sites (any iolet link): the per-step observation row is 24 B each
+    e = d.export() if rank == 0 else None
     obs_sites = 0
     if e is not None:
         lk = e["link_kind"]
         obs_sites = int(((lk >= 2).any(1)).sum())
+        del e, lk
     e2e = {"value": n * e2e_steps / e2e_s / 1e6, "unit": "MSUPS",
            "h2d_bytes_per_step": 8 * len(bcs.entries), "d2h_bytes_per_step": 24 * obs_sites,
            "note": "Simulation.run(1) per step via the C-ABI, iolet series on (per-step BC staging H2D, "

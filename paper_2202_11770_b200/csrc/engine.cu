@@ -142,6 +142,40 @@ struct DevMem {
         CK(cudaMalloc(&p, bytes));
         return static_cast<T*>(p);
     }
+    // Keeps the allocation when it is already large enough (no cudaFree /
+    // cudaMalloc, which synchronise the device, on the per-run path).
+    template <class T>
+    T* reserve(size_t n) {
+        if (!p || bytes < n * sizeof(T)) return alloc<T>(n);
+        return static_cast<T*>(p);
+    }
+    template <class T>
+    T* get() const { return static_cast<T*>(p); }
+};
+
+// Page-locked host buffer (portable across the process's devices) so the
+// per-run staging H2D and observation D2H are true async DMA.
+struct PinnedMem {
+    void* p = nullptr;
+    size_t bytes = 0;
+    PinnedMem() = default;
+    PinnedMem(const PinnedMem&) = delete;
+    PinnedMem& operator=(const PinnedMem&) = delete;
+    ~PinnedMem() {
+        if (p) cudaFreeHost(p);
+    }
+    template <class T>
+    T* reserve(size_t n) {
+        const size_t need = std::max<size_t>(n * sizeof(T), 16);
+        if (!p || bytes < need) {
+            if (p) cudaFreeHost(p);
+            p = nullptr;
+            bytes = 0;
+            CK(cudaHostAlloc(&p, need, cudaHostAllocPortable));
+            bytes = need;
+        }
+        return static_cast<T*>(p);
+    }
     template <class T>
     T* get() const { return static_cast<T*>(p); }
 };
@@ -272,6 +306,8 @@ struct WorkerDev {
     int w = 0, dev = 0;
     cudaStream_t sE = nullptr, sM = nullptr;
     cudaEvent_t evSend = nullptr, evMid = nullptr, evEnd = nullptr;
+    cudaEvent_t evRun0 = nullptr, evRun1 = nullptr, evDone = nullptr;  // run() bracket + host-copy completion
+    PinnedMem h_obs;                                                   // observation rows, D2H target
     uint32_t n = 0, n_edge = 0, ep = 0, mp = 0;  // ranges: [0,ep) [ep,n_edge) [n_edge,n_edge+mp) [.., n)
     uint64_t P = 0;
     uint32_t shared = 0;
@@ -321,6 +357,18 @@ class Engine {
     ncclComm_t comm = nullptr;
     std::vector<Capture> caps;
     Series series;
+    PinnedMem h_staged;  // per-run iolet values (run() staging)
+    DevMem obs_gather;   // dist mode: every rank's observation rows (padded)
+    PinnedMem h_gather;
+
+    // dist mode: elements per rank in the padded all-gather of observation
+    // rows (every rank's obs_buf is reserved to this size)
+    uint64_t obs_gather_per(const WorkerDev& wk) const {
+        const size_t n_io = dom.iolets.size();
+        uint64_t maxn = 1;
+        for (auto& o : obs_off_all) maxn = std::max<uint64_t>(maxn, o[n_io]);
+        return 3 * wk.obs_rows * maxn;
+    }
     std::vector<std::vector<std::pair<int, uint32_t>>> obs_order;  // per iolet: (worker, pos)
     std::vector<std::vector<uint32_t>> obs_off_all;  // per worker: per-iolet offsets (+ total), all workers
     uint64_t steps_run = 0;
@@ -579,6 +627,9 @@ class Engine {
             if (wp->evSend) cudaEventDestroy(wp->evSend);
             if (wp->evMid) cudaEventDestroy(wp->evMid);
             if (wp->evEnd) cudaEventDestroy(wp->evEnd);
+            if (wp->evRun0) cudaEventDestroy(wp->evRun0);
+            if (wp->evRun1) cudaEventDestroy(wp->evRun1);
+            if (wp->evDone) cudaEventDestroy(wp->evDone);
             if (wp->sE) cudaStreamDestroy(wp->sE);
             if (wp->sM) cudaStreamDestroy(wp->sM);
         }
@@ -636,6 +687,9 @@ class Engine {
         CK(cudaEventCreateWithFlags(&wk.evSend, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&wk.evMid, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&wk.evEnd, cudaEventDisableTiming));
+        CK(cudaEventCreate(&wk.evRun0));
+        CK(cudaEventCreate(&wk.evRun1));
+        CK(cudaEventCreateWithFlags(&wk.evDone, cudaEventDisableTiming));
         cudaStream_t s = wk.sM;
 
         const WorkerPart& wp = part.parts[size_t(w)];
@@ -1250,7 +1304,8 @@ class Engine {
                 wp->obs_row_base = first;
                 wp->obs_rows = rows - first;
                 CK(cudaSetDevice(wp->dev));
-                wp->obs_buf.alloc<double>(3 * std::max<uint64_t>(wp->obs_rows * wp->n_obs, 1));
+                wp->obs_buf.reserve<double>(dist ? obs_gather_per(*wp)
+                                                 : 3 * std::max<uint64_t>(wp->obs_rows * wp->n_obs, 1));
             }
         }
     }
@@ -1266,8 +1321,12 @@ class Engine {
                     record_state(*wp, wp->sM, 0, wp->f_old());
                 }
         // host staging of the per-step iolet values (engine.hpp:332-341)
+        // into a pinned buffer, copied stream-ordered ahead of the step loop (the
+        // previous run() has completed, so the buffer is free to overwrite)
         const size_t n_io = bcs.size();
-        std::vector<double> staged(std::max<size_t>(n * n_io, 1), 0.0);
+        const size_t n_staged = std::max<size_t>(n * n_io, 1);
+        double* staged = h_staged.reserve<double>(n_staged);
+        staged[0] = 0.0;
         for (uint64_t k = 0; k < n; ++k) {
             const double t = double(steps_run + k + 1) * prm.dt_s;
             for (size_t io = 0; io < n_io; ++io) {
@@ -1278,17 +1337,13 @@ class Engine {
         for (auto& wp : W) {
             if (!wp) continue;
             CK(cudaSetDevice(wp->dev));
-            upload(wp->staged, staged, wp->sM);
-            CK(cudaStreamSynchronize(wp->sM));
+            double* d = wp->staged.reserve<double>(n_staged);
+            CK(cudaMemcpyAsync(d, staged, n_staged * sizeof(double), cudaMemcpyHostToDevice, wp->sM));
             wp->tev_used = 0;
         }
-        std::vector<cudaEvent_t> t0(W.size(), nullptr), t1(W.size(), nullptr);
+        std::vector<cudaEvent_t> t0(W.size(), nullptr), t1(W.size(), nullptr), done(W.size(), nullptr);
         for (size_t w = 0; w < W.size(); ++w)
-            if (W[w]) {
-                CK(cudaSetDevice(W[w]->dev));
-                CK(cudaEventCreate(&t0[w]));
-                CK(cudaEventCreate(&t1[w]));
-            }
+            if (W[w]) t0[w] = W[w]->evRun0, t1[w] = W[w]->evRun1, done[w] = W[w]->evDone;
         const auto h0 = std::chrono::steady_clock::now();
         for (size_t w = 0; w < W.size(); ++w)
             if (W[w]) {
@@ -1306,8 +1361,27 @@ class Engine {
             if (W[w]) {
                 CK(cudaSetDevice(W[w]->dev));
                 CK(cudaEventRecord(t1[w], W[w]->sM));
+                // this run's observation rows, behind the loop: one device
+                // all-gather (dist mode) and one async copy into pinned memory
+                WorkerDev& wk = *W[w];
+                if (prm.observe_iolets && dist) {
+                    const uint64_t per = obs_gather_per(wk);
+                    CK(cudaStreamWaitEvent(wk.sE, t1[w], 0));
+                    double* dr = obs_gather.reserve<double>(per * uint64_t(nranks));
+                    NK(nccl().AllGather(wk.obs_buf.get<double>(), dr, per, ncclDouble, comm, wk.sE));
+                    double* h = h_gather.reserve<double>(per * uint64_t(nranks));
+                    CK(cudaMemcpyAsync(h, dr, per * uint64_t(nranks) * 8, cudaMemcpyDeviceToHost, wk.sE));
+                    CK(cudaEventRecord(done[w], wk.sE));
+                    continue;
+                }
+                const size_t nb = prm.observe_iolets ? 3 * wk.obs_rows * wk.n_obs : 0;
+                if (nb) {
+                    double* h = wk.h_obs.reserve<double>(nb);
+                    CK(cudaMemcpyAsync(h, wk.obs_buf.get<double>(), nb * 8, cudaMemcpyDeviceToHost, wk.sM));
+                }
+                CK(cudaEventRecord(done[w], wk.sM));
             }
-        wait_all(t1);
+        wait_all(done);
         const auto h1 = std::chrono::steady_clock::now();
         double dmax = 0.0;
         for (size_t w = 0; w < W.size(); ++w)
@@ -1321,8 +1395,6 @@ class Engine {
                         CK(cudaEventElapsedTime(&kms, W[w]->tev[q], W[w]->tev[q + 1]));
                         plain_s += double(kms) * 1e-3;
                     }
-                cudaEventDestroy(t0[w]);
-                cudaEventDestroy(t1[w]);
             }
         dev_loop_s += dmax;
         loop_s += std::chrono::duration<double>(h1 - h0).count();
@@ -1363,7 +1435,9 @@ class Engine {
                     fail(ErrKind::Comm, "exchange failure: worker " + std::to_string(w) +
                                             " timed out waiting for neighbor " + std::to_string(nb));
                 }
-                std::this_thread::sleep_for(std::chrono::microseconds(50));
+                // spin (yielding) for short runs, then back off
+                if (el < 0.02) std::this_thread::yield();
+                else std::this_thread::sleep_for(std::chrono::microseconds(50));
             }
         }
     }
@@ -1624,31 +1698,19 @@ class Engine {
     void assemble_series() {
         if (!prm.observe_iolets) return;
         const size_t n_io = dom.iolets.size();
-        std::vector<std::vector<double>> hb(W.size());
-        for (size_t w = 0; w < W.size(); ++w) {
-            if (!W[w]) continue;
-            WorkerDev& wk = *W[w];
-            CK(cudaSetDevice(wk.dev));
-            hb[w].resize(3 * wk.obs_rows * wk.n_obs);
-            if (!hb[w].empty())
-                CK(cudaMemcpy(hb[w].data(), wk.obs_buf.get<double>(), hb[w].size() * 8, cudaMemcpyDeviceToHost));
-        }
+        // this run's rows were copied into each worker's pinned h_obs by run()
+        std::vector<const double*> hb(W.size(), nullptr);
+        for (size_t w = 0; w < W.size(); ++w)
+            if (W[w]) hb[w] = W[w]->h_obs.get<double>();
         const uint64_t first_row = series.rows;
         const uint64_t rows = steps_run + 1;
-        uint64_t row_base = 0, nrows = 0;
+        uint64_t row_base = 0;
         for (auto& wp : W)
-            if (wp) row_base = wp->obs_row_base, nrows = wp->obs_rows;
+            if (wp) row_base = wp->obs_row_base;
         if (dist) {
-            // every rank needs every worker's rows: all-gather (padded)
-            uint64_t maxn = 0;
-            for (auto& o : obs_off_all) maxn = std::max<uint64_t>(maxn, o[n_io]);
-            const uint64_t per = 3 * nrows * std::max<uint64_t>(maxn, 1);
-            std::vector<double> mine(per, 0.0);
-            std::copy(hb[size_t(rank)].begin(), hb[size_t(rank)].end(), mine.begin());
-            const std::vector<double> all = allgather_host(mine);
-            for (int w = 0; w < prm.workers; ++w)
-                hb[size_t(w)].assign(all.begin() + int64_t(per) * w,
-                                     all.begin() + int64_t(per) * w + int64_t(3 * nrows * obs_off_all[size_t(w)][n_io]));
+            // every worker's rows, all-gathered (padded) on the device by run()
+            const uint64_t per = obs_gather_per(*W[size_t(rank)]);
+            for (int w = 0; w < prm.workers; ++w) hb[size_t(w)] = h_gather.get<double>() + per * uint64_t(w);
         }
         series.max_speed.resize(n_io);
         series.pressure.resize(n_io);
@@ -1658,7 +1720,7 @@ class Engine {
                 double vmax = 0.0, psum = 0.0, qsum = 0.0;
                 for (const auto& [w, pos] : obs_order[k]) {
                     const std::vector<uint32_t>& off = obs_off_all[size_t(w)];
-                    const double* v = &hb[size_t(w)][3 * ((row - row_base) * off[n_io] + off[k] + pos)];
+                    const double* v = hb[size_t(w)] + 3 * ((row - row_base) * off[n_io] + off[k] + pos);
                     vmax = std::max(vmax, v[0]);
                     psum += v[1];
                     qsum += v[2];
