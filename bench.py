@@ -52,29 +52,42 @@ def peaks():
         return 6650.0, "fallback"
 
 
-def workload(M, name, scale=1.0):
-    """Returns (domain, bcs, params, description)."""
+def workload(M, name, scale=1.0, source=False):
+    """Returns (domain, bcs, params, description).  source=True returns the
+    geometry as a Source instead (slab-local construction on each rank)."""
+    def geo(kind, *args):
+        return getattr(M.Source, kind)(*args) if source else getattr(M, "build_" + kind)(*args)
+
     if name == "c2":
         L = max(4, int(round(1400 * scale)))
-        d = M.build_pipe(48, L)
+        d = geo("pipe", 48, L)
         bcs = M.BCSet([M.BCEntry(M.VELOCITY, M.TimeTable(*BEAT)), M.BCEntry(M.PRESSURE, M.TimeTable.constant(CS2))])
         return d, bcs, dict(tau=0.8, dt_s=DT_BEAT), f"C2 pipe R=48 L={L}, 60-bpm velocity inlet, p_out=1/3, tau=0.8"
     if name == "c1":
-        d = M.build_pipe(16, 128)
+        d = geo("pipe", 16, 128)
         dp = 0.02 * 4.0 * (CS2 * 0.4) * 128 / 256.0
         bcs = M.BCSet([M.BCEntry(M.PRESSURE, M.TimeTable.constant(CS2 + dp / 2)),
                        M.BCEntry(M.PRESSURE, M.TimeTable.constant(CS2 - dp / 2))])
         return d, bcs, dict(tau=0.9, dt_s=1.0), "C1 Poiseuille pipe R=16 L=128, pressure iolets, tau=0.9"
     if name == "c3":
         levels = 6  # R0=80, L0=800: 107,037,564 sites, 64 outlets
-        d = M.build_tree(80, max(8, int(round(800 * scale))), levels, 0.8, 0.8)
+        d = geo("tree", 80, max(8, int(round(800 * scale))), levels, 0.8, 0.8)
         n_out = 2 ** levels
         ents = [M.BCEntry(M.PRESSURE, M.TimeTable.constant(CS2 * 1.001))]
         ents += [M.BCEntry(M.PRESSURE, M.TimeTable.constant(CS2 * 0.999)) for _ in range(n_out)]
         return d, M.BCSet(ents), dict(tau=0.8, dt_s=1.0), f"C3 bifurcating tree R0=80 L0={max(8, int(round(800 * scale)))}, {levels} levels, pressure iolets"
+    if name == "c5":
+        # sparse vasculature, ~1e9 sites (SURVEY §8d C5): R0=160, L0=1600, 7 levels
+        # -> 1.01e9 sites at scale 1, ~1.2 % of its bounding box, 129 iolets
+        levels = 7
+        L0 = max(8, int(round(1600 * scale)))
+        d = geo("tree", 160, L0, levels, 0.8, 0.8)
+        ents = [M.BCEntry(M.PRESSURE, M.TimeTable.constant(CS2 * 1.001))]
+        ents += [M.BCEntry(M.PRESSURE, M.TimeTable.constant(CS2 * 0.999)) for _ in range(2 ** levels)]
+        return d, M.BCSet(ents), dict(tau=0.8, dt_s=1.0), f"C5 sparse vascular tree R0=160 L0={L0}, {levels} levels, pressure iolets"
     if name == "c4":
         nz = int(round(2400 * scale))
-        d = M.build_channel(256, 256, nz)
+        d = geo("channel", 256, 256, nz)
         bcs = M.BCSet([M.BCEntry(M.PRESSURE, M.TimeTable.constant(CS2 * 1.001)),
                        M.BCEntry(M.PRESSURE, M.TimeTable.constant(CS2 * 0.999))])
         return d, bcs, dict(tau=0.8, dt_s=1.0), f"C4 dense channel 256x256x{nz}"
@@ -123,11 +136,11 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(sm)}
 
 
-def cpu_reference_run(name, steps_cap, seconds, scale):
+def cpu_reference_run(name, steps_cap, seconds, scale, warmup=1):
     """The unmodified reference (oracle/_ref) on all host cores."""
     import impls
     R = impls.reference()
-    if name in ("c3", "c4"):
+    if name in ("c3", "c4", "c5"):
         # The reference has no tree/channel generator: the product's
         # generator makes the (bounded) sample, handed over as plain arrays
         # (SparseDomain fields) — the reference's own engine runs it.
@@ -135,6 +148,9 @@ def cpu_reference_run(name, steps_cap, seconds, scale):
         if name == "c3":
             dp = Pm.build_tree(32, 160, 6, 0.8, 0.8)
             desc = "C3-shaped tree sample R0=32 L0=160, 6 levels (product generator -> reference SparseDomain)"
+        elif name == "c5":
+            dp = Pm.build_tree(32, 320, 7, 0.8, 0.8)
+            desc = "C5-shaped tree sample R0=32 L0=320, 7 levels (product generator -> reference SparseDomain)"
         else:
             dp = Pm.build_channel(128, 128, 200)
             desc = "C4-shaped channel sample 128x128x200 (product generator -> reference SparseDomain)"
@@ -150,7 +166,7 @@ def cpu_reference_run(name, steps_cap, seconds, scale):
         d, bcs, p, desc = workload(R, name, scale)
     cores = os.cpu_count() or 1
     sim = R.Simulation(d, bcs, R.EngineParams(workers=cores, layout=R.SOA, **p))
-    sim.run(1)  # warm-up
+    sim.run(max(1, warmup))  # untimed warm-up steps
     t0 = sim.step_loop_seconds()
     steps = 0
     while steps < steps_cap and (sim.step_loop_seconds() - t0) < seconds:
@@ -175,9 +191,9 @@ def run_reference_arm(args):
         return
     name = args.workload or ("c2" if args.gpus == 1 else "c3")
     scale = 1.0 if name == "c2" else 0.25
-    v, cores, steps, n, desc = cpu_reference_run(name, max(args.steps, 1), 60.0, scale)
+    v, cores, steps, n, desc = cpu_reference_run(name, max(args.steps, 1), 60.0, scale, args.warmup)
     line = {"impl": "reference", "metric": "MSUPS", "value": v, "unit": "MSUPS", "n_gpus": args.gpus,
-            "steps": steps, "warmup": 1, "ms_per_step": n / (v * 1e6) * 1e3, "higher_is_better": True,
+            "steps": steps, "warmup": args.warmup, "ms_per_step": n / (v * 1e6) * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": desc, "sites": n, "parallelism": f"{cores} CPU worker threads"},
             "cpu_baseline": {"value": v, "unit": "MSUPS", "cores": cores, "kind": "reference",
@@ -200,6 +216,9 @@ def main():
                     help="two buffers (push) or one buffer in place (AA pattern)")
     ap.add_argument("--halo", default="p2p", choices=["nccl", "p2p"],
                     help="N>1 halo exchange: NCCL send/recv + PostReceive, or fused NVLink P2P stores")
+    ap.add_argument("--geometry", default="source", choices=["source", "domain"],
+                    help="N>1: each rank classifies only its own slab of the generator (source) "
+                         "or every rank builds the whole domain")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -231,11 +250,13 @@ def main():
         return P.Simulation.distributed(d, bcs, params, rank, world, bytes(t.cpu().tolist()))
 
     t_setup = time.time()
-    d, bcs, p, desc = workload(P, name, args.scale)
-    n = d.n_sites()
+    slab_src = world > 1 and args.geometry == "source"
+    d, bcs, p, desc = workload(P, name, args.scale, source=slab_src)
     halo_mode = 1 if args.halo == "p2p" else 0
     storage = 1 if args.storage == "aa" else 0
     sim = make_sim(P.EngineParams(workers=world, devices=[local], halo_mode=halo_mode, storage=storage, **p))
+    n = sim.n_sites()
+    sim_slab = sim.slab_local()
     setup_s = time.time() - t_setup
 
     def barrier():
@@ -308,13 +329,9 @@ def main():
     e2e_s = max_over_ranks(time.perf_counter() - t0)
     ser = sim.series()
     n_obs = sum(1 for _ in ser["flow"])
-    # observed sites (any iolet link): the per-step observation row is 24 B each
-    e = d.export() if rank == 0 else None
-    obs_sites = 0
-    if e is not None:
-        lk = e["link_kind"]
-        obs_sites = int(((lk >= 2).any(1)).sum())
-        del e, lk
+    # observation entries (sites x iolets they observe): the per-step row is
+    # 24 B each, device -> host
+    obs_sites = sim.observed_sites()
     e2e = {"value": n * e2e_steps / e2e_s / 1e6, "unit": "MSUPS",
            "h2d_bytes_per_step": 8 * len(bcs.entries), "d2h_bytes_per_step": 24 * obs_sites,
            "note": "Simulation.run(1) per step via the C-ABI, iolet series on (per-step BC staging H2D, "
@@ -339,7 +356,9 @@ def main():
                            "halo": (("NCCL send/recv + PostReceive" if halo_mode == 0 else "fused NVLink P2P stores")
                                     if world > 1 else "none"),
                            "l2": "inputs (f, table) 3.8 GB per step >> 126 MB L2; no flush needed",
-                           "setup_s": round(setup_s, 2)},
+                           "setup_s": round(setup_s, 2),
+                           "geometry": ("slab-local (each rank classifies its own slices)" if sim_slab
+                                        else "whole domain on every rank")},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(launches),
                 "clocks": clk.summary()}

@@ -166,6 +166,35 @@ int splbcu_domain_export(const splbcu_domain* d, int32_t* coords, uint8_t* types
                          splbcu_iolet* iolets, uint64_t* type_ranges);
 void splbcu_domain_free(splbcu_domain* d);
 
+/* ---- geometry sources (slab-local construction) -------------
+ * A source is a generator evaluated one z-slice at a time; the builders above
+ * are splbcu_source_build(splbcu_source_*(...)).  A distributed simulation
+ * created from a source (splbcu_sim_create_dist_source) classifies only its
+ * own slab plus one halo slice per side when the reference partition
+ * (decomp.hpp:65-121) is a z-slab split, instead of every rank holding the
+ * whole SparseDomain (the reference's Simulation ctor, engine.hpp:114-140).
+ * Same argument checks and error texts as the builders. */
+typedef struct splbcu_source splbcu_source;
+int splbcu_source_pipe(int32_t radius, int32_t length, double voxel_size, splbcu_source** out);
+int splbcu_source_bifurcation(int32_t trunk_radius, int32_t branch_radius, int32_t trunk_length,
+                              int32_t branch_length, double voxel_size, splbcu_source** out);
+int splbcu_source_tree(int32_t root_radius, int32_t root_length, int32_t levels, double radius_ratio,
+                       double length_ratio, double voxel_size, splbcu_source** out);
+int splbcu_source_channel(int32_t nx, int32_t ny, int32_t nz, double voxel_size, splbcu_source** out);
+/* The whole domain (classify_sites over every slice). */
+int splbcu_source_build(const splbcu_source* s, splbcu_domain** out);
+/* Host-side view of what rank `worker` of `n_workers` builds (for tests and
+ * tools; computes every worker's slice counts in-process).  Returns 1 in
+ * *slab when the partition is a z-slab split, else 0 and nothing else.  The
+ * window is a domain (sites in global order restricted to the window);
+ * splbcu_window_info gives its global indices; *part the worker's part
+ * (site lists are window indices; other parts empty). */
+int splbcu_source_window(const splbcu_source* s, int32_t n_workers, int32_t worker, int32_t* slab,
+                         splbcu_domain** window, splbcu_partition** part);
+int splbcu_window_info(const splbcu_domain* window, uint64_t* n_global, int32_t* own_lo, int32_t* own_hi,
+                       uint64_t* global_index /* n_sites of the window, or NULL */);
+void splbcu_source_free(splbcu_source* s);
+
 /* ---- decomposition (decomp.hpp:16-188) ------------------------------------ */
 int splbcu_partition_create(const splbcu_domain* d, int32_t n_workers,
                             splbcu_partition** out);
@@ -200,6 +229,18 @@ int splbcu_sim_create_dist(const splbcu_domain* d, const splbcu_bc* bcs,
                            uint32_t n_bcs, const splbcu_params* params,
                            int32_t rank, int32_t nranks,
                            const uint8_t nccl_id[128], splbcu_sim** out);
+/* As splbcu_sim_create_dist, over a geometry source: slab-local construction
+ * (each rank classifies only its own slices + one halo slice per side) when
+ * the partition is a z-slab split, else the whole domain is built.  Results
+ * are bit-identical to splbcu_sim_create_dist on splbcu_source_build(s). */
+int splbcu_sim_create_dist_source(const splbcu_source* src, const splbcu_bc* bcs,
+                                  uint32_t n_bcs, const splbcu_params* params,
+                                  int32_t rank, int32_t nranks,
+                                  const uint8_t nccl_id[128], splbcu_sim** out);
+/* 1 when this rank holds only its window of the domain (then
+ * splbcu_sim_partition returns NULL); sites of the whole domain. */
+int32_t splbcu_sim_slab_local(const splbcu_sim* s);
+uint64_t splbcu_sim_n_sites(const splbcu_sim* s);
 /* run(nSteps) (engine.hpp:155-197). */
 int splbcu_sim_run(splbcu_sim* s, uint64_t n_steps);
 uint64_t splbcu_sim_steps_run(const splbcu_sim* s);
@@ -208,7 +249,8 @@ double splbcu_sim_step_loop_seconds(const splbcu_sim* s);
  * workers' streams) — the number the bench reports. */
 double splbcu_sim_device_loop_seconds(const splbcu_sim* s);
 /* snapshot_fields() (engine.hpp:200-205): 4*n doubles (rho,ux,uy,uz) in domain
- * order.  In dist mode only this rank's sites are written. */
+ * order (n = splbcu_sim_n_sites); in dist mode assembled across ranks
+ * (collective: every rank must call it). */
 int splbcu_sim_snapshot(splbcu_sim* s, double* out4n);
 /* Workers owned by this handle (all in-process; one in dist mode). */
 int32_t splbcu_sim_n_workers(const splbcu_sim* s);
@@ -233,7 +275,7 @@ int splbcu_sim_export_map(splbcu_sim* s, int32_t w, uint32_t* dest, uint8_t* op,
                           int32_t* seg_neighbor, uint32_t* seg_base,
                           uint32_t* seg_count);
 /* assignment() (engine.hpp:143): the partition the simulation uses (borrowed,
- * valid for the simulation's lifetime). */
+ * valid for the simulation's lifetime); NULL when slab-local. */
 const splbcu_partition* splbcu_sim_partition(const splbcu_sim* s);
 /* cache() (engine.hpp:144, 59-68): captures. */
 uint64_t splbcu_sim_n_captures(const splbcu_sim* s);
@@ -257,6 +299,10 @@ int splbcu_sim_kernel_stats(const splbcu_sim* s, double* plain_seconds,
                             uint64_t* plain_launches, uint64_t* plain_sites);
 /* Number of kernels this handle launched inside run() so far. */
 uint64_t splbcu_sim_launch_count(const splbcu_sim* s);
+/* Observation entries per series row over all workers (a site counted once
+ * per iolet it observes; 0 unless observe_iolets): each row moves 24 B per
+ * entry device -> host. */
+uint64_t splbcu_sim_observed_sites(const splbcu_sim* s);
 void splbcu_sim_destroy(splbcu_sim* s);
 
 #ifdef __cplusplus

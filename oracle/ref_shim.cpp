@@ -29,6 +29,7 @@ struct splbcu_partition {
 struct splbcu_sim {
     std::unique_ptr<Simulation> s;
     splbcu_partition view;
+    uint64_t dom_n = 0;
 };
 
 namespace {
@@ -281,6 +282,7 @@ int splbcu_sim_create(const splbcu_domain* d, const splbcu_bc* bcs, uint32_t nb,
         p.exchange_timeout_s = pr->exchange_timeout_s;
         auto s = std::make_unique<splbcu_sim>();
         s->s = std::make_unique<Simulation>(d->d, b, p);
+        s->dom_n = d->d.n_sites();
         *out = s.release();
     });
 }
@@ -399,6 +401,58 @@ int splbcu_sim_kernel_stats(const splbcu_sim*, double* a, uint64_t* b, uint64_t*
     if (c) *c = 0;
     return 0;
 }
+// ---- geometry sources: the reference builds whole domains only ----------------
+struct splbcu_source {
+    int kind;  // 0 pipe, 1 bifurcation
+    int32_t a, b, c, d;
+    double vs;
+};
+int splbcu_source_pipe(int32_t r, int32_t l, double vs, splbcu_source** out) {
+    return guard([&] {
+        if (r < 2 || l < 4) (void)build_pipe(r, l, vs);  // the reference's own argument check throws
+        *out = new splbcu_source{0, r, l, 0, 0, vs};
+    });
+}
+int splbcu_source_bifurcation(int32_t tr, int32_t br, int32_t tl, int32_t bl, double vs, splbcu_source** out) {
+    return guard([&] {
+        if (tr < 2 || br < 2 || tl < 4 || bl < 4) (void)build_bifurcation(tr, br, tl, bl, vs);
+        *out = new splbcu_source{1, tr, br, tl, bl, vs};
+    });
+}
+int splbcu_source_tree(int32_t, int32_t, int32_t, double, double, double, splbcu_source**) {
+    g_err = "reference has no tree generator";
+    return SPLBCU_ERR_CONFIG;
+}
+int splbcu_source_channel(int32_t, int32_t, int32_t, double, splbcu_source**) {
+    g_err = "reference has no channel generator";
+    return SPLBCU_ERR_CONFIG;
+}
+int splbcu_source_build(const splbcu_source* s, splbcu_domain** out) {
+    if (!s) {
+        g_err = "null source";
+        return SPLBCU_ERR_CONFIG;
+    }
+    return s->kind == 0 ? splbcu_domain_build_pipe(s->a, s->b, s->vs, out)
+                        : splbcu_domain_build_bifurcation(s->a, s->b, s->c, s->d, s->vs, out);
+}
+int splbcu_source_window(const splbcu_source*, int32_t, int32_t, int32_t*, splbcu_domain**, splbcu_partition**) {
+    g_err = "reference has no slab-local construction";
+    return SPLBCU_ERR_CONFIG;
+}
+int splbcu_window_info(const splbcu_domain*, uint64_t*, int32_t*, int32_t*, uint64_t*) {
+    g_err = "domain is not a source window";
+    return SPLBCU_ERR_CONFIG;
+}
+void splbcu_source_free(splbcu_source* s) { delete s; }
+int splbcu_sim_create_dist_source(const splbcu_source*, const splbcu_bc*, uint32_t, const splbcu_params*, int32_t,
+                                  int32_t, const uint8_t*, splbcu_sim**) {
+    g_err = "reference has no NCCL path";
+    return SPLBCU_ERR_CONFIG;
+}
+int32_t splbcu_sim_slab_local(const splbcu_sim*) { return 0; }
+uint64_t splbcu_sim_observed_sites(const splbcu_sim*) { return 0; }
+uint64_t splbcu_sim_n_sites(const splbcu_sim* s) { return s->dom_n; }
+
 uint64_t splbcu_sim_launch_count(const splbcu_sim*) { return 0; }
 void splbcu_sim_destroy(splbcu_sim* s) { delete s; }
 

@@ -1252,6 +1252,66 @@ int splbcu_sim_kernel_stats(const splbcu_sim* S, double* a, uint64_t* b, uint64_
     if (c) *c = 0;
     return 0;
 }
+/* ---- geometry sources: the oracle builds whole domains only ---------------- */
+struct splbcu_source {
+    int kind; /* 0 pipe, 1 bifurcation */
+    int32_t a, b, c, d;
+    double vs;
+};
+static int new_source(int kind, int32_t a, int32_t b, int32_t c, int32_t d, double vs, splbcu_source** out) {
+    splbcu_source* s = (splbcu_source*)calloc(1, sizeof *s);
+    if (!s) return set_err(SPLBCU_ERR_RUNTIME, "out of memory");
+    s->kind = kind, s->a = a, s->b = b, s->c = c, s->d = d, s->vs = vs;
+    *out = s;
+    return SPLBCU_OK;
+}
+int splbcu_source_pipe(int32_t r, int32_t l, double vs, splbcu_source** o) {
+    if (r < 2 || l < 4) return set_err(SPLBCU_ERR_GEOMETRY, "build_pipe: need radius >= 2 and length >= 4");
+    return new_source(0, r, l, 0, 0, vs, o);
+}
+int splbcu_source_bifurcation(int32_t tr, int32_t br, int32_t tl, int32_t bl, double vs, splbcu_source** o) {
+    if (tr < 2 || br < 2 || tl < 4 || bl < 4)
+        return set_err(SPLBCU_ERR_GEOMETRY, "build_bifurcation: need radii >= 2 and lengths >= 4");
+    return new_source(1, tr, br, tl, bl, vs, o);
+}
+int splbcu_source_tree(int32_t a, int32_t b, int32_t c, double d_, double e, double f, splbcu_source** o) {
+    (void)a, (void)b, (void)c, (void)d_, (void)e, (void)f, (void)o;
+    return set_err(SPLBCU_ERR_CONFIG, "oracle: the tree generator is product-only; pass its arrays");
+}
+int splbcu_source_channel(int32_t a, int32_t b, int32_t c, double d_, splbcu_source** o) {
+    (void)a, (void)b, (void)c, (void)d_, (void)o;
+    return set_err(SPLBCU_ERR_CONFIG, "oracle: the channel generator is product-only; pass its arrays");
+}
+int splbcu_source_build(const splbcu_source* s, splbcu_domain** out) {
+    if (!s) return set_err(SPLBCU_ERR_CONFIG, "null source");
+    return s->kind == 0 ? splbcu_domain_build_pipe(s->a, s->b, s->vs, out)
+                        : splbcu_domain_build_bifurcation(s->a, s->b, s->c, s->d, s->vs, out);
+}
+int splbcu_source_window(const splbcu_source* s, int32_t n, int32_t w, int32_t* slab, splbcu_domain** win,
+                         splbcu_partition** part) {
+    (void)s, (void)n, (void)w, (void)slab, (void)win, (void)part;
+    return set_err(SPLBCU_ERR_CONFIG, "oracle: slab-local windows are product-only");
+}
+int splbcu_window_info(const splbcu_domain* d, uint64_t* a, int32_t* b, int32_t* c, uint64_t* e) {
+    (void)d, (void)a, (void)b, (void)c, (void)e;
+    return set_err(SPLBCU_ERR_CONFIG, "domain is not a source window");
+}
+void splbcu_source_free(splbcu_source* s) { free(s); }
+int splbcu_sim_create_dist_source(const splbcu_source* a, const splbcu_bc* b, uint32_t c, const splbcu_params* d,
+                                  int32_t e, int32_t f, const uint8_t* g, splbcu_sim** h) {
+    (void)a, (void)b, (void)c, (void)d, (void)e, (void)f, (void)g, (void)h;
+    return set_err(SPLBCU_ERR_CONFIG, "oracle: no NCCL path");
+}
+uint64_t splbcu_sim_observed_sites(const splbcu_sim* S) {
+    (void)S;
+    return 0;
+}
+int32_t splbcu_sim_slab_local(const splbcu_sim* S) {
+    (void)S;
+    return 0;
+}
+uint64_t splbcu_sim_n_sites(const splbcu_sim* S) { return S->dom->n; }
+
 uint64_t splbcu_sim_launch_count(const splbcu_sim* S) {
     (void)S;
     return 0;

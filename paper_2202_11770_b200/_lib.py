@@ -67,6 +67,14 @@ SIGNATURES = [
     ("splbcu_domain_voxel_size", C.c_double, [_P]),
     ("splbcu_domain_export", c_int, [_P, c_i32p, c_u8p, c_u8p, c_u16p, C.POINTER(Iolet), c_u64p]),
     ("splbcu_domain_free", None, [_P]),
+    ("splbcu_source_pipe", c_int, [c_int, c_int, C.c_double, _PP]),
+    ("splbcu_source_bifurcation", c_int, [c_int, c_int, c_int, c_int, C.c_double, _PP]),
+    ("splbcu_source_tree", c_int, [c_int, c_int, c_int, C.c_double, C.c_double, C.c_double, _PP]),
+    ("splbcu_source_channel", c_int, [c_int, c_int, c_int, C.c_double, _PP]),
+    ("splbcu_source_build", c_int, [_P, _PP]),
+    ("splbcu_source_window", c_int, [_P, c_int, c_int, c_i32p, _PP, _PP]),
+    ("splbcu_window_info", c_int, [_P, c_u64p, c_i32p, c_i32p, c_u64p]),
+    ("splbcu_source_free", None, [_P]),
     ("splbcu_partition_create", c_int, [_P, c_int, _PP]),
     ("splbcu_partition_global", c_int, [_P, c_i32p, c_u32p]),
     ("splbcu_partition_part_shape", c_int, [_P, c_int, c_u32p, c_u32p, c_u32p]),
@@ -77,6 +85,10 @@ SIGNATURES = [
     ("splbcu_nccl_unique_id", c_int, [c_u8p]),
     ("splbcu_sim_create_dist", c_int, [_P, C.POINTER(BC), C.c_uint32, C.POINTER(Params), c_int, c_int,
                                        c_u8p, _PP]),
+    ("splbcu_sim_create_dist_source", c_int, [_P, C.POINTER(BC), C.c_uint32, C.POINTER(Params), c_int, c_int,
+                                              c_u8p, _PP]),
+    ("splbcu_sim_slab_local", c_int, [_P]),
+    ("splbcu_sim_n_sites", C.c_uint64, [_P]),
     ("splbcu_sim_run", c_int, [_P, C.c_uint64]),
     ("splbcu_sim_steps_run", C.c_uint64, [_P]),
     ("splbcu_sim_step_loop_seconds", C.c_double, [_P]),
@@ -100,6 +112,7 @@ SIGNATURES = [
     ("splbcu_sim_set_kernel_timing", c_int, [_P, c_int]),
     ("splbcu_sim_kernel_stats", c_int, [_P, c_dp, c_u64p, c_u64p]),
     ("splbcu_sim_launch_count", C.c_uint64, [_P]),
+    ("splbcu_sim_observed_sites", C.c_uint64, [_P]),
     ("splbcu_sim_destroy", None, [_P]),
 ]
 

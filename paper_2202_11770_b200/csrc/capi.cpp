@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <string>
 
@@ -15,6 +16,14 @@ using namespace splbcu;
 
 struct splbcu_domain {
     Domain d;
+    // set on windows from splbcu_source_window
+    bool window = false;
+    uint64_t n_global = 0;
+    int32_t own_lo = 0, own_hi = -1;
+    std::vector<uint64_t> global_index;
+};
+struct splbcu_source {
+    Source s;
 };
 struct splbcu_partition {
     Partition p;
@@ -274,6 +283,87 @@ int splbcu_domain_export(const splbcu_domain* dd, int32_t* coords, uint8_t* type
 
 void splbcu_domain_free(splbcu_domain* d) { delete d; }
 
+// ---- sources -------------------------------------------------------------------
+static int make_source(splbcu_source** out, const std::function<Source()>& f) {
+    return guard([&] {
+        auto p = std::make_unique<splbcu_source>();
+        p->s = f();
+        *out = p.release();
+    });
+}
+int splbcu_source_pipe(int32_t radius, int32_t length, double voxel_size, splbcu_source** out) {
+    return make_source(out, [&] { return source_pipe(radius, length, voxel_size); });
+}
+int splbcu_source_bifurcation(int32_t tr, int32_t br, int32_t tl, int32_t bl, double voxel_size,
+                              splbcu_source** out) {
+    return make_source(out, [&] { return source_bifurcation(tr, br, tl, bl, voxel_size); });
+}
+int splbcu_source_tree(int32_t root_radius, int32_t root_length, int32_t levels, double radius_ratio,
+                       double length_ratio, double voxel_size, splbcu_source** out) {
+    return make_source(out, [&] {
+        return source_tree(root_radius, root_length, levels, radius_ratio, length_ratio, voxel_size);
+    });
+}
+int splbcu_source_channel(int32_t nx, int32_t ny, int32_t nz, double voxel_size, splbcu_source** out) {
+    return make_source(out, [&] { return source_channel(nx, ny, nz, voxel_size); });
+}
+int splbcu_source_build(const splbcu_source* s, splbcu_domain** out) {
+    return guard([&] {
+        check_ptr(s, "source");
+        auto d = std::make_unique<splbcu_domain>();
+        d->d = build_from_source(s->s);
+        *out = d.release();
+    });
+}
+int splbcu_source_window(const splbcu_source* s, int32_t n_workers, int32_t worker, int32_t* slab,
+                         splbcu_domain** window, splbcu_partition** part) {
+    return guard([&] {
+        check_ptr(s, "source");
+        if (worker < 0 || worker >= n_workers) config_error("source window: worker out of range");
+        const SlabPlan plan = plan_slabs(plan_source(s->s), s->s.z0, n_workers);
+        if (slab) *slab = plan.ok ? 1 : 0;
+        if (!plan.ok) return;
+        // every worker's own-slice counts, as the ranks' all-gather provides them
+        std::vector<uint64_t> counts;
+        Window mine;
+        for (int v = 0; v < n_workers; ++v) {
+            std::vector<uint64_t> own;
+            Window w = classify_window(s->s, plan, v, &own, nullptr);
+            counts.insert(counts.end(), own.begin(), own.end());
+            if (v == worker) mine = std::move(w);
+        }
+        finish_window(mine, plan, counts);
+        if (part) {
+            auto p = std::make_unique<splbcu_partition>();
+            p->p = partition_window(mine, plan, n_workers);
+            *part = p.release();
+        }
+        if (window) {
+            auto d = std::make_unique<splbcu_domain>();
+            d->window = true;
+            d->n_global = mine.n_global;
+            d->own_lo = mine.own_lo;
+            d->own_hi = mine.own_hi;
+            d->global_index.resize(mine.dom.n);
+            for (uint64_t q = 0; q < mine.dom.n; ++q) d->global_index[q] = mine.global_of(q);
+            d->d = std::move(mine.dom);
+            *window = d.release();
+        }
+    });
+}
+int splbcu_window_info(const splbcu_domain* w, uint64_t* n_global, int32_t* own_lo, int32_t* own_hi,
+                       uint64_t* global_index) {
+    return guard([&] {
+        check_ptr(w, "domain");
+        if (!w->window) config_error("domain is not a source window");
+        if (n_global) *n_global = w->n_global;
+        if (own_lo) *own_lo = w->own_lo;
+        if (own_hi) *own_hi = w->own_hi;
+        if (global_index) std::memcpy(global_index, w->global_index.data(), w->global_index.size() * 8);
+    });
+}
+void splbcu_source_free(splbcu_source* s) { delete s; }
+
 // ---- partition --------------------------------------------------------------
 int splbcu_partition_create(const splbcu_domain* d, int32_t n_workers, splbcu_partition** out) {
     return guard([&] {
@@ -353,6 +443,22 @@ int splbcu_sim_create_dist(const splbcu_domain* d, const splbcu_bc* bcs, uint32_
     });
 }
 
+int splbcu_sim_create_dist_source(const splbcu_source* src, const splbcu_bc* bcs, uint32_t n_bcs,
+                                  const splbcu_params* params, int32_t rank, int32_t nranks, const uint8_t id[128],
+                                  splbcu_sim** out) {
+    return guard([&] {
+        check_ptr(src, "source");
+        check_ptr(params, "params");
+        check_ptr(id, "nccl id");
+        auto s = std::make_unique<splbcu_sim>();
+        s->s = std::make_unique<Simulation>(src->s, to_bcs(bcs, n_bcs), to_params(params), rank, nranks, id);
+        *out = s.release();
+    });
+}
+uint64_t splbcu_sim_observed_sites(const splbcu_sim* s) { return s ? s->s->observed_sites() : 0; }
+int32_t splbcu_sim_slab_local(const splbcu_sim* s) { return s && s->s->slab_local() ? 1 : 0; }
+uint64_t splbcu_sim_n_sites(const splbcu_sim* s) { return s ? s->s->n_sites() : 0; }
+
 int splbcu_sim_run(splbcu_sim* s, uint64_t n) {
     return guard([&] {
         check_ptr(s, "simulation");
@@ -409,7 +515,7 @@ int splbcu_sim_export_map(splbcu_sim* s, int32_t w, uint32_t* dest, uint8_t* op,
 }
 
 const splbcu_partition* splbcu_sim_partition(const splbcu_sim* s) {
-    if (!s) return nullptr;
+    if (!s || s->s->slab_local()) return nullptr;
     auto* ss = const_cast<splbcu_sim*>(s);
     ss->part_view.p = s->s->partition();
     ss->part_view.borrowed = true;

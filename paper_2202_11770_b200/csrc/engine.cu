@@ -15,6 +15,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <atomic>
 #include <thread>
 
 #include <cub/device/device_radix_sort.cuh>
@@ -378,9 +379,100 @@ class Engine {
     bool p2p_mode = false;
     bool aa_mode = false;  // single-buffer AA storage (params.storage == 1)
     std::vector<IoletDev> io_host;
+    std::unique_ptr<Window> win;  // slab-local build: dom holds this rank's window only
+    uint64_t n_global = 0;        // sites of the whole domain
 
     Engine(const Domain& d, std::vector<BCEntry> b, Params p, int rank_, int nranks_, const void* nccl_id)
         : dom(d), bcs(std::move(b)), prm(std::move(p)) {
+        begin(rank_, nranks_, nccl_id);
+        validate_setup();
+        part = splbcu::partition(dom, prm.workers);
+        n_global = dom.n;
+        finish_setup();
+    }
+
+    // Distributed engine over a geometry source: when the
+    // reference partition is a z-slab split, each rank classifies only its
+    // own slices plus one halo slice on each side; per-slice type counts are
+    // all-gathered to place its sites in the global order.  Otherwise (and
+    // in-process) the whole domain is built, exactly as the builders do.
+    Engine(const Source& src, std::vector<BCEntry> b, Params p, int rank_, int nranks_, const void* nccl_id)
+        : bcs(std::move(b)), prm(std::move(p)) {
+        begin(rank_, nranks_, nccl_id);
+        SlabPlan plan;
+        if (dist) {
+            const SourcePlan sp = plan_source(src);
+            phase("slab: plan");
+            plan = plan_slabs(sp, src.z0, prm.workers);
+        }
+        if (!plan.ok) {
+            dom = build_from_source(src);
+            validate_setup();
+            part = splbcu::partition(dom, prm.workers);
+            n_global = dom.n;
+        } else {
+            std::vector<uint64_t> own, io_links;
+            win = std::make_unique<Window>(classify_window(src, plan, rank, &own, &io_links));
+            phase("slab: classify window");
+            // every slice's per-type counts, in worker (= slice) order
+            const std::vector<std::vector<uint64_t>> all = allgather_setup(own);
+            std::vector<uint64_t> counts;
+            for (auto& v : all) counts.insert(counts.end(), v.begin(), v.end());
+            finish_window(*win, plan, counts);
+            // classify_sites' global check (geometry.hpp:199-206): every iolet has links somewhere
+            const std::vector<std::vector<uint64_t>> links = allgather_setup(io_links);
+            for (size_t k = 0; k < src.iolets.size(); ++k) {
+                uint64_t c = 0;
+                for (auto& v : links) c += v[k];
+                if (c == 0)
+                    geometry_error("classify_sites: iolet " + std::to_string(k) + " intersects no boundary links");
+            }
+            dom = std::move(win->dom);  // the engine's domain is the window
+            n_global = win->n_global;
+            validate_params();
+            part = partition_window(*win, plan, prm.workers);
+            phase("slab: partition");
+        }
+        finish_setup();
+    }
+
+    // Global site index of a site of `dom` (identity unless slab-local).
+    uint64_t global_of_site(uint64_t s) const {
+        if (!win) return s;
+        const int t = dom.types[s];
+        return win->g_first[t] + (s - dom.type_ranges[t][0]);
+    }
+
+    // Host all-gather of one vector per rank (lengths may differ), usable
+    // before the workers exist.
+    std::vector<std::vector<uint64_t>> allgather_setup(const std::vector<uint64_t>& mine) {
+        CK(cudaSetDevice(prm.devices[0]));
+        cudaStream_t s = nullptr;
+        CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        DevMem a, b;
+        auto gather = [&](const std::vector<uint64_t>& v, size_t per) {
+            uint64_t* da = a.reserve<uint64_t>(per);
+            uint64_t* db = b.reserve<uint64_t>(per * size_t(nranks));
+            CK(cudaMemsetAsync(da, 0, per * 8, s));
+            if (!v.empty()) CK(cudaMemcpyAsync(da, v.data(), v.size() * 8, cudaMemcpyHostToDevice, s));
+            NK(nccl().AllGather(da, db, per, ncclUint64, comm, s));
+            std::vector<uint64_t> h(per * size_t(nranks));
+            CK(cudaMemcpyAsync(h.data(), db, h.size() * 8, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            return h;
+        };
+        const std::vector<uint64_t> len = gather({uint64_t(mine.size())}, 1);
+        size_t per = 1;
+        for (uint64_t l : len) per = std::max<size_t>(per, size_t(l));
+        const std::vector<uint64_t> all = gather(mine, per);
+        CK(cudaStreamDestroy(s));
+        std::vector<std::vector<uint64_t>> out{size_t(nranks)};
+        for (int r = 0; r < nranks; ++r)
+            out[size_t(r)].assign(all.begin() + int64_t(per) * r, all.begin() + int64_t(per) * r + int64_t(len[size_t(r)]));
+        return out;
+    }
+
+    void begin(int rank_, int nranks_, const void* nccl_id) {
         dist = nccl_id != nullptr;
         rank = rank_;
         nranks = nranks_;
@@ -399,9 +491,10 @@ class Engine {
             std::memcpy(&id, nccl_id, sizeof(id));
             NK(nccl_checked().CommInitRank(&comm, nranks, id, rank));
         }
-        validate_setup();
+    }
+
+    void finish_setup() {
         omega = 1.0 / prm.tau;  // RelaxationParams (lattice.hpp:83-84), dt = 1
-        part = splbcu::partition(dom, prm.workers);
         for (auto& g : dom.iolets) {
             IoletDev x{};
             for (int a = 0; a < 3; ++a) x.center[a] = g.center[a], x.normal[a] = g.normal[a];
@@ -644,6 +737,9 @@ class Engine {
     // validate_setup (engine.hpp:223-241)
     void validate_setup() {
         validate_domain(dom);
+        validate_params();
+    }
+    void validate_params() {
         if (prm.workers < 1) config_error("engine: workers must be >= 1");
         if (bcs.size() != dom.iolets.size())
             config_error("engine: boundary conditions configured for " + std::to_string(bcs.size()) +
@@ -725,7 +821,7 @@ class Engine {
         wk.global_of_int.resize(wk.n);
         for (uint32_t j = 0; j < wk.n; ++j) {
             wk.int_of_ref[wk.ref_of_int[j]] = j;
-            wk.global_of_int[j] = wp.sites[wk.ref_of_int[j]];
+            wk.global_of_int[j] = uint32_t(global_of_site(wp.sites[wk.ref_of_int[j]]));
         }
 
         // Lookup subset: own sites + halo (slab: the two adjacent planes;
@@ -750,7 +846,7 @@ class Engine {
                 if (part.slab && (c < pmin - 1 || c > pmax + 1)) continue;
                 lkeys.push_back(ix.keys[q]);
                 lowner.push_back(part.owner[g]);
-                lglobal.push_back(g);
+                lglobal.push_back(uint32_t(global_of_site(g)));
                 llocal.push_back(part.owner[g] == w ? wk.int_of_ref[part.local_index[g]] : 0u);
             }
         }
@@ -762,7 +858,7 @@ class Engine {
         std::vector<int32_t> coords(3 * uint64_t(wk.n));
         std::vector<uint8_t> kind(18 * uint64_t(wk.n));
         for (uint32_t j = 0; j < wk.n; ++j) {
-            const uint64_t g = wk.global_of_int[j];
+            const uint64_t g = wp.sites[wk.ref_of_int[j]];  // index into dom
             std::memcpy(&coords[3 * uint64_t(j)], &dom.coords[3 * g], 12);
             std::memcpy(&kind[18 * uint64_t(j)], &dom.link_kind[18 * g], 18);
         }
@@ -934,6 +1030,7 @@ class Engine {
         std::vector<std::vector<uint32_t>> per_w_count(size_t(prm.workers), std::vector<uint32_t>(n_io, 0));
         size_t q = 0;
         std::vector<uint8_t> member(n_io);
+        std::vector<std::vector<uint64_t>> own_obs(n_io);  // slab-local: own sites' global indices
         while (q < dom.iolet_link_pos.size()) {
             const uint64_t g = dom.iolet_link_pos[q] / 18;
             std::fill(member.begin(), member.end(), 0);
@@ -944,11 +1041,38 @@ class Engine {
             for (size_t k = 0; k < n_io; ++k) {
                 if (!member[k]) continue;
                 const int w = part.owner[g];
+                if (win && w != rank) continue;  // halo site: its owner observes it
+                if (win) own_obs[k].push_back(global_of_site(g));
                 obs_order[k].push_back({w, per_w_count[size_t(w)][k]++});
                 if (W[size_t(w)]) {
                     WorkerDev& wk = *W[size_t(w)];
                     wk.obs_sites[k].push_back(wk.int_of_ref[part.local_index[g]]);
                 }
+            }
+        }
+        if (win) {
+            // every rank's observed sites (iolet-major, global indices): the
+            // series order is ascending global index across ranks
+            std::vector<uint64_t> mine;
+            for (size_t k = 0; k < n_io; ++k) {
+                mine.push_back(own_obs[k].size());
+                mine.insert(mine.end(), own_obs[k].begin(), own_obs[k].end());
+            }
+            const std::vector<std::vector<uint64_t>> all = allgather_setup(mine);
+            for (size_t k = 0; k < n_io; ++k) obs_order[k].clear();
+            std::vector<std::vector<std::tuple<uint64_t, int, uint32_t>>> merged(n_io);
+            for (int w = 0; w < prm.workers; ++w) {
+                const std::vector<uint64_t>& v = all[size_t(w)];
+                size_t p = 0;
+                for (size_t k = 0; k < n_io; ++k) {
+                    const uint64_t c = v.at(p++);
+                    per_w_count[size_t(w)][k] = uint32_t(c);
+                    for (uint64_t j = 0; j < c; ++j) merged[k].emplace_back(v.at(p++), w, uint32_t(j));
+                }
+            }
+            for (size_t k = 0; k < n_io; ++k) {
+                std::sort(merged[k].begin(), merged[k].end());
+                for (auto& [g, w, pos] : merged[k]) obs_order[k].push_back({w, pos});
             }
         }
         obs_off_all.assign(size_t(prm.workers), std::vector<uint32_t>(n_io + 1, 0));
@@ -1292,7 +1416,7 @@ class Engine {
                 if (!caps.empty() && caps.back().step == st) continue;
                 Capture c;
                 c.step = st;
-                c.fields.assign(4 * dom.n, 0.0);
+                c.fields.assign(4 * n_global, 0.0);
                 caps.push_back(std::move(c));
             }
         }
@@ -1715,21 +1839,39 @@ class Engine {
         series.max_speed.resize(n_io);
         series.pressure.resize(n_io);
         series.flow.resize(n_io);
-        for (size_t k = 0; k < n_io; ++k)
-            for (uint64_t row = first_row; row < rows; ++row) {
-                double vmax = 0.0, psum = 0.0, qsum = 0.0;
-                for (const auto& [w, pos] : obs_order[k]) {
-                    const std::vector<uint32_t>& off = obs_off_all[size_t(w)];
-                    const double* v = hb[size_t(w)] + 3 * ((row - row_base) * off[n_io] + off[k] + pos);
-                    vmax = std::max(vmax, v[0]);
-                    psum += v[1];
-                    qsum += v[2];
-                }
-                const double n_obs = double(obs_order[k].size());
-                series.max_speed[k].push_back(vmax);
-                series.pressure[k].push_back(psum / n_obs);
-                series.flow[k].push_back(qsum);
-            }
+        for (size_t k = 0; k < n_io; ++k) {
+            series.max_speed[k].resize(rows);
+            series.pressure[k].resize(rows);
+            series.flow[k].resize(rows);
+        }
+        // each iolet's rows are an independent ordered reduction: iolets are
+        // handed out one at a time to a few threads when there is enough work
+        uint64_t work = 0;
+        for (size_t k = 0; k < n_io; ++k) work += obs_order[k].size();
+        work *= rows - first_row;
+        std::atomic<size_t> next{0};
+        auto reduce = [&] {
+            for (size_t k; (k = next.fetch_add(1)) < n_io;)
+                    for (uint64_t row = first_row; row < rows; ++row) {
+                        double vmax = 0.0, psum = 0.0, qsum = 0.0;
+                        for (const auto& [w, pos] : obs_order[k]) {
+                            const std::vector<uint32_t>& off = obs_off_all[size_t(w)];
+                            const double* v = hb[size_t(w)] + 3 * ((row - row_base) * off[n_io] + off[k] + pos);
+                            vmax = std::max(vmax, v[0]);
+                            psum += v[1];
+                            qsum += v[2];
+                        }
+                        const double n_obs = double(obs_order[k].size());
+                        series.max_speed[k][row] = vmax;
+                        series.pressure[k][row] = psum / n_obs;
+                        series.flow[k][row] = qsum;
+                    }
+        };
+        const int nt = work > (1u << 16) ? int(std::min<size_t>({size_t(hw_threads()), size_t(8), n_io})) : 1;
+        std::vector<std::thread> th;
+        for (int t = 1; t < nt; ++t) th.emplace_back(reduce);
+        reduce();
+        for (auto& t : th) t.join();
         series.rows = rows;
     }
 
@@ -1741,7 +1883,7 @@ class Engine {
     }
 
     void snapshot(double* out) {
-        if (dist) std::fill(out, out + 4 * dom.n, 0.0);
+        if (dist) std::fill(out, out + 4 * n_global, 0.0);
         for (auto& wp : W) {
             if (!wp) continue;
             WorkerDev& wk = *wp;
@@ -1754,7 +1896,7 @@ class Engine {
             for (uint32_t j = 0; j < wk.n; ++j)
                 std::memcpy(&out[4 * uint64_t(wk.global_of_int[j])], &h[4 * uint64_t(j)], 32);
         }
-        if (dist) allreduce_host_sum(out, 4 * dom.n);  // every rank returns the whole domain
+        if (dist) allreduce_host_sum(out, 4 * n_global);  // every rank returns the whole domain
     }
 
     // AA storage: f in the reference meaning, as 19 planes of P (internal order).
@@ -1914,7 +2056,17 @@ Simulation::Simulation(const Domain& d, std::vector<BCEntry> bcs, Params p)
 Simulation::Simulation(const Domain& d, std::vector<BCEntry> bcs, Params p, int rank, int nranks,
                        const void* nccl_id)
     : e_(std::make_unique<Engine>(d, std::move(bcs), std::move(p), rank, nranks, nccl_id)) {}
+Simulation::Simulation(const Source& src, std::vector<BCEntry> bcs, Params p, int rank, int nranks,
+                       const void* nccl_id)
+    : e_(std::make_unique<Engine>(src, std::move(bcs), std::move(p), rank, nranks, nccl_id)) {}
 Simulation::~Simulation() = default;
+bool Simulation::slab_local() const { return e_->win != nullptr; }
+uint64_t Simulation::n_sites() const { return e_->n_global; }
+uint64_t Simulation::observed_sites() const {
+    uint64_t n = 0;
+    for (auto& o : e_->obs_off_all) n += o.empty() ? 0 : o.back();
+    return n;
+}
 void Simulation::run(uint64_t n) { e_->run(n); }
 uint64_t Simulation::steps_run() const { return e_->steps_run; }
 double Simulation::step_loop_seconds() const { return e_->loop_s; }

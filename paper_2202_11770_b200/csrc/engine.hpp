@@ -57,7 +57,14 @@ class Simulation {
     // One process per GPU with NCCL (rank owns worker `rank`).
     Simulation(const Domain& d, std::vector<BCEntry> bcs, Params p, int rank, int nranks,
                const void* nccl_id);
+    // Distributed engine over a geometry source: slab-local construction
+    // when the partition is a z-slab split (nccl_id null: in-process, whole domain).
+    Simulation(const Source& src, std::vector<BCEntry> bcs, Params p, int rank, int nranks,
+               const void* nccl_id);
     ~Simulation();
+    bool slab_local() const;  // this rank holds only its window of the domain
+    uint64_t n_sites() const; // sites of the whole domain
+    uint64_t observed_sites() const;
 
     void run(uint64_t n);
     uint64_t steps_run() const;

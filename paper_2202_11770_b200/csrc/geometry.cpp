@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
+#include <memory>
 #include <mutex>
 #include <thread>
 
@@ -260,10 +261,19 @@ static uint8_t type_of(bool wall, bool inlet, bool outlet) {
 // (duplicates rejected by the caller).  input_index maps a sorted position
 // back to the caller's order so error reports name the same site as the
 // reference (the first offending voxel in input order).
+// Slab mode (classify_slab): only sites with z in [za, zb] are kept and
+// checked; an iolet without links is reported through io_links instead.
+struct SlabKeep {
+    int32_t za, zb;
+    std::vector<uint64_t>* io_links;
+};
+
 static Domain classify_sorted(std::vector<int32_t>&& coords, const std::vector<uint64_t>& keys,
                               const std::vector<uint32_t>* input_index,
-                              std::vector<IoletGeo>&& iolets, double voxel_size) {
-    const uint64_t n = keys.size();
+                              std::vector<IoletGeo>&& iolets, double voxel_size,
+                              const SlabKeep* slab = nullptr) {
+    uint64_t n = keys.size();
+    auto kept = [&](uint64_t s) { return !slab || (coords[3 * s + 2] >= slab->za && coords[3 * s + 2] <= slab->zb); };
     SiteIndex ix;
     ix.keys = keys;
     ix.build_rows();
@@ -303,7 +313,7 @@ static Domain classify_sorted(std::vector<int32_t>&& coords, const std::vector<u
                         if (crosses_iolet(a, bb, iolets[io])) {
                             k = iolets[io].kind == 0 ? 2 : 3;
                             io_links[t].push_back({18 * s + uint64_t(i - 1), uint16_t(io)});
-                            ++io_count[t][io];
+                            if (kept(s)) ++io_count[t][io];
                             break;
                         }
                 }
@@ -312,7 +322,7 @@ static Domain classify_sorted(std::vector<int32_t>&& coords, const std::vector<u
                 inlet |= k == 2;
                 outlet |= k == 3;
             }
-            if (inlet && outlet) {
+            if (inlet && outlet && kept(s)) {
                 const uint64_t in_idx = input_index ? (*input_index)[s] : s;
                 if (in_idx < bad_in[t]) bad_in[t] = in_idx, bad_pos[t] = s;
             }
@@ -330,9 +340,12 @@ static Domain classify_sorted(std::vector<int32_t>&& coords, const std::vector<u
     for (size_t io = 0; io < iolets.size(); ++io) {
         uint64_t c = 0;
         for (int t = 0; t < nt; ++t) c += io_count[t][io];
-        if (c == 0)
+        if (slab) {
+            if (slab->io_links) slab->io_links->push_back(c);
+        } else if (c == 0) {
             geometry_error("classify_sites: iolet " + std::to_string(io) +
                            " intersects no boundary links");
+        }
     }
 
     phase("classify: links");
@@ -340,8 +353,29 @@ static Domain classify_sorted(std::vector<int32_t>&& coords, const std::vector<u
     // (geometry.hpp:189-195).
     Domain d;
     d.voxel_size = voxel_size;
-    d.n = n;
     d.iolets = std::move(iolets);
+    if (slab) {
+        // drop the classification-only slices: compact the kept sites in place
+        uint64_t m = 0;
+        std::vector<uint64_t> newpos(n, UINT64_MAX);
+        for (uint64_t s = 0; s < n; ++s)
+            if (kept(s)) newpos[s] = m++;
+        for (uint64_t s = 0; s < n; ++s) {
+            const uint64_t q = newpos[s];
+            if (q == UINT64_MAX || q == s) continue;
+            std::memcpy(&coords[3 * q], &coords[3 * s], 12);
+            std::memcpy(&kind[18 * q], &kind[18 * s], 18);
+            type[q] = type[s];
+        }
+        for (auto& v : io_links) {
+            size_t o = 0;
+            for (auto& p : v)
+                if (newpos[p.first / 18] != UINT64_MAX) v[o++] = {18 * newpos[p.first / 18] + p.first % 18, p.second};
+            v.resize(o);
+        }
+        n = m;
+    }
+    d.n = n;
     uint64_t cnt[6] = {};
     for (uint64_t s = 0; s < n; ++s) ++cnt[type[s]];
     uint64_t pos = 0;
@@ -512,47 +546,57 @@ void validate_domain(const Domain& d) {
 constexpr double kAxisOffsetX = 0.375;  // geometry.hpp:279
 constexpr double kAxisOffsetY = 0.5;    // geometry.hpp:280
 
-// build_pipe (geometry.hpp:285-308).  Slices are generated in parallel and
-// concatenated in z order, so the voxel list is already zyx-sorted.
-Domain build_pipe(int radius, int length, double voxel_size) {
+// ---- sources: generators evaluated slice by slice ------------------------------
+// Every builder is build_from_source(source_*): the slice functions are the
+// only definition of each geometry, so a slab classified by a distributed
+// engine (classify_slab) sees exactly the voxels of the whole-domain build.
+
+// build_pipe (geometry.hpp:285-308): every slice is the same disc.
+Source source_pipe(int radius, int length, double voxel_size) {
     if (radius < 2 || length < 4) geometry_error("build_pipe: need radius >= 2 and length >= 4");
     const double r2 = double(radius) * radius;
-    std::vector<int32_t> slice;
+    auto disc = std::make_shared<std::vector<int32_t>>();
     for (int y = -radius - 2; y <= radius + 2; ++y)
         for (int x = -radius - 2; x <= radius + 2; ++x) {
             const double dx = x - kAxisOffsetX, dy = y - kAxisOffsetY;
             if (dx * dx + dy * dy < r2) {
-                slice.push_back(x);
-                slice.push_back(y);
+                disc->push_back(x);
+                disc->push_back(y);
             }
         }
-    const uint64_t per = slice.size() / 2;
-    std::vector<int32_t> vox(3 * per * uint64_t(length));
-    parallel_for(uint64_t(length), [&](uint64_t b, uint64_t e, int) {
-        for (uint64_t z = b; z < e; ++z)
-            for (uint64_t k = 0; k < per; ++k) {
-                int32_t* v = &vox[3 * (z * per + k)];
-                v[0] = slice[2 * k];
-                v[1] = slice[2 * k + 1];
-                v[2] = int32_t(z);
-            }
-    }, 1);
-    std::vector<IoletGeo> io = {
+    Source s;
+    s.voxel_size = voxel_size;
+    s.z0 = 0;
+    s.z1 = length - 1;
+    s.iolets = {
         {0, {kAxisOffsetX, kAxisOffsetY, -0.5}, {0.0, 0.0, 1.0}, double(radius)},
         {1, {kAxisOffsetX, kAxisOffsetY, double(length - 1) + 0.5}, {0.0, 0.0, -1.0}, double(radius)},
     };
-    return classify_sites(vox, std::move(io), voxel_size);
+    s.slice = [disc](int32_t, std::vector<int32_t>& xy) { xy = *disc; };
+    return s;
 }
 
-// build_bifurcation (geometry.hpp:313-363)
-Domain build_bifurcation(int tr, int br, int tl, int bl, double voxel_size) {
+// build_bifurcation (geometry.hpp:313-363): a trunk disc, then two discs
+// whose centres diverge linearly in x.
+Source source_bifurcation(int tr, int br, int tl, int bl, double voxel_size) {
     if (tr < 2 || br < 2 || tl < 4 || bl < 4)
         geometry_error("build_bifurcation: need radii >= 2 and lengths >= 4");
     constexpr double kSlope = 0.5;
-    std::vector<int32_t> vox;
     const int xmax = int(std::ceil(kSlope * bl)) + tr + br + 2;
     const int rmax = std::max(tr, br) + 2;
-    for (int z = 0; z < tl + bl; ++z)
+    Source s;
+    s.voxel_size = voxel_size;
+    s.z0 = 0;
+    s.z1 = tl + bl - 1;
+    const double zend = double(tl + bl - 1) + 0.5;
+    const double xend = kSlope * bl;
+    s.iolets = {
+        {0, {kAxisOffsetX, kAxisOffsetY, -0.5}, {0.0, 0.0, 1.0}, double(tr)},
+        {1, {kAxisOffsetX + xend, kAxisOffsetY, zend}, {0.0, 0.0, -1.0}, double(br)},
+        {1, {kAxisOffsetX - xend, kAxisOffsetY, zend}, {0.0, 0.0, -1.0}, double(br)},
+    };
+    s.slice = [=](int32_t z, std::vector<int32_t>& xy) {
+        xy.clear();
         for (int y = -rmax; y <= rmax; ++y)
             for (int x = -xmax; x <= xmax; ++x) {
                 const double dy = y - kAxisOffsetY;
@@ -567,150 +611,242 @@ Domain build_bifurcation(int tr, int br, int tl, int bl, double voxel_size) {
                     fluid = dp * dp + dy * dy < br * br || dm * dm + dy * dy < br * br;
                 }
                 if (fluid) {
-                    vox.push_back(x);
-                    vox.push_back(y);
-                    vox.push_back(z);
+                    xy.push_back(x);
+                    xy.push_back(y);
                 }
             }
-    const double zend = double(tl + bl - 1) + 0.5;
-    const double xend = kSlope * bl;
-    std::vector<IoletGeo> io = {
-        {0, {kAxisOffsetX, kAxisOffsetY, -0.5}, {0.0, 0.0, 1.0}, double(tr)},
-        {1, {kAxisOffsetX + xend, kAxisOffsetY, zend}, {0.0, 0.0, -1.0}, double(br)},
-        {1, {kAxisOffsetX - xend, kAxisOffsetY, zend}, {0.0, 0.0, -1.0}, double(br)},
     };
-    return classify_sites(vox, std::move(io), voxel_size);
+    return s;
 }
 
-// Synthetic bifurcating vessel tree (config C3; no reference equivalent —
-// a recursive generalisation of build_bifurcation).  Level 0 is a trunk
-// along +z; every vessel of level k splits into two level-(k+1) vessels
-// whose centrelines diverge linearly, in x for odd levels and in y for even
-// ones, by a lateral offset sized so sibling subtrees never touch.  Each
-// z-slice is a union of discs (one per active vessel).  One pressure/velocity
-// inlet at the trunk start, one outlet disc per leaf in the last slice + 0.5.
-Domain build_tree(int root_radius, int root_length, int levels, double radius_ratio,
-                  double length_ratio, double voxel_size) {
+// Synthetic bifurcating vessel tree (configs C3 and C5; no reference
+// equivalent — a recursive generalisation of build_bifurcation).  Level 0 is
+// a trunk along +z; every vessel of level k splits into two level-(k+1)
+// vessels whose centrelines diverge linearly, in x for odd levels and in y
+// for even ones, by a lateral offset sized so sibling subtrees never touch.
+// Each z-slice is a union of discs (one per active vessel).  One inlet at the
+// trunk start, one outlet disc per leaf in the last slice + 0.5.
+Source source_tree(int root_radius, int root_length, int levels, double radius_ratio, double length_ratio,
+                   double voxel_size) {
     if (root_radius < 2 || root_length < 4 || levels < 0 || levels > 12 ||
         !(radius_ratio > 0.0 && radius_ratio <= 1.0) || !(length_ratio > 0.0))
         geometry_error("build_tree: need radius >= 2, length >= 4, 0 <= levels <= 12, "
                        "0 < radius_ratio <= 1, length_ratio > 0");
+    struct Tree {
+        int L = 0;
+        std::vector<double> rad, disp;
+        std::vector<int> len, z0;
+        std::vector<std::vector<std::array<double, 4>>> seg;  // x0,y0,x1,y1 per vessel
+    };
+    auto t = std::make_shared<Tree>();
     const int L = levels + 1;
-    std::vector<double> rad(L), disp(L, 0.0);
-    std::vector<int> len(L);
-    for (int k = 0; k < L; ++k) {
-        rad[k] = std::max(2.0, root_radius * std::pow(radius_ratio, k));
-    }
+    t->L = L;
+    t->rad.assign(L, 0.0);
+    t->disp.assign(L, 0.0);
+    t->len.assign(L, 0);
+    for (int k = 0; k < L; ++k) t->rad[k] = std::max(2.0, root_radius * std::pow(radius_ratio, k));
     // lateral offset of a level-k vessel over its length (k >= 1), from the
     // leaves up: clear the widest descendant spread on the same axis.
     for (int k = L - 1; k >= 1; --k) {
         double spread = 0.0;
-        for (int j = k + 2; j < L; j += 2) spread += disp[j];
-        disp[k] = spread + rad[k] + 2.0;
+        for (int j = k + 2; j < L; j += 2) spread += t->disp[j];
+        t->disp[k] = spread + t->rad[k] + 2.0;
     }
     for (int k = 0; k < L; ++k) {
         int l = int(std::lround(root_length * std::pow(length_ratio, k)));
         l = std::max(l, 4);
-        if (k >= 1) l = std::max(l, int(std::ceil(1.5 * disp[k])));  // slope <= 2/3
-        len[k] = l;
+        if (k >= 1) l = std::max(l, int(std::ceil(1.5 * t->disp[k])));  // slope <= 2/3
+        t->len[k] = l;
     }
-    std::vector<int> z0(L + 1, 0);
-    for (int k = 0; k < L; ++k) z0[k + 1] = z0[k] + len[k];
-    const int nz = z0[L];
+    t->z0.assign(L + 1, 0);
+    for (int k = 0; k < L; ++k) t->z0[k + 1] = t->z0[k] + t->len[k];
+    const int nz = t->z0[L];
     // Vessel v of level k runs from its parent's end point to that point
     // +- disp[k] (level 0: the straight trunk).
-    std::vector<std::vector<std::array<double, 4>>> seg(L);  // x0,y0,x1,y1
-    seg[0].push_back({kAxisOffsetX, kAxisOffsetY, kAxisOffsetX, kAxisOffsetY});
+    t->seg.resize(L);
+    t->seg[0].push_back({kAxisOffsetX, kAxisOffsetY, kAxisOffsetX, kAxisOffsetY});
     for (int k = 1; k < L; ++k)
-        for (auto& p : seg[k - 1]) {
-            const double dx = (k % 2 == 1) ? disp[k] : 0.0;
-            const double dy = (k % 2 == 0) ? disp[k] : 0.0;
-            seg[k].push_back({p[2], p[3], p[2] - dx, p[3] - dy});
-            seg[k].push_back({p[2], p[3], p[2] + dx, p[3] + dy});
+        for (auto& p : t->seg[k - 1]) {
+            const double dx = (k % 2 == 1) ? t->disp[k] : 0.0;
+            const double dy = (k % 2 == 0) ? t->disp[k] : 0.0;
+            t->seg[k].push_back({p[2], p[3], p[2] - dx, p[3] - dy});
+            t->seg[k].push_back({p[2], p[3], p[2] + dx, p[3] + dy});
         }
-    // voxelise slice by slice (parallel over slices), each slice sorted (y,x)
-    std::vector<std::vector<int32_t>> slices{size_t(nz)};
-    parallel_for(uint64_t(nz), [&](uint64_t b, uint64_t e, int) {
+    Source s;
+    s.voxel_size = voxel_size;
+    s.z0 = 0;
+    s.z1 = nz - 1;
+    s.iolets.push_back({0, {kAxisOffsetX, kAxisOffsetY, -0.5}, {0.0, 0.0, 1.0}, t->rad[0]});
+    {
+        const int k = L - 1;
+        const double zend = double(nz - 1) + 0.5;
+        for (auto& sg : t->seg[size_t(k)]) {
+            // leaf centre extrapolated to the outlet plane
+            const double f = (zend - t->z0[k] + 1.0) / double(t->len[k]);
+            s.iolets.push_back(
+                {1, {sg[0] + f * (sg[2] - sg[0]), sg[1] + f * (sg[3] - sg[1]), zend}, {0.0, 0.0, -1.0}, t->rad[k]});
+        }
+    }
+    s.slice = [t](int32_t z, std::vector<int32_t>& xy) {
+        int k = 0;
+        while (k + 1 < t->L && z >= t->z0[k + 1]) ++k;
         std::vector<uint64_t> keys;
-        for (uint64_t zz = b; zz < e; ++zz) {
-            const int z = int(zz);
-            int k = 0;
-            while (k + 1 < L && z >= z0[k + 1]) ++k;
-            keys.clear();
-            const double r = rad[k];
-            const double r2 = r * r;
-            const double f = len[k] > 1 ? double(z - z0[k] + 1) / double(len[k]) : 1.0;
-            auto add_disc = [&](double cx, double cy, double rr2, double rr) {
-                const int x0 = int(std::floor(cx - rr)) - 1, x1 = int(std::ceil(cx + rr)) + 1;
-                const int y0 = int(std::floor(cy - rr)) - 1, y1 = int(std::ceil(cy + rr)) + 1;
-                for (int y = y0; y <= y1; ++y)
-                    for (int x = x0; x <= x1; ++x) {
-                        const double dx = x - cx, dy = y - cy;
-                        if (dx * dx + dy * dy < rr2)
-                            keys.push_back((uint64_t(int64_t(y) + kBias) << 21) | uint64_t(int64_t(x) + kBias));
-                    }
-            };
-            for (auto& s : seg[size_t(k)]) {
-                const double cx = s[0] + f * (s[2] - s[0]);
-                const double cy = s[1] + f * (s[3] - s[1]);
-                add_disc(cx, cy, r2, r);
-            }
-            std::sort(keys.begin(), keys.end());
-            keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
-            auto& out = slices[zz];
-            out.resize(3 * keys.size());
-            const uint64_t m = (uint64_t(1) << 21) - 1;
-            for (size_t q = 0; q < keys.size(); ++q) {
-                out[3 * q] = int32_t(int64_t(keys[q] & m) - kBias);
-                out[3 * q + 1] = int32_t(int64_t(keys[q] >> 21) - kBias);
-                out[3 * q + 2] = z;
-            }
+        const double r = t->rad[k];
+        const double r2 = r * r;
+        const double f = t->len[k] > 1 ? double(z - t->z0[k] + 1) / double(t->len[k]) : 1.0;
+        for (auto& sg : t->seg[size_t(k)]) {
+            const double cx = sg[0] + f * (sg[2] - sg[0]);
+            const double cy = sg[1] + f * (sg[3] - sg[1]);
+            const int x0 = int(std::floor(cx - r)) - 1, x1 = int(std::ceil(cx + r)) + 1;
+            const int y0 = int(std::floor(cy - r)) - 1, y1 = int(std::ceil(cy + r)) + 1;
+            for (int y = y0; y <= y1; ++y)
+                for (int x = x0; x <= x1; ++x) {
+                    const double dx = x - cx, dy = y - cy;
+                    if (dx * dx + dy * dy < r2)
+                        keys.push_back((uint64_t(int64_t(y) + kBias) << 21) | uint64_t(int64_t(x) + kBias));
+                }
         }
-    }, 1);
-    uint64_t total = 0;
-    for (auto& s : slices) total += s.size();
-    std::vector<int32_t> vox;
-    vox.reserve(total);
-    for (auto& s : slices) {
-        vox.insert(vox.end(), s.begin(), s.end());
-        std::vector<int32_t>().swap(s);
-    }
-    phase("tree: voxelise");
-    std::vector<IoletGeo> io;
-    io.push_back({0, {kAxisOffsetX, kAxisOffsetY, -0.5}, {0.0, 0.0, 1.0}, rad[0]});
-    const int k = L - 1;
-    const double zend = double(nz - 1) + 0.5;
-    for (auto& s : seg[size_t(k)]) {
-        // leaf centre extrapolated to the outlet plane
-        const double f = (zend - z0[k] + 1.0) / double(len[k]);
-        io.push_back({1, {s[0] + f * (s[2] - s[0]), s[1] + f * (s[3] - s[1]), zend}, {0.0, 0.0, -1.0}, rad[k]});
-    }
-    return classify_sites(vox, std::move(io), voxel_size);
+        std::sort(keys.begin(), keys.end());
+        keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
+        xy.resize(2 * keys.size());
+        const uint64_t m = (uint64_t(1) << 21) - 1;
+        for (size_t q = 0; q < keys.size(); ++q) {
+            xy[2 * q] = int32_t(int64_t(keys[q] & m) - kBias);
+            xy[2 * q + 1] = int32_t(int64_t(keys[q] >> 21) - kBias);
+        }
+    };
+    return s;
 }
 
 // Dense rectangular channel (config C4): every voxel of [0,nx)x[0,ny)x[0,nz)
 // is fluid; inlet/outlet discs cover the whole cross-section.
-Domain build_channel(int nx, int ny, int nz, double voxel_size) {
+Source source_channel(int nx, int ny, int nz, double voxel_size) {
     if (nx < 2 || ny < 2 || nz < 4) geometry_error("build_channel: need nx, ny >= 2 and nz >= 4");
-    const uint64_t per = uint64_t(nx) * uint64_t(ny);
-    std::vector<int32_t> vox(3 * per * uint64_t(nz));
-    parallel_for(uint64_t(nz), [&](uint64_t b, uint64_t e, int) {
-        for (uint64_t z = b; z < e; ++z)
-            for (int y = 0; y < ny; ++y)
-                for (int x = 0; x < nx; ++x) {
-                    int32_t* v = &vox[3 * (z * per + uint64_t(y) * nx + uint64_t(x))];
-                    v[0] = x;
-                    v[1] = y;
-                    v[2] = int32_t(z);
-                }
-    }, 1);
+    Source s;
+    s.voxel_size = voxel_size;
+    s.z0 = 0;
+    s.z1 = nz - 1;
     const double cx = 0.5 * (nx - 1), cy = 0.5 * (ny - 1);
     const double rad = 0.5 * std::sqrt(double(nx) * nx + double(ny) * ny);
-    std::vector<IoletGeo> io = {
+    s.iolets = {
         {0, {cx, cy, -0.5}, {0.0, 0.0, 1.0}, rad},
         {1, {cx, cy, double(nz - 1) + 0.5}, {0.0, 0.0, -1.0}, rad},
     };
-    return classify_sites(vox, std::move(io), voxel_size);
+    s.slice = [nx, ny](int32_t, std::vector<int32_t>& xy) {
+        xy.resize(2 * uint64_t(nx) * uint64_t(ny));
+        uint64_t q = 0;
+        for (int y = 0; y < ny; ++y)
+            for (int x = 0; x < nx; ++x) xy[q++] = x, xy[q++] = y;
+    };
+    return s;
+}
+
+// Voxels of slices [za, zb] in zyx order (parallel over slices).
+static std::vector<int32_t> voxelise(const Source& src, int32_t za, int32_t zb) {
+    za = std::max(za, src.z0);
+    zb = std::min(zb, src.z1);
+    if (zb < za) return {};
+    const uint64_t ns = uint64_t(int64_t(zb) - za + 1);
+    std::vector<std::vector<int32_t>> slices(ns);
+    parallel_for(ns, [&](uint64_t b, uint64_t e, int) {
+        for (uint64_t k = b; k < e; ++k) src.slice(za + int32_t(k), slices[k]);
+    }, 1);
+    uint64_t total = 0;
+    for (auto& s : slices) total += s.size() / 2;
+    std::vector<int32_t> vox(3 * total);
+    std::vector<uint64_t> off(ns + 1, 0);
+    for (uint64_t k = 0; k < ns; ++k) off[k + 1] = off[k] + slices[k].size() / 2;
+    parallel_for(ns, [&](uint64_t b, uint64_t e, int) {
+        for (uint64_t k = b; k < e; ++k) {
+            const std::vector<int32_t>& xy = slices[k];
+            int32_t* v = &vox[3 * off[k]];
+            for (uint64_t q = 0; q < xy.size() / 2; ++q) {
+                v[3 * q] = xy[2 * q];
+                v[3 * q + 1] = xy[2 * q + 1];
+                v[3 * q + 2] = za + int32_t(k);
+            }
+            std::vector<int32_t>().swap(slices[k]);
+        }
+    }, 1);
+    return vox;
+}
+
+Domain build_from_source(const Source& src) {
+    std::vector<int32_t> vox = voxelise(src, src.z0, src.z1);
+    phase("source: voxelise");
+    return classify_sites(vox, src.iolets, src.voxel_size);
+}
+
+Domain build_pipe(int radius, int length, double voxel_size) {
+    return build_from_source(source_pipe(radius, length, voxel_size));
+}
+Domain build_bifurcation(int tr, int br, int tl, int bl, double voxel_size) {
+    return build_from_source(source_bifurcation(tr, br, tl, bl, voxel_size));
+}
+Domain build_tree(int root_radius, int root_length, int levels, double radius_ratio, double length_ratio,
+                  double voxel_size) {
+    return build_from_source(source_tree(root_radius, root_length, levels, radius_ratio, length_ratio, voxel_size));
+}
+Domain build_channel(int nx, int ny, int nz, double voxel_size) {
+    return build_from_source(source_channel(nx, ny, nz, voxel_size));
+}
+
+SourcePlan plan_source(const Source& src) {
+    SourcePlan p;
+    if (src.z1 < src.z0) return p;
+    const uint64_t ns = uint64_t(int64_t(src.z1) - src.z0 + 1);
+    p.plane_count.assign(ns, 0);
+    const int nt = hw_threads();
+    std::vector<std::array<int32_t, 4>> ext(nt, {INT32_MAX, INT32_MIN, INT32_MAX, INT32_MIN});
+    parallel_for(ns, [&](uint64_t b, uint64_t e, int t) {
+        std::vector<int32_t> xy;
+        for (uint64_t k = b; k < e; ++k) {
+            src.slice(src.z0 + int32_t(k), xy);
+            p.plane_count[k] = xy.size() / 2;
+            for (size_t q = 0; q < xy.size(); q += 2) {
+                ext[t][0] = std::min(ext[t][0], xy[q]);
+                ext[t][1] = std::max(ext[t][1], xy[q]);
+                ext[t][2] = std::min(ext[t][2], xy[q + 1]);
+                ext[t][3] = std::max(ext[t][3], xy[q + 1]);
+            }
+        }
+    }, 1);
+    p.lo[0] = p.lo[1] = p.lo[2] = INT32_MAX;
+    p.hi[0] = p.hi[1] = p.hi[2] = INT32_MIN;
+    for (auto& x : ext) {
+        p.lo[0] = std::min(p.lo[0], x[0]);
+        p.hi[0] = std::max(p.hi[0], x[1]);
+        p.lo[1] = std::min(p.lo[1], x[2]);
+        p.hi[1] = std::max(p.hi[1], x[3]);
+    }
+    for (uint64_t k = 0; k < ns; ++k)
+        if (p.plane_count[k]) {
+            p.n += p.plane_count[k];
+            p.lo[2] = std::min(p.lo[2], src.z0 + int32_t(k));
+            p.hi[2] = std::max(p.hi[2], src.z0 + int32_t(k));
+        }
+    return p;
+}
+
+Domain classify_slab(const Source& src, int32_t za, int32_t zb, std::vector<uint64_t>* io_links) {
+    for (size_t k = 0; k < src.iolets.size(); ++k)
+        if (!unit_normal(src.iolets[k]))
+            geometry_error("classify_sites: iolet " + std::to_string(k) + " normal is not unit length");
+    std::vector<int32_t> vox = voxelise(src, za - 1, zb + 1);  // + one classification-only slice each side
+    const uint64_t n = vox.size() / 3;
+    for (uint64_t s = 0; s < 3 * n; ++s)
+        if (vox[s] < -(int32_t(1) << 20) + 1 || vox[s] >= (int32_t(1) << 20) - 1)
+            geometry_error("classify_sites: voxel coordinate out of range");
+    std::vector<uint64_t> keys(n);
+    parallel_for(n, [&](uint64_t b, uint64_t e, int) {
+        for (uint64_t s = b; s < e; ++s) keys[s] = zyx_key(vox[3 * s], vox[3 * s + 1], vox[3 * s + 2]);
+    });
+    for (uint64_t s = 1; s < n; ++s)
+        if (!(keys[s - 1] < keys[s])) geometry_error("classify_slab: source slice not strictly (y, x)-ordered");
+    phase("slab: voxelise+keys");
+    std::vector<IoletGeo> io(src.iolets);
+    SlabKeep keep{za, zb, io_links};
+    return classify_sorted(std::move(vox), keys, nullptr, std::move(io), src.voxel_size, &keep);
 }
 
 // ---- SPLB v1 file format (geometry_io.hpp:14-129) ----------------------------

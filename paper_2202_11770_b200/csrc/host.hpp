@@ -110,6 +110,40 @@ Domain build_channel(int nx, int ny, int nz, double voxel_size);
 Domain read_domain(const std::string& path);
 void write_domain(const Domain& d, const std::string& path);
 
+// ---- geometry sources (slab-local construction) --------------
+// A generator evaluated one z-slice at a time.  The builders above are
+// build_from_source(source_*(...)); a distributed engine instead classifies
+// only its own slab (± halo planes) of the same source.
+struct Source {
+    double voxel_size = 1.0;
+    int32_t z0 = 0, z1 = -1;  // slices [z0, z1]
+    std::vector<IoletGeo> iolets;
+    // fluid voxels of slice z as (x, y) pairs in ascending (y, x) order
+    std::function<void(int32_t z, std::vector<int32_t>& xy)> slice;
+};
+Source source_pipe(int radius, int length, double voxel_size);
+Source source_bifurcation(int trunk_radius, int branch_radius, int trunk_length, int branch_length,
+                          double voxel_size);
+Source source_tree(int root_radius, int root_length, int levels, double radius_ratio, double length_ratio,
+                   double voxel_size);
+Source source_channel(int nx, int ny, int nz, double voxel_size);
+Domain build_from_source(const Source& src);
+
+// Per-slice fluid counts and the x/y extent of a source (every slice voxelised).
+struct SourcePlan {
+    std::vector<uint64_t> plane_count;  // slice z0 + k
+    int32_t lo[3] = {0, 0, 0}, hi[3] = {-1, -1, -1};
+    uint64_t n = 0;
+};
+SourcePlan plan_source(const Source& src);
+
+// Classified sites of slices [za, zb] of a source (clamped to its range).
+// Sites of the first/last slice are classified as if the neighbouring slices
+// were absent, so callers pass one extra slice on each side and discard it.
+// Unlike classify_sites, an iolet without links here is not an error (it may
+// lie in another slab); `io_links` counts each iolet's links.
+Domain classify_slab(const Source& src, int32_t za, int32_t zb, std::vector<uint64_t>* io_links);
+
 // ---- decomposition (decomp.hpp) ------------------------------------------
 struct WorkerPart {
     std::vector<uint32_t> sites;  // global indices, worker-local order
@@ -132,6 +166,50 @@ struct Partition {
 };
 
 Partition partition(const Domain& d, int n_workers, const SiteIndex* index = nullptr);
+
+// ---- slab-local construction (distributed engine) ----------
+// The reference partition of a source computed from per-slice counts alone:
+// valid when it is a z-slab split (longest axis z, at least as many non-empty
+// slices as workers), which is then the same split partition() makes of the
+// whole domain.
+struct SlabPlan {
+    bool ok = false;
+    uint64_t n = 0;                     // global site count
+    int32_t plane_lo = 0;               // first non-empty slice
+    std::vector<int32_t> plane_owner;   // slice plane_lo + k -> worker
+    std::vector<uint64_t> plane_count;  // slice plane_lo + k -> sites
+    int32_t own_lo(int w) const;
+    int32_t own_hi(int w) const;
+};
+SlabPlan plan_slabs(const SourcePlan& sp, int32_t z0, int n_workers);
+
+// One worker's window: its slices plus one halo slice on each side, with
+// sites in global (type-major zyx) order restricted to the window, so each
+// type's window sites are one contiguous run of the global order.
+struct Window {
+    Domain dom;
+    int worker = 0;
+    int32_t own_lo = 0, own_hi = -1;
+    uint64_t n_global = 0;
+    uint64_t g_type_ranges[6][2] = {};
+    uint64_t g_first[6] = {};  // global index of the window's first site of each type
+    uint64_t global_of(uint64_t s) const {
+        const int t = dom.types[s];
+        return g_first[t] + (s - dom.type_ranges[t][0]);
+    }
+};
+// Classifies the window of `worker`; `own_counts` receives the per-type
+// counts of each own slice (6 per slice, own_lo first) and `io_links` each
+// iolet's link count over the own slices.
+Window classify_window(const Source& src, const SlabPlan& plan, int worker, std::vector<uint64_t>* own_counts,
+                       std::vector<uint64_t>* io_links);
+// Fixes the global indices from every slice's per-type counts (6 per slice,
+// plane_lo first, all workers' own_counts concatenated in worker order).
+void finish_window(Window& w, const SlabPlan& plan, const std::vector<uint64_t>& counts);
+// partition() of the whole domain, restricted to what `w.worker` needs: the
+// owner of every window site, and the worker's own part (sites as window
+// indices) with its edge/mid groups and neighbours.  Other parts stay empty.
+Partition partition_window(const Window& w, const SlabPlan& plan, int n_workers);
 
 // ---- time tables (boundary.hpp:18-74) ------------------------------------
 struct TimeTable {

@@ -207,7 +207,17 @@ class SparseDomain:
 
     @property
     def iolets(self) -> List[Iolet]:
-        return self.export()["iolets"]
+        nio = int(lib.splbcu_domain_n_iolets(self._h))
+        ios = (L.Iolet * max(nio, 1))()
+        _check(lib.splbcu_domain_export(self._h, None, None, None, None, ios, None))
+        return [Iolet(ios[k].kind, list(ios[k].center), list(ios[k].normal), ios[k].radius) for k in range(nio)]
+
+    @property
+    def type_ranges(self) -> np.ndarray:
+        """[begin, end) of each CollisionType in site order (SparseDomain::type_ranges)."""
+        tr = np.zeros(12, np.uint64)
+        _check(lib.splbcu_domain_export(self._h, None, None, None, None, None, _ptr(tr, C.c_uint64)))
+        return tr.reshape(6, 2).astype(np.int64)
 
     def validate(self) -> None:
         _check(lib.splbcu_domain_validate(self._h))
@@ -269,6 +279,73 @@ def build_channel(nx, ny, nz, voxel_size=1.0):
     h = C.c_void_p()
     _check(lib.splbcu_domain_build_channel(nx, ny, nz, voxel_size, C.byref(h)))
     return SparseDomain(h)
+
+
+class Source:
+    """A geometry generator evaluated slice by slice (include/splbcu.h,
+    "geometry sources").  ``build()`` is the whole domain, identical to the
+    matching ``build_*``; ``Simulation.distributed(source, ...)`` builds only
+    each rank's slab."""
+
+    def __init__(self, handle):
+        self._h = C.c_void_p(handle) if not isinstance(handle, C.c_void_p) else handle
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and h.value:
+            lib.splbcu_source_free(h)
+            self._h = C.c_void_p(None)
+
+    @property
+    def handle(self):
+        return self._h
+
+    @staticmethod
+    def _make(fn, *args) -> "Source":
+        h = C.c_void_p()
+        _check(fn(*args, C.byref(h)))
+        return Source(h)
+
+    @staticmethod
+    def pipe(radius, length, voxel_size=1.0) -> "Source":
+        return Source._make(lib.splbcu_source_pipe, radius, length, voxel_size)
+
+    @staticmethod
+    def bifurcation(trunk_radius, branch_radius, trunk_length, branch_length, voxel_size=1.0) -> "Source":
+        return Source._make(lib.splbcu_source_bifurcation, trunk_radius, branch_radius, trunk_length,
+                            branch_length, voxel_size)
+
+    @staticmethod
+    def tree(root_radius, root_length, levels, radius_ratio=0.8, length_ratio=0.8, voxel_size=1.0) -> "Source":
+        return Source._make(lib.splbcu_source_tree, root_radius, root_length, levels, radius_ratio, length_ratio,
+                            voxel_size)
+
+    @staticmethod
+    def channel(nx, ny, nz, voxel_size=1.0) -> "Source":
+        return Source._make(lib.splbcu_source_channel, nx, ny, nz, voxel_size)
+
+    def build(self) -> "SparseDomain":
+        h = C.c_void_p()
+        _check(lib.splbcu_source_build(self._h, C.byref(h)))
+        return SparseDomain(h)
+
+    def window(self, n_workers: int, worker: int):
+        """What rank `worker` builds in slab-local mode: None when the
+        partition is not a z-slab split, else a dict with the window domain,
+        its global indices, own slice range, global site count and the
+        worker's part (site lists index the window)."""
+        slab = C.c_int32()
+        hd, hp = C.c_void_p(), C.c_void_p()
+        _check(lib.splbcu_source_window(self._h, n_workers, worker, C.byref(slab), C.byref(hd), C.byref(hp)))
+        if not slab.value:
+            return None
+        dom = SparseDomain(hd)
+        n = dom.n_sites()
+        gi = np.zeros(max(n, 1), np.uint64)
+        ng, lo, hi = C.c_uint64(), C.c_int32(), C.c_int32()
+        _check(lib.splbcu_window_info(hd, C.byref(ng), C.byref(lo), C.byref(hi), _ptr(gi, C.c_uint64)))
+        part = PartitionAssignment(hp, n, n_workers)
+        return dict(domain=dom, global_index=gi[:n], own=(lo.value, hi.value), n_global=ng.value, part=part)
 
 
 # ---- decomposition ----------------------------------------------------------------
@@ -424,6 +501,7 @@ class Simulation:
     def __init__(self, domain: SparseDomain, bcs: BCSet, params: EngineParams, _dist=None):
         self.domain_ = domain
         self.params = params
+        self._n_io = len(bcs.entries)
         arr, keep = _bc_array(bcs)
         pc, devs = _params_c(params)
         h = C.c_void_p()
@@ -432,8 +510,8 @@ class Simulation:
         else:
             rank, nranks, uid = _dist
             idb = (C.c_uint8 * 128).from_buffer_copy(bytes(uid))
-            _check(lib.splbcu_sim_create_dist(domain.handle, arr, len(bcs.entries), C.byref(pc), rank, nranks,
-                                              idb, C.byref(h)))
+            create = lib.splbcu_sim_create_dist_source if isinstance(domain, Source) else lib.splbcu_sim_create_dist
+            _check(create(domain.handle, arr, len(bcs.entries), C.byref(pc), rank, nranks, idb, C.byref(h)))
         self._h = h
         del keep, devs
         self._part = None
@@ -446,7 +524,16 @@ class Simulation:
 
     @classmethod
     def distributed(cls, domain, bcs, params, rank: int, nranks: int, uid: bytes) -> "Simulation":
+        """One process per GPU.  `domain` may be a SparseDomain (every rank
+        holds all of it) or a Source (slab-local construction)."""
         return cls(domain, bcs, params, _dist=(rank, nranks, uid))
+
+    def slab_local(self) -> bool:
+        return bool(lib.splbcu_sim_slab_local(self._h))
+
+    def n_sites(self) -> int:
+        """Sites of the whole domain."""
+        return int(lib.splbcu_sim_n_sites(self._h))
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -495,8 +582,11 @@ class Simulation:
     def launch_count(self) -> int:
         return int(lib.splbcu_sim_launch_count(self._h))
 
+    def observed_sites(self) -> int:
+        return int(lib.splbcu_sim_observed_sites(self._h))
+
     def snapshot_fields(self) -> np.ndarray:
-        out = np.zeros(4 * self.domain_.n_sites())
+        out = np.zeros(4 * self.n_sites())
         _check(lib.splbcu_sim_snapshot(self._h, _ptr(out, C.c_double)))
         return out
 
@@ -509,8 +599,9 @@ class Simulation:
     def assignment(self) -> PartitionAssignment:
         if self._part is None:
             h = lib.splbcu_sim_partition(self._h)
-            self._part = PartitionAssignment(C.c_void_p(h), self.domain_.n_sites(), self.params.workers,
-                                             owned=False)
+            if not h:
+                raise Error("assignment(): not held by a slab-local simulation")
+            self._part = PartitionAssignment(C.c_void_p(h), self.n_sites(), self.params.workers, owned=False)
         return self._part
 
     def map(self, w: int) -> StreamingMap:
@@ -535,7 +626,7 @@ class Simulation:
 
     def cache(self) -> List[Capture]:
         out = []
-        n = self.domain_.n_sites()
+        n = self.n_sites()
         for k in range(int(lib.splbcu_sim_n_captures(self._h))):
             st = C.c_uint64()
             f = np.zeros(4 * n)
@@ -545,7 +636,7 @@ class Simulation:
 
     def series(self):
         rows = int(lib.splbcu_sim_series_rows(self._h))
-        nio = int(lib.splbcu_domain_n_iolets(self.domain_.handle))
+        nio = self._n_io  # one BC entry per iolet (validated at construction)
         res = dict(rows=rows, max_speed=[], pressure=[], flow=[])
         if rows == 0:
             return res

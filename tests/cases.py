@@ -159,10 +159,11 @@ def noise_for(n_sites, seed, amp):
     return rng.uniform(0.0, amp, size=(n_sites, 19))
 
 
-def apply_noise(M, sim, noise):
+def apply_noise(M, sim, noise, pa=None):
     """Adds noise[g, i] to f_old of global site g, direction i, on every
-    worker the simulation holds (reference layout / local order)."""
-    pa = sim.assignment()
+    worker the simulation holds (reference layout / local order).  `pa`
+    (parts[w].sites = global indices) defaults to sim.assignment()."""
+    pa = pa or sim.assignment()
     for w in range(pa.n_workers):
         if not sim.is_local(w):
             continue

@@ -89,7 +89,7 @@ def test_gloo_two_ranks_agree_on_decomposition():
 
 
 NCCL_SCRIPT = textwrap.dedent("""
-    import os
+    import os, types
     import numpy as np
     import torch, torch.distributed as td
     import cases, impls
@@ -104,10 +104,23 @@ NCCL_SCRIPT = textwrap.dedent("""
                noise=(11, 0.01))
     d = cases.make_domain(P, cases.DOMAINS[run["domain"]])
     kw = dict(tau=0.8, dt_s=1e-3, workers=world, capture_period=20, observe_iolets=True)
-    mode = int(os.environ["HALO"])  # 0 NCCL, 1 fused P2P, 2 AA single buffer (P2P in place)
-    prm = P.EngineParams(devices=[rank], halo_mode=min(mode, 1), storage=1 if mode == 2 else 0, **kw)
-    sim = P.Simulation.distributed(d, cases.make_bcs(P, run["bcs"]), prm, rank, world, obj[0])
-    cases.apply_noise(P, sim, cases.noise_for(d.n_sites(), *run["noise"]))
+    # 0 NCCL, 1 fused P2P, 2 AA single buffer (P2P in place); 3/4/5 the same
+    # three built slab-locally from a geometry source
+    mode = int(os.environ["HALO"])
+    base = mode % 3
+    prm = P.EngineParams(devices=[rank], halo_mode=min(base, 1), storage=1 if base == 2 else 0, **kw)
+    pa = None
+    if mode >= 3:
+        src = P.Source.bifurcation(4, 3, 12, 12)
+        sim = P.Simulation.distributed(src, cases.make_bcs(P, run["bcs"]), prm, rank, world, obj[0])
+        assert sim.slab_local() and sim.n_sites() == d.n_sites()
+        win = src.window(world, rank)
+        parts = [types.SimpleNamespace(sites=np.zeros(0, np.int64)) for _ in range(world)]
+        parts[rank] = types.SimpleNamespace(sites=win["global_index"][win["part"].parts[rank].sites])
+        pa = types.SimpleNamespace(n_workers=world, parts=parts)
+    else:
+        sim = P.Simulation.distributed(d, cases.make_bcs(P, run["bcs"]), prm, rank, world, obj[0])
+    cases.apply_noise(P, sim, cases.noise_for(d.n_sites(), *run["noise"]), pa)
     sim.run(25)
     sim.run(run["steps"] - 25)
     # snapshot, captures and iolet series are assembled across ranks
@@ -126,10 +139,12 @@ NCCL_SCRIPT = textwrap.dedent("""
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("halo", ["0", "1", "2"])
+@pytest.mark.parametrize("halo", ["0", "1", "2", "3", "4", "5"])
 def test_nccl_ranks_match_single_process(halo):
-    """halo 0: NCCL send/recv + PostReceive; halo 1: fused NVLink P2P stores
-    into IPC-mapped neighbour buffers, flag-synchronised."""
+    """halo 0: NCCL send/recv + PostReceive; 1: fused NVLink P2P stores into
+    IPC-mapped neighbour buffers, flag-synchronised; 2: AA single buffer.
+    3/4/5: the same built slab-locally (each rank classifies only its own
+    slices of a geometry source)."""
     import torch
     n = torch.cuda.device_count()
     if n < 2:

@@ -147,3 +147,69 @@ def test_tree_size_model(product):
     e = d.export()
     assert d.n_sites() > 10000
     assert len(e["iolets"]) == 1 + 2 ** 4
+
+
+# ---- slab-local construction ---------------------------------
+SOURCES = {
+    "pipe": (("pipe", 6, 40), "build_pipe", (6, 40)),
+    "bifurcation": (("bifurcation", 5, 3, 12, 16), "build_bifurcation", (5, 3, 12, 16)),
+    "tree": (("tree", 6, 24, 3, 0.8, 0.8), "build_tree", (6, 24, 3, 0.8, 0.8)),
+    "channel": (("channel", 6, 5, 30), "build_channel", (6, 5, 30)),
+}
+
+
+def _source(P, spec):
+    kind, *args = spec
+    return getattr(P.Source, kind)(*args)
+
+
+@pytest.mark.parametrize("name", sorted(SOURCES))
+def test_source_build_matches_builder(product, name):
+    spec, builder, args = SOURCES[name]
+    a = _source(product, spec).build().export()
+    b = getattr(product, builder)(*args).export()
+    for k in ("coords", "types", "link_kind", "link_iolet", "type_ranges"):
+        assert np.array_equal(a[k], b[k]), k
+
+
+@pytest.mark.parametrize("name", sorted(SOURCES))
+@pytest.mark.parametrize("W", [1, 2, 3, 5])
+def test_source_window_matches_whole_domain(product, name, W):
+    """Each rank's window (own slices + one halo slice per side) holds exactly
+    the whole domain's sites there, at their global indices, classified the
+    same; its part equals partition() of the whole domain."""
+    spec, builder, args = SOURCES[name]
+    src = _source(product, spec)
+    full = getattr(product, builder)(*args)
+    e = full.export()
+    part = product.partition(full, W)
+    z = e["coords"][:, 2]
+    for w in range(W):
+        win = src.window(W, w)
+        assert win is not None
+        assert win["n_global"] == full.n_sites()
+        lo, hi = win["own"]
+        gi = win["global_index"].astype(np.int64)
+        want = np.flatnonzero((z >= lo - 1) & (z <= hi + 1))
+        assert np.array_equal(np.sort(gi), want)  # the window is exactly those slices
+        assert np.all(np.diff(gi[np.argsort(gi)]) > 0)
+        we = win["domain"].export()
+        for k in ("coords", "types", "link_kind", "link_iolet"):
+            assert np.array_equal(we[k], e[k][gi]), k
+        mine = win["part"].parts[w]
+        ref = part.parts[w]
+        assert np.array_equal(gi[mine.sites], ref.sites.astype(np.int64))
+        assert mine.n_edge == ref.n_edge
+        assert np.array_equal(mine.edge_ranges, ref.edge_ranges)
+        assert np.array_equal(mine.mid_ranges, ref.mid_ranges)
+        assert mine.neighbors == ref.neighbors
+        assert np.array_equal(win["part"].owner, part.owner[gi])
+
+
+def test_source_window_not_slab(product):
+    """Longest axis x (a wide, short channel) or more workers than slices:
+    the partition is not a z-slab split, so ranks build the whole domain."""
+    assert product.Source.channel(40, 6, 12).window(2, 0) is None
+    assert product.Source.pipe(4, 6).window(7, 0) is None
+    with pytest.raises(product.GeometryError, match="build_pipe"):
+        product.Source.pipe(1, 6)
