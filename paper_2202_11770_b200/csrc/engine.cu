@@ -361,6 +361,12 @@ class Engine {
     PinnedMem h_staged;  // per-run iolet values (run() staging)
     DevMem obs_gather;   // dist mode: every rank's observation rows (padded)
     PinnedMem h_gather;
+    // device-side series (reduce_series_async): entry lists in series order
+    bool dev_series = false;
+    uint32_t n_series_ent = 0, ser_host_ent = 0;
+    std::vector<uint32_t> ser_host_k, ser_dev_k, ser_be;  // iolets reduced on host / device; entry ranges
+    DevMem ser_w, ser_idx, ser_off, ser_tot, ser_kdev, ser_buf, ser_out;
+    PinnedMem h_series, h_series_raw;
 
     // dist mode: elements per rank in the padded all-gather of observation
     // rows (every rank's obs_buf is reserved to this size)
@@ -427,11 +433,12 @@ class Engine {
                 if (c == 0)
                     geometry_error("classify_sites: iolet " + std::to_string(k) + " intersects no boundary links");
             }
-            dom = std::move(win->dom);  // the engine's domain is the window
-            n_global = win->n_global;
-            validate_params();
             part = partition_window(*win, plan, prm.workers);
             phase("slab: partition");
+            dom = std::move(win->dom);  // the engine's domain is the window
+            win->dom = Domain{};
+            n_global = win->n_global;
+            validate_params();
         }
         finish_setup();
     }
@@ -1098,6 +1105,74 @@ class Engine {
             upload(wk.obs_iolet, iol, wk.sM);
             CK(cudaStreamSynchronize(wk.sM));
         }
+        // Series on the device when one worker's device sees every row: dist
+        // mode (after the all-gather) or a single in-process worker.  A
+        // gather kernel puts the entries in series order (long iolets first);
+        // short iolets are reduced there by series_chain, long ones (whose
+        // sequential chain the host runs ~5x faster) are copied out and
+        // reduced on the host, in the same order.
+        dev_series = (dist || prm.workers == 1) && getenv("SPLBCU_HOST_SERIES") == nullptr;
+        if (dev_series) {
+            WorkerDev& wk = *W[size_t(dist ? rank : 0)];
+            CK(cudaSetDevice(wk.dev));
+            constexpr size_t kHostChain = 2048;  // entries per iolet above which the host reduces it
+            std::vector<uint16_t> ew;
+            std::vector<uint32_t> ei, be(2 * n_io, 0), tot(size_t(prm.workers));
+            ser_host_k.clear();
+            ser_dev_k.clear();
+            for (size_t k = 0; k < n_io; ++k) (obs_order[k].size() > kHostChain ? ser_host_k : ser_dev_k).push_back(uint32_t(k));
+            for (const std::vector<uint32_t>* list : {&ser_host_k, &ser_dev_k})
+                for (uint32_t k : *list) {
+                    be[2 * k] = uint32_t(ew.size());
+                    for (const auto& [w, pos] : obs_order[k]) {
+                        ew.push_back(uint16_t(w));
+                        ei.push_back(obs_off_all[size_t(w)][k] + pos);
+                    }
+                    be[2 * k + 1] = uint32_t(ew.size());
+                }
+            ser_host_ent = ser_host_k.empty() ? 0 : be[2 * ser_host_k.back() + 1];
+            ser_be = be;
+            for (int w = 0; w < prm.workers; ++w) tot[size_t(w)] = obs_off_all[size_t(w)][n_io];
+            n_series_ent = uint32_t(ew.size());
+            upload(ser_w, ew, wk.sM);
+            upload(ser_idx, ei, wk.sM);
+            upload(ser_off, be, wk.sM);
+            upload(ser_tot, tot, wk.sM);
+            upload(ser_kdev, ser_dev_k, wk.sM);
+            CK(cudaStreamSynchronize(wk.sM));
+        }
+    }
+
+    // run()'s series: gather this run's rows into series order, reduce the
+    // short iolets on the device, and copy results + the long iolets' entries
+    // to pinned host memory, on stream s (behind the step loop).
+    void reduce_series_async(WorkerDev& wk, cudaStream_t s, const double* src, uint64_t per) {
+        const uint32_t rows = uint32_t(wk.obs_rows), n_io = uint32_t(dom.iolets.size());
+        if (!rows || !n_io) return;
+        const uint64_t ne = std::max<uint32_t>(n_series_ent, 1);
+        double* g = ser_buf.reserve<double>(3 * uint64_t(rows) * ne);
+        double* o = ser_out.reserve<double>(3 * uint64_t(rows) * n_io);
+        const uint64_t ng = uint64_t(n_series_ent) * rows;
+        if (ng) {
+            series_gather<<<unsigned((ng + 255) / 256), 256, 0, s>>>(src, per, ser_tot.get<uint32_t>(),
+                                                                       ser_w.get<uint16_t>(), ser_idx.get<uint32_t>(),
+                                                                       n_series_ent, rows, g);
+            ++launches;
+        }
+        if (!ser_dev_k.empty()) {
+            const uint64_t warps = uint64_t(ser_dev_k.size()) * rows;
+            series_chain<<<unsigned(warps), 32, 0, s>>>(g, ser_kdev.get<uint32_t>(), ser_off.get<uint32_t>(),
+                                                        uint32_t(ser_dev_k.size()), n_io, rows, n_series_ent, o);
+            ++launches;
+        }
+        CK(cudaGetLastError());
+        double* h = h_series.reserve<double>(3 * uint64_t(rows) * n_io);
+        CK(cudaMemcpyAsync(h, o, 3 * uint64_t(rows) * n_io * 8, cudaMemcpyDeviceToHost, s));
+        if (ser_host_ent) {
+            double* hr = h_series_raw.reserve<double>(3 * uint64_t(rows) * ser_host_ent);
+            CK(cudaMemcpy2DAsync(hr, 3 * size_t(ser_host_ent) * 8, g, 3 * size_t(ne) * 8, 3 * size_t(ser_host_ent) * 8,
+                                 rows, cudaMemcpyDeviceToHost, s));
+        }
     }
 
     // ---- stepping -----------------------------------------------------------
@@ -1493,9 +1568,18 @@ class Engine {
                     CK(cudaStreamWaitEvent(wk.sE, t1[w], 0));
                     double* dr = obs_gather.reserve<double>(per * uint64_t(nranks));
                     NK(nccl().AllGather(wk.obs_buf.get<double>(), dr, per, ncclDouble, comm, wk.sE));
-                    double* h = h_gather.reserve<double>(per * uint64_t(nranks));
-                    CK(cudaMemcpyAsync(h, dr, per * uint64_t(nranks) * 8, cudaMemcpyDeviceToHost, wk.sE));
+                    if (dev_series) {
+                        reduce_series_async(wk, wk.sE, dr, per);
+                    } else {
+                        double* h = h_gather.reserve<double>(per * uint64_t(nranks));
+                        CK(cudaMemcpyAsync(h, dr, per * uint64_t(nranks) * 8, cudaMemcpyDeviceToHost, wk.sE));
+                    }
                     CK(cudaEventRecord(done[w], wk.sE));
+                    continue;
+                }
+                if (prm.observe_iolets && dev_series) {
+                    reduce_series_async(wk, wk.sM, wk.obs_buf.get<double>(), 0);
+                    CK(cudaEventRecord(done[w], wk.sM));
                     continue;
                 }
                 const size_t nb = prm.observe_iolets ? 3 * wk.obs_rows * wk.n_obs : 0;
@@ -1505,7 +1589,7 @@ class Engine {
                 }
                 CK(cudaEventRecord(done[w], wk.sM));
             }
-        wait_all(done);
+        wait_all(done, n);
         const auto h1 = std::chrono::steady_clock::now();
         double dmax = 0.0;
         for (size_t w = 0; w < W.size(); ++w)
@@ -1532,9 +1616,11 @@ class Engine {
         }
     }
 
-    // Waits for the step loop; in NCCL mode polls for async comm errors and
-    // applies the reference's exchange timeout (engine.hpp:92-101).
-    void wait_all(const std::vector<cudaEvent_t>& ev) {
+    // Waits for the step loop; in dist mode polls for async comm errors and
+    // applies the reference's exchange timeout (engine.hpp:92-101), scaled to
+    // the run: exchange_timeout_s * (1 + n_steps / 100) for the whole run.
+    void wait_all(const std::vector<cudaEvent_t>& ev, uint64_t n_steps) {
+        const double limit = prm.exchange_timeout_s * (1.0 + double(n_steps) / 100.0);
         const auto start = std::chrono::steady_clock::now();
         for (size_t w = 0; w < W.size(); ++w) {
             if (!W[w]) continue;
@@ -1552,7 +1638,7 @@ class Engine {
                 if (ar != ncclSuccess && ar != ncclInProgress)
                     fail(ErrKind::Comm, std::string("exchange failure: NCCL async error: ") + nccl().GetErrorString(ar));
                 const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - start).count();
-                if (el > prm.exchange_timeout_s * 1000.0) {  // generous: whole run, not one take
+                if (el > limit) {
                     nccl().CommAbort(comm);
                     comm = nullptr;
                     const int nb = W[w]->segs.empty() ? -1 : W[w]->segs.front().nb;
@@ -1822,6 +1908,40 @@ class Engine {
     void assemble_series() {
         if (!prm.observe_iolets) return;
         const size_t n_io = dom.iolets.size();
+        if (dev_series) {
+            // (vmax, pressure, flow) per (row, iolet): short iolets reduced on
+            // the device by run(); long ones here from their gathered entries
+            const uint64_t first_row = series.rows, rows = steps_run + 1;
+            double* h = h_series.get<double>();
+            const double* raw = h_series_raw.get<double>();
+            for (uint64_t r = 0; r < rows - first_row; ++r)
+                for (uint32_t k : ser_host_k) {
+                    const uint32_t b = ser_be[2 * k], e = ser_be[2 * k + 1];
+                    const double* v = raw + 3 * (r * ser_host_ent + b);
+                    double vmax = 0.0, psum = 0.0, qsum = 0.0;
+                    for (uint32_t j = b; j < e; ++j, v += 3) {
+                        vmax = std::max(vmax, v[0]);
+                        psum += v[1];
+                        qsum += v[2];
+                    }
+                    double* o = h + 3 * (r * n_io + k);
+                    o[0] = vmax;
+                    o[1] = psum / double(e - b);
+                    o[2] = qsum;
+                }
+            series.max_speed.resize(n_io);
+            series.pressure.resize(n_io);
+            series.flow.resize(n_io);
+            for (size_t k = 0; k < n_io; ++k)
+                for (uint64_t row = first_row; row < rows; ++row) {
+                    const double* v = h + 3 * ((row - first_row) * n_io + k);
+                    series.max_speed[k].push_back(v[0]);
+                    series.pressure[k].push_back(v[1]);
+                    series.flow[k].push_back(v[2]);
+                }
+            series.rows = rows;
+            return;
+        }
         // this run's rows were copied into each worker's pinned h_obs by run()
         std::vector<const double*> hb(W.size(), nullptr);
         for (size_t w = 0; w < W.size(); ++w)

@@ -967,6 +967,95 @@ __global__ void lbm_iolet_observe(const double* __restrict__ f, uint64_t P, uint
     o[2] = (m.ux * g.normal[0] + m.uy * g.normal[1]) + m.uz * g.normal[2];
 }
 
+// ---- iolet series on the device (assemble_series, engine.hpp:602-629) ------
+// Observation rows of every worker (worker w's rows at src + per*w, each row
+// tot[w] entries of 3 doubles) are first gathered into iolet-major order
+// (entry j of the CSR ent_* lists, ascending global site per iolet), then one
+// warp per (iolet, row) runs the reference's sequential reduction.
+__global__ void series_gather(const double* __restrict__ src, uint64_t per, const uint32_t* __restrict__ tot,
+                              const uint16_t* __restrict__ ent_w, const uint32_t* __restrict__ ent_idx,
+                              uint32_t n_ent, uint32_t rows, double* __restrict__ dst) {
+    const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= uint64_t(n_ent) * rows) return;
+    const uint32_t j = uint32_t(t % n_ent), r = uint32_t(t / n_ent);
+    const uint32_t w = ent_w[j];
+    const double* v = src + per * w + 3 * (uint64_t(r) * tot[w] + ent_idx[j]);
+    double* o = dst + 3 * t;
+    o[0] = v[0];
+    o[1] = v[1];
+    o[2] = v[2];
+}
+
+// Sequential in entry order, as the host loop: vmax = std::max(vmax, v0),
+// psum += v1, qsum += v2; then (vmax, psum / n, qsum).  One warp per
+// (iolet, row), launched as 32-thread blocks.  The lanes stage chunks of
+// kChunk entries in shared memory, loading the next chunk into registers
+// while every lane runs the same ordered add chain over the current one with
+// broadcast reads, so the sums are bit-identical to the host's.  The max is
+// order-free: (v < x) ? x : v from +0.0 keeps the first of equal values and
+// skips NaN, so each lane folds its own entries and the lanes are folded.
+__global__ void __launch_bounds__(32) series_chain(const double* __restrict__ g, const uint32_t* __restrict__ kdev,
+                                                   const uint32_t* __restrict__ ent_be, uint32_t n_dev, uint32_t n_io,
+                                                   uint32_t rows, uint32_t n_ent, double* __restrict__ out) {
+    constexpr int kPer = 8, kChunk = 32 * kPer;  // a chunk's chain (~kChunk DADD latencies) covers a load
+    __shared__ double c1[kChunk], c2[kChunk];
+    const uint32_t warp = blockIdx.x;
+    const int lane = threadIdx.x;
+    if (warp >= n_dev * rows) return;
+    const uint32_t k = kdev[warp % n_dev], r = warp / n_dev;
+    const uint32_t b = ent_be[2 * k], e = ent_be[2 * k + 1];
+    const double* base = g + 3 * (uint64_t(r) * n_ent);
+    double vmax = 0.0, psum = 0.0, qsum = 0.0;
+    double a0[kPer], a1[kPer], a2[kPer];
+    auto load = [&](uint32_t c) {
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+            const uint32_t x = c + uint32_t(u * 32 + lane);
+            if (x < e) {
+                const double* v = base + 3 * uint64_t(x);
+                a0[u] = v[0], a1[u] = v[1], a2[u] = v[2];
+            } else {
+                a0[u] = 0.0, a1[u] = 0.0, a2[u] = 0.0;
+            }
+        }
+    };
+    load(b);
+    for (uint32_t c = b; c < e; c += kChunk) {
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+            vmax = (vmax < a0[u]) ? a0[u] : vmax;
+            c1[u * 32 + lane] = a1[u];
+            c2[u * 32 + lane] = a2[u];
+        }
+        __syncwarp();
+        load(c + kChunk);
+        if (e - c >= uint32_t(kChunk)) {
+#pragma unroll 32
+            for (int l = 0; l < kChunk; ++l) {
+                psum += c1[l];
+                qsum += c2[l];
+            }
+        } else {
+            for (uint32_t l = 0; l < e - c; ++l) {
+                psum += c1[l];
+                qsum += c2[l];
+            }
+        }
+        __syncwarp();
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double x = __shfl_xor_sync(0xffffffffu, vmax, o);
+        vmax = (vmax < x) ? x : vmax;
+    }
+    if (lane == 0) {
+        double* o = out + 3 * (uint64_t(r) * n_io + k);
+        o[0] = vmax;
+        o[1] = psum / double(e - b);
+        o[2] = qsum;
+    }
+}
+
 #endif  // __CUDACC__
 
 }  // namespace splbcu

@@ -31,7 +31,11 @@ def _free_port():
     return p
 
 
-def _run_ranks(script, world, env_extra=None, timeout=600):
+def _run_ranks(script, world, env_extra=None, timeout=300):
+    """Runs `script` as `world` ranks; a rank still running at the deadline
+    (e.g. waiting on a peer that died) is killed with all the others."""
+    import time
+    deadline = time.time() + timeout
     port = _free_port()
     procs = []
     for r in range(world):
@@ -43,10 +47,12 @@ def _run_ranks(script, world, env_extra=None, timeout=600):
     outs = []
     for p in procs:
         try:
-            out, _ = p.communicate(timeout=timeout)
+            out, _ = p.communicate(timeout=max(1.0, deadline - time.time()))
         except subprocess.TimeoutExpired:
-            p.kill()
+            for q in procs:
+                q.kill()
             out, _ = p.communicate()
+            out += "\n[test harness] killed at the deadline"
         outs.append((p.returncode, out))
     return outs
 
