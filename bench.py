@@ -329,13 +329,14 @@ def main():
     e2e_s = max_over_ranks(time.perf_counter() - t0)
     ser = sim.series()
     n_obs = sum(1 for _ in ser["flow"])
-    # observation entries (sites x iolets they observe): the per-step row is
-    # 24 B each, device -> host
-    obs_sites = sim.observed_sites()
+    # the series row's device -> host bytes (reduced values + the entries of
+    # the iolets the host reduces)
+    d2h = sim.series_d2h_bytes()
     e2e = {"value": n * e2e_steps / e2e_s / 1e6, "unit": "MSUPS",
-           "h2d_bytes_per_step": 8 * len(bcs.entries), "d2h_bytes_per_step": 24 * obs_sites,
-           "note": "Simulation.run(1) per step via the C-ABI, iolet series on (per-step BC staging H2D, "
-                   "observation row D2H), host wall clock"}
+           "h2d_bytes_per_step": 8 * len(bcs.entries), "d2h_bytes_per_step": d2h,
+           "note": "Simulation.run(1) per step via the C-ABI with the iolet series on: per-step BC values "
+                   "H2D, the step, the series row (all-gathered across ranks, reduced in the reference's order) "
+                   "D2H, host wall clock"}
     sim.close()
 
     cpu = None

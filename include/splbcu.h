@@ -299,10 +299,9 @@ int splbcu_sim_kernel_stats(const splbcu_sim* s, double* plain_seconds,
                             uint64_t* plain_launches, uint64_t* plain_sites);
 /* Number of kernels this handle launched inside run() so far. */
 uint64_t splbcu_sim_launch_count(const splbcu_sim* s);
-/* Observation entries per series row over all workers (a site counted once
- * per iolet it observes; 0 unless observe_iolets): each row moves 24 B per
- * entry device -> host. */
-uint64_t splbcu_sim_observed_sites(const splbcu_sim* s);
+/* Bytes the iolet series moves device -> host per step (0 unless
+ * observe_iolets): reduced rows plus the entries of iolets the host reduces. */
+uint64_t splbcu_sim_series_d2h_bytes(const splbcu_sim* s);
 void splbcu_sim_destroy(splbcu_sim* s);
 
 #ifdef __cplusplus

@@ -450,7 +450,7 @@ int splbcu_sim_create_dist_source(const splbcu_source*, const splbcu_bc*, uint32
     return SPLBCU_ERR_CONFIG;
 }
 int32_t splbcu_sim_slab_local(const splbcu_sim*) { return 0; }
-uint64_t splbcu_sim_observed_sites(const splbcu_sim*) { return 0; }
+uint64_t splbcu_sim_series_d2h_bytes(const splbcu_sim*) { return 0; }
 uint64_t splbcu_sim_n_sites(const splbcu_sim* s) { return s->dom_n; }
 
 uint64_t splbcu_sim_launch_count(const splbcu_sim*) { return 0; }

@@ -1302,7 +1302,7 @@ int splbcu_sim_create_dist_source(const splbcu_source* a, const splbcu_bc* b, ui
     (void)a, (void)b, (void)c, (void)d, (void)e, (void)f, (void)g, (void)h;
     return set_err(SPLBCU_ERR_CONFIG, "oracle: no NCCL path");
 }
-uint64_t splbcu_sim_observed_sites(const splbcu_sim* S) {
+uint64_t splbcu_sim_series_d2h_bytes(const splbcu_sim* S) {
     (void)S;
     return 0;
 }

@@ -455,7 +455,7 @@ int splbcu_sim_create_dist_source(const splbcu_source* src, const splbcu_bc* bcs
         *out = s.release();
     });
 }
-uint64_t splbcu_sim_observed_sites(const splbcu_sim* s) { return s ? s->s->observed_sites() : 0; }
+uint64_t splbcu_sim_series_d2h_bytes(const splbcu_sim* s) { return s ? s->s->series_d2h_bytes() : 0; }
 int32_t splbcu_sim_slab_local(const splbcu_sim* s) { return s && s->s->slab_local() ? 1 : 0; }
 uint64_t splbcu_sim_n_sites(const splbcu_sim* s) { return s ? s->s->n_sites() : 0; }
 

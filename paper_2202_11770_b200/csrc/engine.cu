@@ -368,6 +368,15 @@ class Engine {
     DevMem ser_w, ser_idx, ser_off, ser_tot, ser_kdev, ser_buf, ser_out;
     PinnedMem h_series, h_series_raw;
 
+    uint64_t series_d2h_bytes() const {
+        if (!prm.observe_iolets) return 0;
+        if (dev_series) return 24 * (uint64_t(dom.iolets.size()) + ser_host_ent);
+        uint64_t n = 0;  // host path: every local worker's rows
+        for (auto& wp : W)
+            if (wp) n += wp->n_obs;
+        return 24 * n;
+    }
+
     // dist mode: elements per rank in the padded all-gather of observation
     // rows (every rank's obs_buf is reserved to this size)
     uint64_t obs_gather_per(const WorkerDev& wk) const {
@@ -2182,11 +2191,7 @@ Simulation::Simulation(const Source& src, std::vector<BCEntry> bcs, Params p, in
 Simulation::~Simulation() = default;
 bool Simulation::slab_local() const { return e_->win != nullptr; }
 uint64_t Simulation::n_sites() const { return e_->n_global; }
-uint64_t Simulation::observed_sites() const {
-    uint64_t n = 0;
-    for (auto& o : e_->obs_off_all) n += o.empty() ? 0 : o.back();
-    return n;
-}
+uint64_t Simulation::series_d2h_bytes() const { return e_->series_d2h_bytes(); }
 void Simulation::run(uint64_t n) { e_->run(n); }
 uint64_t Simulation::steps_run() const { return e_->steps_run; }
 double Simulation::step_loop_seconds() const { return e_->loop_s; }

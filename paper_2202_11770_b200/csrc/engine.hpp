@@ -64,7 +64,7 @@ class Simulation {
     ~Simulation();
     bool slab_local() const;  // this rank holds only its window of the domain
     uint64_t n_sites() const; // sites of the whole domain
-    uint64_t observed_sites() const;
+    uint64_t series_d2h_bytes() const;
 
     void run(uint64_t n);
     uint64_t steps_run() const;

@@ -582,8 +582,8 @@ class Simulation:
     def launch_count(self) -> int:
         return int(lib.splbcu_sim_launch_count(self._h))
 
-    def observed_sites(self) -> int:
-        return int(lib.splbcu_sim_observed_sites(self._h))
+    def series_d2h_bytes(self) -> int:
+        return int(lib.splbcu_sim_series_d2h_bytes(self._h))
 
     def snapshot_fields(self) -> np.ndarray:
         out = np.zeros(4 * self.n_sites())
