@@ -156,6 +156,44 @@ inline SparseDomain build_bifurcation(int tr, int br, int tl, int bl, double vox
     return SparseDomain(d);
 }
 
+// Geometry source (include/splbcu.h "geometry sources"): a generator evaluated
+// slice by slice; build() is the whole domain, Simulation::distributed(source,
+// ...) classifies only each rank's slab.
+class Source {
+  public:
+    explicit Source(splbcu_source* h) : h_(h, &splbcu_source_free) {}
+    static Source pipe(int radius, int length, double voxel_size = 1.0) {
+        splbcu_source* s = nullptr;
+        detail::check(splbcu_source_pipe(radius, length, voxel_size, &s));
+        return Source(s);
+    }
+    static Source bifurcation(int tr, int br, int tl, int bl, double voxel_size = 1.0) {
+        splbcu_source* s = nullptr;
+        detail::check(splbcu_source_bifurcation(tr, br, tl, bl, voxel_size, &s));
+        return Source(s);
+    }
+    static Source tree(int root_radius, int root_length, int levels, double radius_ratio = 0.8,
+                       double length_ratio = 0.8, double voxel_size = 1.0) {
+        splbcu_source* s = nullptr;
+        detail::check(splbcu_source_tree(root_radius, root_length, levels, radius_ratio, length_ratio, voxel_size, &s));
+        return Source(s);
+    }
+    static Source channel(int nx, int ny, int nz, double voxel_size = 1.0) {
+        splbcu_source* s = nullptr;
+        detail::check(splbcu_source_channel(nx, ny, nz, voxel_size, &s));
+        return Source(s);
+    }
+    SparseDomain build() const {
+        splbcu_domain* d = nullptr;
+        detail::check(splbcu_source_build(h_.get(), &d));
+        return SparseDomain(d);
+    }
+    splbcu_source* handle() const { return h_.get(); }
+
+  private:
+    std::shared_ptr<splbcu_source> h_;
+};
+
 struct Capture {
     uint64_t step = 0;
     std::vector<double> fields;  // 4 * nSites, (rho, ux, uy, uz) in domain order
@@ -185,40 +223,77 @@ struct DistributionStore {
 
 // engine.hpp:121-205
 class Simulation {
-  public:
-    Simulation(const SparseDomain& domain, const BCSet& bcs, const EngineParams& p) : domain_(domain), params_(p) {
+    // BCSet + EngineParams in C form (the arrays stay alive for the create call)
+    struct CArgs {
         std::vector<std::vector<double>> keep;
         std::vector<splbcu_bc> bc;
-        for (auto& e : bcs.entries) {
-            std::vector<double> t, v;
-            for (auto& n : e.table.nodes) t.push_back(n.first), v.push_back(n.second);
-            keep.push_back(std::move(t));
-            keep.push_back(std::move(v));
-            bc.push_back({int32_t(e.kind), keep[keep.size() - 2].data(), keep.back().data(),
-                          uint32_t(e.table.nodes.size()), e.table.period});
-        }
         splbcu_params c;
-        splbcu_params_default(&c);
-        c.tau = p.tau, c.rho0 = p.rho0, c.dt_s = p.dt_s;
-        c.layout = int32_t(p.layout), c.scheme = int32_t(p.scheme), c.sequence = int32_t(p.sequence);
-        c.workers = p.workers, c.capture_period = p.capture_period, c.observe_iolets = p.observe_iolets;
-        c.exchange_timeout_s = p.exchange_timeout_s;
-        c.halo_mode = p.halo_mode;
-        c.storage = p.storage;
-        c.n_devices = int32_t(p.devices.size());
-        c.device_ids = p.devices.data();
+        CArgs(const BCSet& bcs, const EngineParams& p) {
+            for (auto& e : bcs.entries) {
+                std::vector<double> t, v;
+                for (auto& n : e.table.nodes) t.push_back(n.first), v.push_back(n.second);
+                keep.push_back(std::move(t));
+                keep.push_back(std::move(v));
+                bc.push_back({int32_t(e.kind), keep[keep.size() - 2].data(), keep.back().data(),
+                              uint32_t(e.table.nodes.size()), e.table.period});
+            }
+            splbcu_params_default(&c);
+            c.tau = p.tau, c.rho0 = p.rho0, c.dt_s = p.dt_s;
+            c.layout = int32_t(p.layout), c.scheme = int32_t(p.scheme), c.sequence = int32_t(p.sequence);
+            c.workers = p.workers, c.capture_period = p.capture_period, c.observe_iolets = p.observe_iolets;
+            c.exchange_timeout_s = p.exchange_timeout_s;
+            c.halo_mode = p.halo_mode;
+            c.storage = p.storage;
+            c.n_devices = int32_t(p.devices.size());
+            c.device_ids = p.devices.data();
+        }
+    };
+    Simulation(std::shared_ptr<SparseDomain> d, const EngineParams& p, uint32_t n_io, splbcu_sim* s)
+        : domain_(std::move(d)), params_(p), n_io_(n_io), h_(s) {}
+
+  public:
+    Simulation(const SparseDomain& domain, const BCSet& bcs, const EngineParams& p)
+        : domain_(std::make_shared<SparseDomain>(domain)), params_(p), n_io_(uint32_t(bcs.entries.size())) {
+        CArgs a(bcs, p);
         splbcu_sim* s = nullptr;
-        detail::check(splbcu_sim_create(domain.handle(), bc.data(), uint32_t(bc.size()), &c, &s));
+        detail::check(splbcu_sim_create(domain.handle(), a.bc.data(), uint32_t(a.bc.size()), &a.c, &s));
         h_.reset(s);
+    }
+
+    // One process per GPU (B200; no reference equivalent): this process owns
+    // worker `rank` of p.workers == nranks on p.devices[0]; nccl_id = 128
+    // bytes from nccl_unique_id() on rank 0, broadcast by the caller.
+    static void nccl_unique_id(uint8_t out[128]) { detail::check(splbcu_nccl_unique_id(out)); }
+    static Simulation distributed(const SparseDomain& domain, const BCSet& bcs, const EngineParams& p, int rank,
+                                  int nranks, const uint8_t nccl_id[128]) {
+        CArgs a(bcs, p);
+        splbcu_sim* s = nullptr;
+        detail::check(splbcu_sim_create_dist(domain.handle(), a.bc.data(), uint32_t(a.bc.size()), &a.c, rank,
+                                             nranks, nccl_id, &s));
+        return Simulation(std::make_shared<SparseDomain>(domain), p, uint32_t(bcs.entries.size()), s);
+    }
+    // ... over a geometry source: each rank classifies only its own slab.
+    static Simulation distributed(const Source& src, const BCSet& bcs, const EngineParams& p, int rank, int nranks,
+                                  const uint8_t nccl_id[128]) {
+        CArgs a(bcs, p);
+        splbcu_sim* s = nullptr;
+        detail::check(splbcu_sim_create_dist_source(src.handle(), a.bc.data(), uint32_t(a.bc.size()), &a.c, rank,
+                                                    nranks, nccl_id, &s));
+        return Simulation(nullptr, p, uint32_t(bcs.entries.size()), s);
     }
 
     void run(uint64_t n_steps) { detail::check(splbcu_sim_run(h_.get(), n_steps)); }
     uint64_t steps_run() const { return splbcu_sim_steps_run(h_.get()); }
     double step_loop_seconds() const { return splbcu_sim_step_loop_seconds(h_.get()); }
-    const SparseDomain& domain() const { return domain_; }
+    uint64_t n_sites() const { return splbcu_sim_n_sites(h_.get()); }
+    bool slab_local() const { return splbcu_sim_slab_local(h_.get()) != 0; }
+    const SparseDomain& domain() const {
+        if (!domain_) throw Error("domain(): a slab-local simulation holds no whole domain");
+        return *domain_;
+    }
 
     std::vector<double> snapshot_fields() const {
-        std::vector<double> out(4 * domain_.n_sites());
+        std::vector<double> out(4 * n_sites());
         detail::check(splbcu_sim_snapshot(h_.get(), out.data()));
         return out;
     }
@@ -242,7 +317,7 @@ class Simulation {
         const uint64_t n = splbcu_sim_n_captures(h_.get());
         for (uint64_t k = 0; k < n; ++k) {
             Capture cap;
-            cap.fields.resize(4 * domain_.n_sites());
+            cap.fields.resize(4 * n_sites());
             detail::check(splbcu_sim_capture(h_.get(), k, &cap.step, cap.fields.data()));
             c.captures.push_back(std::move(cap));
         }
@@ -253,8 +328,7 @@ class Simulation {
         IoletSeries s;
         s.rows = splbcu_sim_series_rows(h_.get());
         if (!s.rows) return s;
-        const uint32_t nio = splbcu_domain_n_iolets(domain_.handle());
-        for (uint32_t k = 0; k < nio; ++k) {
+        for (uint32_t k = 0; k < n_io_; ++k) {
             std::vector<double> a(s.rows), b(s.rows), c(s.rows);
             detail::check(splbcu_sim_series(h_.get(), k, a.data(), b.data(), c.data()));
             s.max_speed.push_back(std::move(a));
@@ -268,8 +342,9 @@ class Simulation {
     struct Del {
         void operator()(splbcu_sim* s) const { splbcu_sim_destroy(s); }
     };
-    SparseDomain domain_;
+    std::shared_ptr<SparseDomain> domain_;  // null when slab-local
     EngineParams params_;
+    uint32_t n_io_ = 0;
     std::unique_ptr<splbcu_sim, Del> h_;
 };
 

@@ -1199,13 +1199,15 @@ class Engine {
     // Persistent TMA kernel over the compressed table (mid-group range only).
     template <int T, int S, int B, int H = 2>
     void launch_tmc(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e) {
-        using Lm = PushTmaSmem<T, S, false>;
+        using L0 = PushTmaSmem<T, S, false>;
+        // + the int16 delta planes per stage when H & 8
+        constexpr uint32_t kBytes = S * (L0::kF + ((H & 8) ? uint32_t(kQ - 1) * T * 2 : 0u)) + S * 8;
         static int cfg_dev = -1, resident = 0;
         if (cfg_dev != wk.dev) {
             CK(cudaFuncSetAttribute(lbm_push_tmc<T, S, B, H>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    int(Lm::kBytes)));
+                                    int(kBytes)));
             int per_sm = 0, sms = 0;
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lbm_push_tmc<T, S, B, H>, T, Lm::kBytes));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lbm_push_tmc<T, S, B, H>, T, kBytes));
             CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, wk.dev));
             resident = std::max(1, per_sm) * sms;
             cfg_dev = wk.dev;
@@ -1215,7 +1217,7 @@ class Engine {
         const unsigned grid = unsigned(std::min<uint32_t>(ntiles, uint32_t(resident)));
         Planes19 pl;
         for (int i = 0; i < kQ; ++i) pl.p[i] = wk.f_new() + uint64_t(i) * wk.P;
-        lbm_push_tmc<T, S, B, H><<<grid, T, Lm::kBytes, s>>>(wk.f_old(), wk.f_new(), wk.dtab.get<int16_t>(),
+        lbm_push_tmc<T, S, B, H><<<grid, T, kBytes, s>>>(wk.f_old(), wk.f_new(), wk.dtab.get<int16_t>(),
                                                               wk.gbase.get<uint32_t>(), wk.tab.get<uint32_t>(), wk.P,
                                                               wk.PG, b, e, omega, pl);
     }
@@ -1233,6 +1235,7 @@ class Engine {
                     case 46: launch_tmc<128, 2, 4, 6>(wk, s, b, e); return;
                     case 47: launch_tmc<128, 3, 3, 6>(wk, s, b, e); return;
                     case 48: launch_tmc<96, 2, 5, 6>(wk, s, b, e); return;
+                    case 49: launch_tmc<256, 2, 2, 10>(wk, s, b, e); return;
                     default: launch_tmc<256, 2, 2>(wk, s, b, e); return;
                 }
             }

@@ -342,8 +342,13 @@ lbm_push_tmc(const double* __restrict__ fo, double* __restrict__ fn, const int16
              const uint32_t* __restrict__ gbase, const uint32_t* __restrict__ tab, uint64_t P, uint64_t PG,
              uint32_t begin, uint32_t end, double omega, const __grid_constant__ Planes19 planes) {
     using L = PushTmaSmem<T, S, false>;
+    // kHints & 8: the tile's int16 deltas travel with its f planes (bulk
+    // copies into the same stage) and the group bases are loaded one tile
+    // ahead, so no table load latency is exposed in the direction loop
+    constexpr bool kDS = (kHints & 8) != 0;
+    constexpr uint32_t kStage = L::kF + (kDS ? uint32_t(kQ - 1) * T * 2 : 0u);
     extern __shared__ __align__(128) unsigned char smem[];
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S * L::kStage);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S * kStage);
     const uint32_t base = begin & ~31u;  // warps cover aligned 32-site groups
     const uint32_t ntiles = (end - base + T - 1) / T;
     const uint32_t G = gridDim.x;
@@ -359,14 +364,24 @@ lbm_push_tmc(const double* __restrict__ fo, double* __restrict__ fn, const int16
         const uint32_t tile = blockIdx.x + k * G;
         if (tile >= ntiles) return;
         const int st = int(k % S);
-        unsigned char* buf = smem + st * L::kStage;
+        unsigned char* buf = smem + st * kStage;
         const uint64_t t0 = uint64_t(base) + uint64_t(tile) * T;
-        mbar_expect_tx(&bar[st], L::kStage);
+        mbar_expect_tx(&bar[st], kStage);
 #pragma unroll 1
         for (int i = 0; i < kQ; ++i) bulk_g2s(buf + i * T * 8, fo + uint64_t(i) * P + t0, T * 8, &bar[st], policy);
+        if constexpr (kDS) {
+#pragma unroll 1
+            for (int i = 0; i < kQ - 1; ++i)
+                bulk_g2s(buf + L::kF + i * T * 2, dtab + uint64_t(i) * P + t0, T * 2, &bar[st], policy);
+        }
     };
     if (tid == 0)
         for (uint32_t k = 0; k + 1 < uint32_t(S); ++k) issue(k);
+    auto load_base = [&](uint32_t tile) -> uint32_t {
+        const uint32_t sg = base + tile * T + tid;
+        return (lane < kQ - 1 && tile < ntiles) ? __ldg(gbase + uint64_t(lane) * PG + (sg >> 5)) : 0u;
+    };
+    uint32_t bnext = kDS ? load_base(blockIdx.x) : 0u;
     for (uint32_t k = 0;; ++k) {
         const uint32_t tile = blockIdx.x + k * G;
         if (tile >= ntiles) break;
@@ -375,14 +390,24 @@ lbm_push_tmc(const double* __restrict__ fo, double* __restrict__ fn, const int16
         const uint32_t s = base + tile * T + tid;
         const bool live = s >= begin && s < end;
         int16_t dl[kQ - 1];
+        uint32_t breg;
+        if constexpr (kDS) {
+            breg = bnext;
+            bnext = load_base(tile + G);
+            mbar_wait(&bar[st], (k / S) & 1u);
+            const int16_t* ds = reinterpret_cast<const int16_t*>(smem + st * kStage + L::kF);
 #pragma unroll
-        for (int i = 0; i < kQ - 1; ++i) {
-            if constexpr ((kHints & 4) != 0) dl[i] = live ? __ldg(dtab + uint64_t(i) * P + s) : int16_t(0);
-            else dl[i] = live ? __ldcs(dtab + uint64_t(i) * P + s) : int16_t(0);
+            for (int i = 0; i < kQ - 1; ++i) dl[i] = ds[i * T + tid];
+        } else {
+#pragma unroll
+            for (int i = 0; i < kQ - 1; ++i) {
+                if constexpr ((kHints & 4) != 0) dl[i] = live ? __ldg(dtab + uint64_t(i) * P + s) : int16_t(0);
+                else dl[i] = live ? __ldcs(dtab + uint64_t(i) * P + s) : int16_t(0);
+            }
+            breg = (lane < kQ - 1) ? __ldg(gbase + uint64_t(lane) * PG + (s >> 5)) : 0u;
+            mbar_wait(&bar[st], (k / S) & 1u);
         }
-        const uint32_t breg = (lane < kQ - 1) ? __ldg(gbase + uint64_t(lane) * PG + (s >> 5)) : 0u;
-        mbar_wait(&bar[st], (k / S) & 1u);
-        const double* fs = reinterpret_cast<const double*>(smem + st * L::kStage);
+        const double* fs = reinterpret_cast<const double*>(smem + st * kStage);
         double f[kQ];
 #pragma unroll
         for (int i = 0; i < kQ; ++i) f[i] = fs[i * T + tid];

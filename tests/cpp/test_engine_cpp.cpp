@@ -110,6 +110,22 @@ int main() {
         }
         CHECK(threw);
     }
+    {  // B200 extension: one-rank distributed engine over a geometry source
+       // (slab-local construction) == the in-process engine on the built domain
+        auto p = params(1);
+        p.observe_iolets = true;
+        const Source src = Source::pipe(3, 12);
+        uint8_t id[128];
+        Simulation::nccl_unique_id(id);
+        Simulation a = Simulation::distributed(src, pipe_bcs(0.34, cs2), p, 0, 1, id);
+        Simulation b(src.build(), pipe_bcs(0.34, cs2), p);
+        a.run(30);
+        b.run(30);
+        CHECK(a.slab_local() && !b.slab_local());
+        CHECK(a.n_sites() == b.domain().n_sites());
+        CHECK(a.snapshot_fields() == b.snapshot_fields());
+        CHECK(a.series().flow == b.series().flow);
+    }
     std::printf("%d check(s) failed\n", g_fail);
     return g_fail;
 }
