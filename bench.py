@@ -4,18 +4,25 @@
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                   [--workload c2|c3|c1|c4]
 
-N=1 default workload: config C2 — build_pipe(48, 1400) (10,130,400 sites),
-60-bpm pulsatile velocity inlet (proj/configs/pipe_beat.cfg), outlet p=1/3,
-tau 0.8, dt 5e-4 s.  N>1 (torchrun, one process per GPU, NCCL halo exchange):
-config C3 — a ~1e8-site bifurcating vessel tree, strong scaling.
+Default workload at every N: config C3 — a 1.07e8-site bifurcating vessel
+tree (BASELINE configs[2], the config the metric "MSUPS at 1/2/4/8 B200" is
+quoted on), pressure iolets, strong scaling (the same total work at every N,
+so the driver's per-N values give the strong-scaling efficiency directly).
+N>1: torchrun, one process per GPU, slab decomposition, fused NVLink P2P halo.
+At N=1 the line also carries `secondary`: config C2 — build_pipe(48, 1400)
+(10,130,400 sites), 60-bpm pulsatile velocity inlet (proj/configs/
+pipe_beat.cfg), outlet p=1/3, tau 0.8, dt 5e-4 s — kernel-only value and
+roofline (`--workload c2` makes it the primary line).
 
 value  : sites*steps / device time of the step loop (CUDA events on the
          launching streams, max over ranks), inputs resident in HBM.
 e2e    : the same metric through the public C-ABI call sequence a user makes
          (Simulation.run(1) per step with the iolet series on: per-step BC
          staging H2D and the observation row D2H), host wall clock.
-roofline: the plain-site fused kernel, 376 algorithmic B/site
-         (19*8 read + 19*8 write + 18*4 index), per-launch CUDA events.
+roofline: the bulk plain-site fused kernel (lbm_push_tmc), its own
+         algorithmic bytes (342.25 B/site: 19*8 read + 19*8 write + 18*(2+4/32)
+         compressed index) per launch / CUDA-event launch time; frac_376
+         restates it in SURVEY §8d's 376 B/site.
 cpu_baseline: the unmodified reference (oracle/_ref) on this host's cores,
          bounded sample of the same workload (rank 0, N=1 only).
 """
@@ -176,20 +183,64 @@ def cpu_reference_run(name, steps_cap, seconds, scale, warmup=1):
     return d.n_sites() * steps / T / 1e6, cores, steps, d.n_sites(), desc
 
 
-def load_profile_traffic():
+def load_profile_traffic(name):
+    """DRAM bytes per site of the bulk plain kernel from the committed ncu
+    capture of this workload (profiles/ncu_summary.json), or None."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
             s = json.load(f)
-        return s.get("traffic_bytes_per_site")
+        return s.get(name, {}).get("traffic_bytes_per_site")
     except Exception:
         return None
+
+
+def timed_loop(sim, n, steps, warmup, bps, barrier, max_over_ranks, gpu, name):
+    """W untimed steps, then K steps timed by CUDA events on the launching
+    streams (max over ranks), with per-launch events on the bulk plain kernel
+    and nvidia-smi clocks sampled during the timed region."""
+    sim.run(warmup)
+    barrier()
+    sim.set_kernel_timing(True)
+    k0 = sim.kernel_stats()
+    l0 = sim.launch_count()
+    d0 = sim.device_loop_seconds()
+    with ClockSampler(gpu) as clk:
+        sim.run(steps)  # run() syncs its streams before returning
+    barrier()
+    dev_s = max_over_ranks(sim.device_loop_seconds() - d0)
+    k1 = sim.kernel_stats()
+    launches = sim.launch_count() - l0
+    sim.set_kernel_timing(False)
+    value = n * steps / dev_s / 1e6
+    ks, kl, kn = k1[0] - k0[0], k1[1] - k0[1], k1[2] - k0[2]
+    hbm, src = peaks()
+    traffic = load_profile_traffic(name)
+    # The default kernel reads a compressed table (int16 deltas + a u32 base per
+    # 32 sites): its algorithmic bytes are 304 + 18*(2 + 4/32) = 342.25 B/site
+    # (AA storage: even steps 304, odd steps 376 -> 340 on average).
+    # `achieved`/`frac` use those bytes (the DRAM rate the kernel really
+    # sustains); `achieved_376`/`frac_376` restate it in SURVEY §8d's
+    # 376 B/site (the reference data layout), which can exceed 1.0 because the
+    # kernel moves fewer bytes than that layout.
+    achieved = (kn / kl) * bps / (ks / kl) / 1e9 if kl else None
+    achieved_376 = (kn / kl) * BYTES_PER_SITE / (ks / kl) / 1e9 if kl else None
+    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+            "frac": achieved / hbm if achieved else None,
+            "traffic": (traffic * kn / kl) if (traffic and kl) else None,
+            "peak_source": src, "kernel": "lbm_push_tmc (Inner+Wall fused collide+stream, TMA-pipelined)",
+            "bytes_per_site": bps, "achieved_376": achieved_376,
+            "frac_376": achieved_376 / hbm if achieved_376 else None,
+            "sites_per_launch": kn / kl if kl else None, "avg_launch_ms": ks / kl * 1e3 if kl else None,
+            "kernel_share": ks / dev_s if dev_s else None}
+    return value, dev_s, launches, roof, clk
+
 
 
 def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    name = args.workload or ("c2" if args.gpus == 1 else "c3")
+    name = args.workload or "c3"
     scale = 1.0 if name == "c2" else 0.25
     v, cores, steps, n, desc = cpu_reference_run(name, max(args.steps, 1), 60.0, scale, args.warmup)
     line = {"impl": "reference", "metric": "MSUPS", "value": v, "unit": "MSUPS", "n_gpus": args.gpus,
@@ -211,6 +262,7 @@ def main():
     ap.add_argument("--workload", default=None)
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true", help="N=1: skip the C2 kernel-only line")
     ap.add_argument("--quick", action="store_true", help="kernel-only number (tuning runs)")
     ap.add_argument("--storage", default="two", choices=["two", "aa"],
                     help="two buffers (push) or one buffer in place (AA pattern)")
@@ -229,7 +281,7 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    name = args.workload or ("c2" if world == 1 else "c3")
+    name = args.workload or "c3"
     if world > 1:
         import torch
         import torch.distributed as td
@@ -273,41 +325,9 @@ def main():
         td.all_reduce(t, op=td.ReduceOp.MAX)
         return float(t.item())
 
-    sim.run(args.warmup)
-    barrier()
-    sim.set_kernel_timing(True)
-    k0 = sim.kernel_stats()
-    l0 = sim.launch_count()
-    d0 = sim.device_loop_seconds()
-    with ClockSampler(local) as clk:
-        sim.run(args.steps)  # run() syncs its streams before returning
-    barrier()
-    dev_s = max_over_ranks(sim.device_loop_seconds() - d0)
-    k1 = sim.kernel_stats()
-    launches = sim.launch_count() - l0
-    sim.set_kernel_timing(False)
-    value = n * args.steps / dev_s / 1e6
-    ks, kl, kn = k1[0] - k0[0], k1[1] - k0[1], k1[2] - k0[2]
-    hbm, src = peaks()
-    traffic = load_profile_traffic()
-    # The default kernel reads a compressed table (int16 deltas + a u32 base per
-    # 32 sites): its algorithmic bytes are 304 + 18*(2 + 4/32) = 342.25 B/site
-    # (AA storage: even steps 304, odd steps 376 -> 340 on average).
-    # `achieved`/`frac` use those bytes (the DRAM rate the kernel really
-    # sustains); `achieved_376`/`frac_376` restate it in SURVEY §8d's
-    # 376 B/site (the reference data layout), which can exceed 1.0 because the
-    # kernel moves fewer bytes than that layout.
     bps = 340.0 if args.storage == "aa" else DESIGN_BYTES_PER_SITE
-    achieved = (kn / kl) * bps / (ks / kl) / 1e9 if kl else None
-    achieved_376 = (kn / kl) * BYTES_PER_SITE / (ks / kl) / 1e9 if kl else None
-    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-            "frac": achieved / hbm if achieved else None,
-            "traffic": (traffic * kn / kl) if (traffic and kl) else None,
-            "peak_source": src, "kernel": "lbm_push_tmc (Inner+Wall fused collide+stream, TMA-pipelined)",
-            "bytes_per_site": bps, "achieved_376": achieved_376,
-            "frac_376": achieved_376 / hbm if achieved_376 else None,
-            "sites_per_launch": kn / kl if kl else None, "avg_launch_ms": ks / kl * 1e3 if kl else None,
-            "kernel_share": ks / dev_s if dev_s else None}
+    value, dev_s, launches, roof, clk = timed_loop(sim, n, args.steps, args.warmup, bps, barrier, max_over_ranks, local,
+                                                  name)
 
     if args.quick:
         if rank == 0:
@@ -339,12 +359,25 @@ def main():
                    "D2H, host wall clock"}
     sim.close()
 
+    secondary = None
+    if world == 1 and name != "c2" and not args.no_secondary:
+        # BASELINE configs[1] (the 1e7-site pulsatile pipe), kernel-only
+        d, bcs, p, desc2 = workload(P, "c2")
+        sim = P.Simulation(d, bcs, P.EngineParams(workers=1, devices=[local], storage=storage, **p))
+        n2 = sim.n_sites()
+        v2, dev2, _, roof2, clk2 = timed_loop(sim, n2, max(args.steps, 50), args.warmup, bps, barrier,
+                                              max_over_ranks, local, "c2")
+        sim.close()
+        del d
+        secondary = {"workload": desc2, "sites": n2, "value": v2, "unit": "MSUPS",
+                     "ms_per_step": dev2 / max(args.steps, 50) * 1e3, "roofline": roof2, "clocks": clk2.summary()}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
             v, cores, steps, cn, cdesc = cpu_reference_run(name, 1000, 12.0, 0.1 if name == "c2" else 0.05)
             cpu = {"value": v, "unit": "MSUPS", "cores": cores, "kind": "reference",
-                   "sample": f"{steps} steps of {cdesc} ({cn} sites; L scaled 1/10 of the GPU workload)"}
+                   "sample": f"{steps} steps of {cdesc} ({cn} sites)"}
         except Exception as ex:  # the reference shim may be absent
             cpu = {"value": None, "unit": "MSUPS", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {ex}"}
@@ -356,13 +389,15 @@ def main():
                 "config": {"workload": desc, "sites": n, "parallelism": f"slab decomposition x{world}",
                            "halo": (("NCCL send/recv + PostReceive" if halo_mode == 0 else "fused NVLink P2P stores")
                                     if world > 1 else "none"),
-                           "l2": "inputs (f, table) 3.8 GB per step >> 126 MB L2; no flush needed",
+                           "l2": f"inputs (f, table) {n * 376 / 1e9:.1f} GB per step >> 126 MB L2; no flush needed",
                            "setup_s": round(setup_s, 2),
                            "geometry": ("slab-local (each rank classifies its own slices)" if sim_slab
                                         else "whole domain on every rank")},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(launches),
                 "clocks": clk.summary()}
+        if secondary:
+            line["secondary"] = secondary
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as td

@@ -1223,7 +1223,7 @@ class Engine {
     }
 
     void launch_plain(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia, bool mid) {
-        if (plain_variant >= 40 && plain_variant < 50) {
+        if (plain_variant >= 40 && plain_variant < 60) {
             if (mid && wk.ctab_ok) {
                 switch (plain_variant) {
                     case 40: launch_tmc<256, 2, 2>(wk, s, b, e); return;
@@ -1236,6 +1236,10 @@ class Engine {
                     case 47: launch_tmc<128, 3, 3, 6>(wk, s, b, e); return;
                     case 48: launch_tmc<96, 2, 5, 6>(wk, s, b, e); return;
                     case 49: launch_tmc<256, 2, 2, 10>(wk, s, b, e); return;
+                    case 52: launch_tmc<256, 2, 2, 38>(wk, s, b, e); return;   // 43 + evict-last stores
+                    case 53: launch_tmc<256, 2, 2, 36>(wk, s, b, e); return;   // evict-first loads, evict-last stores
+                    case 54: launch_tmc<256, 2, 2, 102>(wk, s, b, e); return;  // 52 with fraction 0.5
+                    case 55: launch_tmc<256, 2, 2, 100>(wk, s, b, e); return;  // 53 with fraction 0.5
                     default: launch_tmc<256, 2, 2>(wk, s, b, e); return;
                 }
             }

@@ -173,6 +173,14 @@ __device__ __forceinline__ uint64_t evict_first_policy() {
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
+__device__ __forceinline__ uint64_t evict_last_policy(float fraction) {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, %1;" : "=l"(p) : "f"(fraction));
+    return p;
+}
+__device__ __forceinline__ void st_hint(double* p, double v, uint64_t policy) {
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(policy) : "memory");
+}
 __device__ __forceinline__ uint64_t evict_normal_policy() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
@@ -360,6 +368,10 @@ lbm_push_tmc(const double* __restrict__ fo, double* __restrict__ fn, const int16
     }
     __syncthreads();
     const uint64_t policy = (kHints & 2) ? evict_normal_policy() : evict_first_policy();
+    // kHints & 32: f_new stores carry an L2 evict-last hint (a fraction 0.5 of
+    // them with kHints & 64), so partially written sectors stay in L2 until
+    // the slice-later writers complete them
+    const uint64_t spolicy = evict_last_policy((kHints & 64) ? 0.5f : 1.0f);
     auto issue = [&](uint32_t k) {
         const uint32_t tile = blockIdx.x + k * G;
         if (tile >= ntiles) return;
@@ -414,7 +426,11 @@ lbm_push_tmc(const double* __restrict__ fo, double* __restrict__ fn, const int16
         const Macro m = macro_of(f);
         double feq[kQ];
         feq_all(m.rho, m.ux, m.uy, m.uz, feq);
-        if (live) fn[s] = relax(f[0], feq[0], omega);
+        if constexpr ((kHints & 32) != 0) {
+            if (live) st_hint(fn + s, relax(f[0], feq[0], omega), spolicy);
+        } else {
+            if (live) fn[s] = relax(f[0], feq[0], omega);
+        }
 #pragma unroll
         for (int i = 1; i < kQ; ++i) {
             const double fpost = relax(f[i], feq[i], omega);
@@ -431,7 +447,11 @@ lbm_push_tmc(const double* __restrict__ fo, double* __restrict__ fn, const int16
             const bool bb = d == kDeltaBounce;
             const uintptr_t pb = reinterpret_cast<uintptr_t>(bb ? planes.p[inv(i)] : planes.p[i]);
             double* dst = reinterpret_cast<double*>(pb) + (bb ? s : t);
-            if (live) *dst = fpost;
+            if constexpr ((kHints & 32) != 0) {
+                if (live) st_hint(dst, fpost, spolicy);
+            } else {
+                if (live) *dst = fpost;
+            }
         }
         __syncthreads();  // stage st is free for the copy issued next iteration
     }
