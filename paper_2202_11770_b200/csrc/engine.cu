@@ -1201,7 +1201,8 @@ class Engine {
     void launch_tmc(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e) {
         using L0 = PushTmaSmem<T, S, false>;
         // + the int16 delta planes per stage when H & 8
-        constexpr uint32_t kBytes = S * (L0::kF + ((H & 8) ? uint32_t(kQ - 1) * T * 2 : 0u)) + S * 8;
+        constexpr uint32_t kBytes = S * (L0::kF + ((H & 8) ? uint32_t(kQ - 1) * T * 2 : 0u) +
+                                         ((H & 136) == 136 ? uint32_t(kQ - 1) * (T / 32) * 4 : 0u)) + S * 8;
         static int cfg_dev = -1, resident = 0;
         if (cfg_dev != wk.dev) {
             CK(cudaFuncSetAttribute(lbm_push_tmc<T, S, B, H>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1212,7 +1213,7 @@ class Engine {
             resident = std::max(1, per_sm) * sms;
             cfg_dev = wk.dev;
         }
-        const uint32_t base = b & ~31u;
+        const uint32_t base = b & ((H & 136) == 136 ? ~127u : ~31u);
         const uint32_t ntiles = (e - base + T - 1) / T;
         const unsigned grid = unsigned(std::min<uint32_t>(ntiles, uint32_t(resident)));
         Planes19 pl;
@@ -1240,6 +1241,9 @@ class Engine {
                     case 53: launch_tmc<256, 2, 2, 36>(wk, s, b, e); return;   // evict-first loads, evict-last stores
                     case 54: launch_tmc<256, 2, 2, 102>(wk, s, b, e); return;  // 52 with fraction 0.5
                     case 55: launch_tmc<256, 2, 2, 100>(wk, s, b, e); return;  // 53 with fraction 0.5
+                    case 56: launch_tmc<256, 2, 2, 142>(wk, s, b, e); return;  // deltas + group bases by TMA
+                    case 57: launch_tmc<256, 2, 2, 138>(wk, s, b, e); return;  // 56, evict-first bulk loads
+                    case 58: launch_tmc<128, 3, 3, 142>(wk, s, b, e); return;  // 56, 3 stages of 128
                     default: launch_tmc<256, 2, 2>(wk, s, b, e); return;
                 }
             }

@@ -354,10 +354,16 @@ lbm_push_tmc(const double* __restrict__ fo, double* __restrict__ fn, const int16
     // copies into the same stage) and the group bases are loaded one tile
     // ahead, so no table load latency is exposed in the direction loop
     constexpr bool kDS = (kHints & 8) != 0;
-    constexpr uint32_t kStage = L::kF + (kDS ? uint32_t(kQ - 1) * T * 2 : 0u);
+    // kHints & 128 (with 8): the group bases too — 18 bulk copies of T/32 u32
+    // per tile, so the loop body issues no global load at all
+    constexpr bool kGS = kDS && (kHints & 128) != 0;
+    constexpr uint32_t kDOff = L::kF, kGOff = L::kF + uint32_t(kQ - 1) * T * 2;
+    constexpr uint32_t kStage = L::kF + (kDS ? uint32_t(kQ - 1) * T * 2 : 0u) + (kGS ? uint32_t(kQ - 1) * (T / 32) * 4 : 0u);
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S * kStage);
-    const uint32_t base = begin & ~31u;  // warps cover aligned 32-site groups
+    // warps cover aligned 32-site groups; kGS: tiles start on 128 sites so the
+    // group-base copies are 16-byte aligned
+    const uint32_t base = begin & (kGS ? ~127u : ~31u);
     const uint32_t ntiles = (end - base + T - 1) / T;
     const uint32_t G = gridDim.x;
     const uint32_t tid = threadIdx.x;
@@ -384,7 +390,13 @@ lbm_push_tmc(const double* __restrict__ fo, double* __restrict__ fn, const int16
         if constexpr (kDS) {
 #pragma unroll 1
             for (int i = 0; i < kQ - 1; ++i)
-                bulk_g2s(buf + L::kF + i * T * 2, dtab + uint64_t(i) * P + t0, T * 2, &bar[st], policy);
+                bulk_g2s(buf + kDOff + i * T * 2, dtab + uint64_t(i) * P + t0, T * 2, &bar[st], policy);
+        }
+        if constexpr (kGS) {
+#pragma unroll 1
+            for (int i = 0; i < kQ - 1; ++i)
+                bulk_g2s(buf + kGOff + i * (T / 32) * 4, gbase + uint64_t(i) * PG + (t0 >> 5), (T / 32) * 4, &bar[st],
+                         policy);
         }
     };
     if (tid == 0)
@@ -393,7 +405,7 @@ lbm_push_tmc(const double* __restrict__ fo, double* __restrict__ fn, const int16
         const uint32_t sg = base + tile * T + tid;
         return (lane < kQ - 1 && tile < ntiles) ? __ldg(gbase + uint64_t(lane) * PG + (sg >> 5)) : 0u;
     };
-    uint32_t bnext = kDS ? load_base(blockIdx.x) : 0u;
+    uint32_t bnext = (kDS && !kGS) ? load_base(blockIdx.x) : 0u;
     for (uint32_t k = 0;; ++k) {
         const uint32_t tile = blockIdx.x + k * G;
         if (tile >= ntiles) break;
@@ -403,11 +415,18 @@ lbm_push_tmc(const double* __restrict__ fo, double* __restrict__ fn, const int16
         const bool live = s >= begin && s < end;
         int16_t dl[kQ - 1];
         uint32_t breg;
-        if constexpr (kDS) {
+        if constexpr (kGS) {
+            mbar_wait(&bar[st], (k / S) & 1u);
+            const uint32_t* gs = reinterpret_cast<const uint32_t*>(smem + st * kStage + kGOff);
+            breg = lane < kQ - 1 ? gs[lane * (T / 32) + (tid >> 5)] : 0u;
+            const int16_t* ds = reinterpret_cast<const int16_t*>(smem + st * kStage + kDOff);
+#pragma unroll
+            for (int i = 0; i < kQ - 1; ++i) dl[i] = ds[i * T + tid];
+        } else if constexpr (kDS) {
             breg = bnext;
             bnext = load_base(tile + G);
             mbar_wait(&bar[st], (k / S) & 1u);
-            const int16_t* ds = reinterpret_cast<const int16_t*>(smem + st * kStage + L::kF);
+            const int16_t* ds = reinterpret_cast<const int16_t*>(smem + st * kStage + kDOff);
 #pragma unroll
             for (int i = 0; i < kQ - 1; ++i) dl[i] = ds[i * T + tid];
         } else {
