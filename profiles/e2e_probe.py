@@ -4,6 +4,7 @@ Runs the bench workload under torchrun like bench.py and times, per step,
 run(1) with the iolet series off and on, next to the device step time.
     python -m torch.distributed.run --nproc-per-node N profiles/e2e_probe.py [workload]
 """
+import json
 import os
 import sys
 import time
@@ -48,11 +49,22 @@ def main():
         for _ in range(K):
             sim.run(1)
         wall = (time.perf_counter() - t0) / K
-        out[observe] = dict(wall_ms=wall * 1e3, device_ms=(sim.device_loop_seconds() - d0) / K * 1e3,
-                            loop_ms=(sim.step_loop_seconds() - l0) / K * 1e3)
+        rec = dict(wall_ms=wall * 1e3, device_ms=(sim.device_loop_seconds() - d0) / K * 1e3,
+                   loop_ms=(sim.step_loop_seconds() - l0) / K * 1e3)
+        # one run(K): the same steps with a single host round trip
+        if world > 1:
+            td.barrier()
+        t0 = time.perf_counter()
+        sim.run(K)
+        rec["runK_ms_per_step"] = (time.perf_counter() - t0) / K * 1e3
+        if world > 1:
+            allr = [None] * world
+            td.all_gather_object(allr, rec)
+            rec = {k: [round(r[k], 4) for r in allr] for k in rec}
+        out[observe] = rec
         sim.close()
     if rank == 0:
-        print(desc, world, out, flush=True)
+        print(desc, world, json.dumps(out), flush=True)
     if world > 1:
         td.destroy_process_group()
 
