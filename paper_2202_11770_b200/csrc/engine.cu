@@ -366,7 +366,14 @@ class Engine {
     uint32_t n_series_ent = 0, ser_host_ent = 0;
     std::vector<uint32_t> ser_host_k, ser_dev_k, ser_be;  // iolets reduced on host / device; entry ranges
     DevMem ser_w, ser_idx, ser_off, ser_tot, ser_kdev, ser_buf, ser_out;
-    PinnedMem h_series, h_series_raw;
+    // double-buffered so a run's copies never land in the batch the host is
+    // still reducing: the long iolets of run k are reduced on the host while
+    // run k+1's steps execute (lazily, at the next run() or series() call)
+    PinnedMem h_series[2], h_series_raw[2];
+    int ser_next = 0;                 // buffer the next run's copies go to
+    bool ser_pending = false;         // a run's batch awaits host reduction
+    int ser_pend_buf = 0;
+    uint64_t ser_pend_rows = 0;       // series rows once that batch is in
 
     uint64_t series_d2h_bytes() const {
         if (!prm.observe_iolets) return 0;
@@ -1155,7 +1162,7 @@ class Engine {
     // run()'s series: gather this run's rows into series order, reduce the
     // short iolets on the device, and copy results + the long iolets' entries
     // to pinned host memory, on stream s (behind the step loop).
-    void reduce_series_async(WorkerDev& wk, cudaStream_t s, const double* src, uint64_t per) {
+    void reduce_series_async(WorkerDev& wk, cudaStream_t s, const double* src, uint64_t per, int buf) {
         const uint32_t rows = uint32_t(wk.obs_rows), n_io = uint32_t(dom.iolets.size());
         if (!rows || !n_io) return;
         const uint64_t ne = std::max<uint32_t>(n_series_ent, 1);
@@ -1175,10 +1182,10 @@ class Engine {
             ++launches;
         }
         CK(cudaGetLastError());
-        double* h = h_series.reserve<double>(3 * uint64_t(rows) * n_io);
+        double* h = h_series[buf].reserve<double>(3 * uint64_t(rows) * n_io);
         CK(cudaMemcpyAsync(h, o, 3 * uint64_t(rows) * n_io * 8, cudaMemcpyDeviceToHost, s));
         if (ser_host_ent) {
-            double* hr = h_series_raw.reserve<double>(3 * uint64_t(rows) * ser_host_ent);
+            double* hr = h_series_raw[buf].reserve<double>(3 * uint64_t(rows) * ser_host_ent);
             CK(cudaMemcpy2DAsync(hr, 3 * size_t(ser_host_ent) * 8, g, 3 * size_t(ne) * 8, 3 * size_t(ser_host_ent) * 8,
                                  rows, cudaMemcpyDeviceToHost, s));
         }
@@ -1202,11 +1209,15 @@ class Engine {
         using L0 = PushTmaSmem<T, S, false>;
         // + the int16 delta planes per stage when H & 8
         constexpr uint32_t kBytes = S * (L0::kF + ((H & 8) ? uint32_t(kQ - 1) * T * 2 : 0u) +
-                                         ((H & 136) == 136 ? uint32_t(kQ - 1) * (T / 32) * 4 : 0u)) + S * 8;
+                                         ((H & 136) == 136 ? uint32_t(kQ - 1) * (T / 32) * 4 : 0u)) + S * 8 +
+                                    ((H & 1032) == 1024 ? 2 * (uint32_t(kQ - 1) * T * 2 + uint32_t(kQ - 1) * (T / 32) * 4) : 0u);
         static int cfg_dev = -1, resident = 0;
         if (cfg_dev != wk.dev) {
             CK(cudaFuncSetAttribute(lbm_push_tmc<T, S, B, H>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     int(kBytes)));
+            if (const char* c = getenv("SPLBCU_CARVEOUT"))  // tuning: shared-memory share of L1 (percent)
+                CK(cudaFuncSetAttribute(lbm_push_tmc<T, S, B, H>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                        atoi(c)));
             int per_sm = 0, sms = 0;
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lbm_push_tmc<T, S, B, H>, T, kBytes));
             CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, wk.dev));
@@ -1244,6 +1255,8 @@ class Engine {
                     case 56: launch_tmc<256, 2, 2, 142>(wk, s, b, e); return;  // deltas + group bases by TMA
                     case 57: launch_tmc<256, 2, 2, 138>(wk, s, b, e); return;  // 56, evict-first bulk loads
                     case 58: launch_tmc<128, 3, 3, 142>(wk, s, b, e); return;  // 56, 3 stages of 128
+                    case 50: launch_tmc<256, 2, 2, 1030>(wk, s, b, e); return;  // 43 + cp.async table ring
+                    case 51: launch_tmc<128, 2, 4, 1030>(wk, s, b, e); return;  // 50 with 128-site tiles
                     default: launch_tmc<256, 2, 2>(wk, s, b, e); return;
                 }
             }
@@ -1589,7 +1602,7 @@ class Engine {
                     double* dr = obs_gather.reserve<double>(per * uint64_t(nranks));
                     NK(nccl().AllGather(wk.obs_buf.get<double>(), dr, per, ncclDouble, comm, wk.sE));
                     if (dev_series) {
-                        reduce_series_async(wk, wk.sE, dr, per);
+                        reduce_series_async(wk, wk.sE, dr, per, ser_next);
                     } else {
                         double* h = h_gather.reserve<double>(per * uint64_t(nranks));
                         CK(cudaMemcpyAsync(h, dr, per * uint64_t(nranks) * 8, cudaMemcpyDeviceToHost, wk.sE));
@@ -1598,7 +1611,7 @@ class Engine {
                     continue;
                 }
                 if (prm.observe_iolets && dev_series) {
-                    reduce_series_async(wk, wk.sM, wk.obs_buf.get<double>(), 0);
+                    reduce_series_async(wk, wk.sM, wk.obs_buf.get<double>(), 0, ser_next);
                     CK(cudaEventRecord(done[w], wk.sM));
                     continue;
                 }
@@ -1609,6 +1622,8 @@ class Engine {
                 }
                 CK(cudaEventRecord(done[w], wk.sM));
             }
+        // the previous run's long iolets, on the host while these steps run
+        flush_series();
         wait_all(done, n);
         const auto h1 = std::chrono::steady_clock::now();
         double dmax = 0.0;
@@ -1627,7 +1642,14 @@ class Engine {
         dev_loop_s += dmax;
         loop_s += std::chrono::duration<double>(h1 - h0).count();
         steps_run += n;
-        assemble_series();
+        if (prm.observe_iolets && dev_series) {
+            ser_pending = true;
+            ser_pend_buf = ser_next;
+            ser_pend_rows = steps_run + 1;
+            ser_next ^= 1;
+        } else {
+            assemble_series();
+        }
         if (dist) {
             // captures of this run hold this rank's sites only: assemble them
             for (size_t c = 0; c < caps.size(); ++c)
@@ -1925,15 +1947,22 @@ class Engine {
     }
 
     // assemble_series (engine.hpp:602-629): reduce in ascending global order.
+    // Completes the series with the pending run's batch (device path).
+    void flush_series() {
+        if (!ser_pending) return;
+        ser_pending = false;
+        assemble_series();
+    }
+
     void assemble_series() {
         if (!prm.observe_iolets) return;
         const size_t n_io = dom.iolets.size();
         if (dev_series) {
             // (vmax, pressure, flow) per (row, iolet): short iolets reduced on
             // the device by run(); long ones here from their gathered entries
-            const uint64_t first_row = series.rows, rows = steps_run + 1;
-            double* h = h_series.get<double>();
-            const double* raw = h_series_raw.get<double>();
+            const uint64_t first_row = series.rows, rows = ser_pend_rows;
+            double* h = h_series[ser_pend_buf].get<double>();
+            const double* raw = h_series_raw[ser_pend_buf].get<double>();
             for (uint64_t r = 0; r < rows - first_row; ++r)
                 for (uint32_t k : ser_host_k) {
                     const uint32_t b = ser_be[2 * k], e = ser_be[2 * k + 1];
@@ -2227,6 +2256,9 @@ void Simulation::set_f(int w, int which, const double* host) { e_->set_f(w, whic
 ExportedMap Simulation::export_map(int w) { return e_->export_map(w); }
 const Partition& Simulation::partition() const { return e_->part; }
 const std::vector<Capture>& Simulation::captures() const { return e_->caps; }
-const Series& Simulation::series() const { return e_->series; }
+const Series& Simulation::series() const {
+    e_->flush_series();
+    return e_->series;
+}
 
 }  // namespace splbcu
