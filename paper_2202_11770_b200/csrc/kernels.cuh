@@ -439,6 +439,20 @@ lbm_push_tmc(const double* __restrict__ fo, double* __restrict__ fn, const int16
         cp_async_wait_all();
         __syncthreads();
     }
+    // kHints & 4096: register prefetch of the next tile's table, issued after
+    // this tile's divisions (whose slow-path CALL waits for every load in
+    // flight) so it lands during the direction loop and the next TMA wait
+    constexpr bool kPF = !kDS && !kCP && (kHints & 4096) != 0;
+    int16_t dn[kQ - 1];
+    uint32_t bn = 0;
+    auto load_table = [&](uint32_t tile, int16_t* d, uint32_t& b, uint32_t dep) {
+        const uint32_t sn = base + tile * T + tid + dep;
+        const bool ln = tile < ntiles && sn >= begin && sn < end;
+#pragma unroll
+        for (int i = 0; i < kQ - 1; ++i) d[i] = ln ? __ldg(dtab + uint64_t(i) * P + sn) : int16_t(0);
+        b = (lane < kQ - 1 && tile < ntiles) ? __ldg(gbase + uint64_t(lane) * PG + (sn >> 5)) : 0u;
+    };
+    if constexpr (kPF) load_table(blockIdx.x, dn, bn, 0u);
     for (uint32_t k = 0;; ++k) {
         const uint32_t tile = blockIdx.x + k * G;
         if (tile >= ntiles) break;
@@ -448,7 +462,12 @@ lbm_push_tmc(const double* __restrict__ fo, double* __restrict__ fn, const int16
         const bool live = s >= begin && s < end;
         int16_t dl[kQ - 1];
         uint32_t breg;
-        if constexpr (kCP) {
+        if constexpr (kPF) {
+#pragma unroll
+            for (int i = 0; i < kQ - 1; ++i) dl[i] = dn[i];
+            breg = bn;
+            mbar_wait(&bar[st], (k / S) & 1u);
+        } else if constexpr (kCP) {
             issue_table(k + 1);
             cp_async_commit();
             const unsigned char* tb = tring + (k & 1u) * (kTD + kTB);
@@ -485,6 +504,18 @@ lbm_push_tmc(const double* __restrict__ fo, double* __restrict__ fn, const int16
 #pragma unroll
         for (int i = 0; i < kQ; ++i) f[i] = fs[i * T + tid];
         const Macro m = macro_of(f);
+        if constexpr (kPF) {
+            // an always-zero term the compilers cannot fold (a popcount of 32
+            // bits is at most 32) ties the prefetch addresses to the three
+            // quotients, so the loads are not hoisted above the divisions
+            uint32_t pc;
+            asm("popc.b32 %0, %1;"
+                : "=r"(pc)
+                : "r"(uint32_t((__double_as_longlong(m.ux) ^ __double_as_longlong(m.uy) ^
+                                __double_as_longlong(m.uz)) >> 32)));
+            const uint32_t dep = pc >> 6;
+            load_table(tile + G, dn, bn, dep);
+        }
         double feq[kQ];
         feq_all(m.rho, m.ux, m.uy, m.uz, feq);
         if constexpr ((kHints & 32) != 0) {
