@@ -1258,7 +1258,6 @@ class Engine {
                     case 58: launch_tmc<128, 3, 3, 142>(wk, s, b, e); return;  // 56, 3 stages of 128
                     case 50: launch_tmc<256, 2, 2, 1030>(wk, s, b, e); return;  // 43 + cp.async table ring
                     case 59: launch_tmc<256, 2, 2, 4102>(wk, s, b, e); return;  // 43 + table prefetch after the divisions
-                    case 51: launch_tmc<256, 2, 2, 12294>(wk, s, b, e); return;  // 59 + zero numerators skip the division
                     default: launch_tmc<256, 2, 2>(wk, s, b, e); return;
                 }
             }

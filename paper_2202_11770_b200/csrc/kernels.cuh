@@ -503,7 +503,7 @@ lbm_push_tmc(const double* __restrict__ fo, double* __restrict__ fn, const int16
         double f[kQ];
 #pragma unroll
         for (int i = 0; i < kQ; ++i) f[i] = fs[i * T + tid];
-        const Macro m = macro_of<(kHints & 8192) != 0>(f);
+        const Macro m = macro_of(f);
         if constexpr (kPF) {
             // an always-zero term the compilers cannot fold (a popcount of 32
             // bits is at most 32) ties the prefetch addresses to the three

@@ -57,23 +57,9 @@ struct Macro {
     double rho, ux, uy, uz;
 };
 
-// m / rho, IEEE round-to-nearest.  kZeroSkip (device): a zero numerator is
-// answered without the division — ptxas sends quotients near zero through a
-// slow-path subroutine, which at rest (every momentum exactly 0) every warp
-// would take three times per site.  +-0 * rho equals +-0 / rho bit for bit
-// (sign = xor) for every finite nonzero rho; other rho take the division.
-template <bool kZeroSkip>
-SPLB_HD double quot(double m, double rho) {
-#ifdef __CUDA_ARCH__
-    if (kZeroSkip && m == 0.0 && rho != 0.0 && fabs(rho) <= 1.7976931348623157e308) return m * rho;
-#endif
-    return m / rho;
-}
-
 // kernel::macro_of (lattice.hpp:106-119).  Each accumulator runs over the
 // directions in ascending order; zero-coefficient terms are dropped and
 // +-1 coefficients folded (exact, see header).
-template <bool kZeroSkip = false>
 SPLB_HD Macro macro_of(const double* f) {
     double rho = f[0];
 #pragma unroll
@@ -108,7 +94,7 @@ SPLB_HD Macro macro_of(const double* f) {
     mz = mz - f[16];
     mz = mz - f[17];
     mz = mz + f[18];
-    return {rho, quot<kZeroSkip>(mx, rho), quot<kZeroSkip>(my, rho), quot<kZeroSkip>(mz, rho)};
+    return {rho, mx / rho, my / rho, mz / rho};
 }
 
 // kernel::usq_term (lattice.hpp:122-124): 1.5*((ux*ux + uy*uy) + uz*uz)
