@@ -1210,8 +1210,7 @@ class Engine {
         using L0 = PushTmaSmem<T, S, false>;
         // + the int16 delta planes per stage when H & 8
         constexpr uint32_t kBytes = S * (L0::kF + ((H & 8) ? uint32_t(kQ - 1) * T * 2 : 0u) +
-                                         ((H & 136) == 136 ? uint32_t(kQ - 1) * (T / 32) * 4 : 0u)) + S * 8 +
-                                    ((H & 1032) == 1024 ? 2 * (uint32_t(kQ - 1) * T * 2 + uint32_t(kQ - 1) * (T / 32) * 4) : 0u);
+                                         ((H & 136) == 136 ? uint32_t(kQ - 1) * (T / 32) * 4 : 0u)) + S * 8;
         static int cfg_dev = -1, resident = 0;
         if (cfg_dev != wk.dev) {
             CK(cudaFuncSetAttribute(lbm_push_tmc<T, S, B, H>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1256,7 +1255,6 @@ class Engine {
                     case 56: launch_tmc<256, 2, 2, 142>(wk, s, b, e); return;  // deltas + group bases by TMA
                     case 57: launch_tmc<256, 2, 2, 138>(wk, s, b, e); return;  // 56, evict-first bulk loads
                     case 58: launch_tmc<128, 3, 3, 142>(wk, s, b, e); return;  // 56, 3 stages of 128
-                    case 50: launch_tmc<256, 2, 2, 1030>(wk, s, b, e); return;  // 43 + cp.async table ring
                     case 59: launch_tmc<256, 2, 2, 4102>(wk, s, b, e); return;  // 43 + table prefetch after the divisions
                     default: launch_tmc<256, 2, 2>(wk, s, b, e); return;
                 }

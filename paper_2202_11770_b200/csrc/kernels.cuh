@@ -181,11 +181,6 @@ __device__ __forceinline__ uint64_t evict_last_policy(float fraction) {
 __device__ __forceinline__ void st_hint(double* p, double v, uint64_t policy) {
     asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(policy) : "memory");
 }
-__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ uint64_t evict_normal_policy() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
@@ -364,15 +359,8 @@ lbm_push_tmc(const double* __restrict__ fo, double* __restrict__ fn, const int16
     constexpr bool kGS = kDS && (kHints & 128) != 0;
     constexpr uint32_t kDOff = L::kF, kGOff = L::kF + uint32_t(kQ - 1) * T * 2;
     constexpr uint32_t kStage = L::kF + (kDS ? uint32_t(kQ - 1) * T * 2 : 0u) + (kGS ? uint32_t(kQ - 1) * (T / 32) * 4 : 0u);
-    // kHints & 1024: the next tile's deltas and group bases are prefetched into
-    // a 2-deep shared-memory ring with per-thread 4-byte cp.async (LDGSTS)
-    // spread over all threads, a whole tile ahead of use
-    constexpr bool kCP = !kDS && (kHints & 1024) != 0;
-    constexpr uint32_t kTD = uint32_t(kQ - 1) * T * 2, kTB = uint32_t(kQ - 1) * (T / 32) * 4;
-    constexpr uint32_t kTabRing = kCP ? 2 * (kTD + kTB) : 0u;
     extern __shared__ __align__(128) unsigned char smem[];
-    unsigned char* tring = smem + S * kStage;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S * kStage + kTabRing);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S * kStage);
     // warps cover aligned 32-site groups; kGS: tiles start on 128 sites so the
     // group-base copies are 16-byte aligned
     const uint32_t base = begin & (kGS ? ~127u : ~31u);
@@ -418,31 +406,10 @@ lbm_push_tmc(const double* __restrict__ fo, double* __restrict__ fn, const int16
         return (lane < kQ - 1 && tile < ntiles) ? __ldg(gbase + uint64_t(lane) * PG + (sg >> 5)) : 0u;
     };
     uint32_t bnext = (kDS && !kGS) ? load_base(blockIdx.x) : 0u;
-    auto issue_table = [&](uint32_t kk) {
-        const uint32_t tile = blockIdx.x + kk * G;
-        if (tile >= ntiles) return;
-        unsigned char* dst = tring + (kk & 1u) * (kTD + kTB);
-        const uint64_t t0 = uint64_t(base) + uint64_t(tile) * T;
-#pragma unroll
-        for (uint32_t w = tid; w < kTD / 4; w += T) {
-            const uint32_t i = w / (T / 2), off = 2 * (w % (T / 2));
-            cp_async4(dst + (i * T + off) * 2, dtab + uint64_t(i) * P + t0 + off);
-        }
-        for (uint32_t w = tid; w < kTB / 4; w += T) {
-            const uint32_t i = w / (T / 32), g = w % (T / 32);
-            cp_async4(dst + kTD + w * 4, gbase + uint64_t(i) * PG + (t0 >> 5) + g);
-        }
-    };
-    if constexpr (kCP) {
-        issue_table(0);
-        cp_async_commit();
-        cp_async_wait_all();
-        __syncthreads();
-    }
     // kHints & 4096: register prefetch of the next tile's table, issued after
     // this tile's divisions (whose slow-path CALL waits for every load in
     // flight) so it lands during the direction loop and the next TMA wait
-    constexpr bool kPF = !kDS && !kCP && (kHints & 4096) != 0;
+    constexpr bool kPF = !kDS && (kHints & 4096) != 0;
     int16_t dn[kQ - 1];
     uint32_t bn = 0;
     auto load_table = [&](uint32_t tile, int16_t* d, uint32_t& b, uint32_t dep) {
@@ -466,15 +433,6 @@ lbm_push_tmc(const double* __restrict__ fo, double* __restrict__ fn, const int16
 #pragma unroll
             for (int i = 0; i < kQ - 1; ++i) dl[i] = dn[i];
             breg = bn;
-            mbar_wait(&bar[st], (k / S) & 1u);
-        } else if constexpr (kCP) {
-            issue_table(k + 1);
-            cp_async_commit();
-            const unsigned char* tb = tring + (k & 1u) * (kTD + kTB);
-            const int16_t* ds = reinterpret_cast<const int16_t*>(tb);
-#pragma unroll
-            for (int i = 0; i < kQ - 1; ++i) dl[i] = ds[i * T + tid];
-            breg = lane < kQ - 1 ? reinterpret_cast<const uint32_t*>(tb + kTD)[lane * (T / 32) + (tid >> 5)] : 0u;
             mbar_wait(&bar[st], (k / S) & 1u);
         } else if constexpr (kGS) {
             mbar_wait(&bar[st], (k / S) & 1u);
@@ -545,7 +503,6 @@ lbm_push_tmc(const double* __restrict__ fo, double* __restrict__ fn, const int16
                 if (live) *dst = fpost;
             }
         }
-        if constexpr (kCP) cp_async_wait_all();  // next tile's table (this thread's copies)
         __syncthreads();  // stage st is free for the copy issued next iteration
     }
 }
