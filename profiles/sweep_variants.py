@@ -27,10 +27,18 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--scale", type=float, default=1.0)
+    ap.add_argument("--tree", default=None, help="R0,L0,levels: a C3-style tree of another size (workload 'tree')")
     ap.add_argument("--pre", type=int, default=0, help="untimed steps before warm-up (developed flow)")
     args = ap.parse_args()
     for name in args.workload.split(","):
-        d, bcs, p, desc = bench.workload(P, name, args.scale)
+        if name == "tree":
+            r0, l0, lv = (int(x) for x in args.tree.split(","))
+            d = P.build_tree(r0, l0, lv, 0.8, 0.8)
+            ents = [P.BCEntry(P.PRESSURE, P.TimeTable.constant(bench.CS2 * 1.001))]
+            ents += [P.BCEntry(P.PRESSURE, P.TimeTable.constant(bench.CS2 * 0.999)) for _ in range(2 ** lv)]
+            bcs, p = P.BCSet(ents), dict(tau=0.8, dt_s=1.0)
+        else:
+            d, bcs, p, desc = bench.workload(P, name, args.scale)
         for v in args.variants.split(","):
             os.environ["SPLBCU_PLAIN_VARIANT"] = v
             sim = P.Simulation(d, bcs, P.EngineParams(workers=1, devices=[0], **p))
