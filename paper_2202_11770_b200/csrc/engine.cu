@@ -324,6 +324,18 @@ struct WorkerDev {
     uint64_t obs_row_base = 0, obs_rows = 0;
     // kernel timing
     std::vector<cudaEvent_t> tev;
+    // Online choice of the bulk (mid) plain kernel: just-in-time table loads
+    // (mid_pick 0) or the prefetch kernel (1).  Both give the same bits; which
+    // is faster depends on the geometry and on the flow (from rest vs developed,
+    // DESIGN §3), so every kTuneEvery mid launches the next 2 x kTuneReps
+    // launches alternate the two under CUDA events and the faster is kept.
+    static constexpr int kTuneReps = 2;
+    static constexpr uint64_t kTuneEvery = 500;
+    int mid_pick = 0;
+    int tune_phase = 0;         // 0: exploit; k > 0: measuring launch k-1
+    bool tune_pending = false;  // measured, events not read yet
+    uint64_t mid_launches = 0, tune_next = 0;
+    cudaEvent_t tune_ev[2 * kTuneReps][2] = {};
     // 2-D tensor maps over the direction-major planes (per f buffer, table)
     CUtensorMap tm_f[2][2];  // [buffer][box T variant: 0 -> 128 sites, 1 -> 256 sites]
     CUtensorMap tm_t[2];
@@ -740,6 +752,9 @@ class Engine {
             if (!wp) continue;
             cudaSetDevice(wp->dev);
             for (auto e : wp->tev) cudaEventDestroy(e);
+            for (auto& pr : wp->tune_ev)
+                for (auto ev : pr)
+                    if (ev) cudaEventDestroy(ev);
             if (wp->evSend) cudaEventDestroy(wp->evSend);
             if (wp->evMid) cudaEventDestroy(wp->evMid);
             if (wp->evEnd) cudaEventDestroy(wp->evEnd);
@@ -1234,6 +1249,54 @@ class Engine {
                                                               wk.PG, b, e, omega, pl);
     }
 
+    // The bulk plain launch through the online kernel choice (WorkerDev::mid_pick).
+    void launch_mid_tuned(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia) {
+        // prior before the first measurement: the prefetch kernel on large ranges
+        if (wk.mid_launches == 0) wk.mid_pick = (e - b >= kPrefetchMinSites) ? 1 : 0;
+        const bool tune = plain_variant == 0 && wk.ctab_ok && getenv("SPLBCU_NO_AUTOTUNE") == nullptr;
+        if (!tune) {
+            launch_plain(wk, s, b, e, ia, true);
+            ++wk.mid_launches;
+            return;
+        }
+        if (wk.tune_pending) {
+            // read the measurement once its last launch has finished (no sync)
+            const cudaError_t q = cudaEventQuery(wk.tune_ev[2 * WorkerDev::kTuneReps - 1][1]);
+            if (q == cudaSuccess) {
+                float t[2] = {0.f, 0.f};
+                for (int k = 0; k < 2 * WorkerDev::kTuneReps; ++k) {
+                    float ms = 0.f;
+                    CK(cudaEventElapsedTime(&ms, wk.tune_ev[k][0], wk.tune_ev[k][1]));
+                    t[k & 1] += ms;
+                }
+                wk.mid_pick = t[1] < t[0] ? 1 : 0;
+                wk.tune_pending = false;
+                wk.tune_next = wk.mid_launches + WorkerDev::kTuneEvery;
+            } else if (q != cudaErrorNotReady) {
+                CK(q);
+            }
+        }
+        if (wk.tune_phase == 0 && !wk.tune_pending && wk.mid_launches >= wk.tune_next) wk.tune_phase = 1;
+        if (wk.tune_phase > 0) {
+            const int k = wk.tune_phase - 1;
+            for (auto& ev : wk.tune_ev[k])
+                if (!ev) CK(cudaEventCreate(&ev));
+            const int keep = wk.mid_pick;
+            wk.mid_pick = k & 1;
+            CK(cudaEventRecord(wk.tune_ev[k][0], s));
+            launch_plain(wk, s, b, e, ia, true);
+            CK(cudaEventRecord(wk.tune_ev[k][1], s));
+            wk.mid_pick = keep;
+            if (++wk.tune_phase > 2 * WorkerDev::kTuneReps) {
+                wk.tune_phase = 0;
+                wk.tune_pending = true;
+            }
+        } else {
+            launch_plain(wk, s, b, e, ia, true);
+        }
+        ++wk.mid_launches;
+    }
+
     void launch_plain(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia, bool mid) {
         if (plain_variant >= 40 && plain_variant < 60) {
             if (mid && wk.ctab_ok) {
@@ -1300,13 +1363,12 @@ class Engine {
             // default: measured best on B200 — compressed table for the bulk
             // (mid) range, u32 table elsewhere; L2 evict-normal bulk loads and
             // read-only-path table loads (C2 ~93 %, C3 ~89 % of the copy roofline)
-            // Large mid ranges prefetch the next tile's table after the
-            // divisions (the group bases no longer stay in L2: C3 +2.6 % from
-            // rest, +8.5 % in a developed flow); small ones (C2, 1e7 sites,
-            // -5.7 % from rest) keep the just-in-time table loads.
+            // The bulk mid range: just-in-time table loads or the next tile's
+            // table prefetched after the divisions, chosen online
+            // (launch_mid_tuned); both measured best somewhere.
             default:
                 if (mid && wk.ctab_ok) {
-                    if (e - b >= kPrefetchMinSites) launch_tmc<256, 2, 2, 4102>(wk, s, b, e);
+                    if (wk.mid_pick == 1) launch_tmc<256, 2, 2, 4102>(wk, s, b, e);
                     else launch_tmc<256, 2, 2, 6>(wk, s, b, e);
                 } else {
                     launch_tma<256, 2, 2, false, 6>(wk, s, b, e);
@@ -1410,7 +1472,7 @@ class Engine {
                 e1 = wk.tev[wk.tev_used++];
                 CK(cudaEventRecord(e0, s));
             }
-            launch_plain(wk, s, b, e, ia, true);
+            launch_mid_tuned(wk, s, b, e, ia);
             if (kernel_timing) CK(cudaEventRecord(e1, s));
             plain_launches++;
             plain_sites += e - b;
