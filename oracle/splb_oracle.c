@@ -1119,12 +1119,12 @@ int splbcu_sim_run(splbcu_sim* S, uint64_t n) {
     return 0;
 }
 
-int splbcu_nccl_unique_id(uint8_t* o) {
+int splbcu_nccl_unique_id(uint8_t o[128]) {
     (void)o;
     return set_err(SPLBCU_ERR_CONFIG, "oracle: no NCCL path");
 }
 int splbcu_sim_create_dist(const splbcu_domain* a, const splbcu_bc* b, uint32_t c, const splbcu_params* d, int32_t e,
-                           int32_t f, const uint8_t* g, splbcu_sim** h) {
+                           int32_t f, const uint8_t g[128], splbcu_sim** h) {
     (void)a, (void)b, (void)c, (void)d, (void)e, (void)f, (void)g, (void)h;
     return set_err(SPLBCU_ERR_CONFIG, "oracle: no NCCL path");
 }
@@ -1298,7 +1298,7 @@ int splbcu_window_info(const splbcu_domain* d, uint64_t* a, int32_t* b, int32_t*
 }
 void splbcu_source_free(splbcu_source* s) { free(s); }
 int splbcu_sim_create_dist_source(const splbcu_source* a, const splbcu_bc* b, uint32_t c, const splbcu_params* d,
-                                  int32_t e, int32_t f, const uint8_t* g, splbcu_sim** h) {
+                                  int32_t e, int32_t f, const uint8_t g[128], splbcu_sim** h) {
     (void)a, (void)b, (void)c, (void)d, (void)e, (void)f, (void)g, (void)h;
     return set_err(SPLBCU_ERR_CONFIG, "oracle: no NCCL path");
 }
