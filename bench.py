@@ -183,15 +183,26 @@ def cpu_reference_run(name, steps_cap, seconds, scale, warmup=1):
     return d.n_sites() * steps / T / 1e6, cores, steps, d.n_sites(), desc
 
 
-def load_profile_traffic(name):
+BULK_KERNELS = {0: "void lbm_push_tmc<256, 2, 2, 6>", 1: "void lbm_push_tmc<256, 2, 2, 4102>"}
+
+
+def load_profile_traffic(name, kernel=None):
     """DRAM bytes per site of the bulk plain kernel from the committed ncu
-    capture of this workload (profiles/ncu_summary.json), or None."""
+    capture of this workload (profiles/ncu_summary.json), or None.  With
+    `kernel` (the template the engine's online choice launched), an entry of
+    the same workload captured on that kernel ("c3", "c3_jit", ...) is
+    preferred."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
             s = json.load(f)
-        return s.get(name, {}).get("traffic_bytes_per_site")
     except Exception:
-        return None
+        return None, None
+    cands = [k for k in s if k == name or k.startswith(name + "_")]
+    for k in cands:
+        if kernel and s[k].get("kernel") == kernel:
+            return s[k].get("traffic_bytes_per_site"), k
+    e = s.get(name, {})
+    return e.get("traffic_bytes_per_site"), (name if e else None)
 
 
 def timed_loop(sim, n, steps, warmup, bps, barrier, max_over_ranks, gpu, name):
@@ -214,7 +225,8 @@ def timed_loop(sim, n, steps, warmup, bps, barrier, max_over_ranks, gpu, name):
     value = n * steps / dev_s / 1e6
     ks, kl, kn = k1[0] - k0[0], k1[1] - k0[1], k1[2] - k0[2]
     hbm, src = peaks()
-    traffic = load_profile_traffic(name)
+    kernel = BULK_KERNELS.get(sim.bulk_kernel())
+    traffic, traffic_key = load_profile_traffic(name, kernel)
     # The default kernel reads a compressed table (int16 deltas + a u32 base per
     # 32 sites): its algorithmic bytes are 304 + 18*(2 + 4/32) = 342.25 B/site
     # (AA storage: even steps 304, odd steps 376 -> 340 on average).
@@ -228,6 +240,7 @@ def timed_loop(sim, n, steps, warmup, bps, barrier, max_over_ranks, gpu, name):
             "frac": achieved / hbm if achieved else None,
             "traffic": (traffic * kn / kl) if (traffic and kl) else None,
             "peak_source": src, "kernel": "lbm_push_tmc (Inner+Wall fused collide+stream, TMA-pipelined)",
+            "kernel_template": kernel, "traffic_source": traffic_key,
             "bytes_per_site": bps, "achieved_376": achieved_376,
             "frac_376": achieved_376 / hbm if achieved_376 else None,
             "sites_per_launch": kn / kl if kl else None, "avg_launch_ms": ks / kl * 1e3 if kl else None,

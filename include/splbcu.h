@@ -299,6 +299,10 @@ int splbcu_sim_kernel_stats(const splbcu_sim* s, double* plain_seconds,
                             uint64_t* plain_launches, uint64_t* plain_sites);
 /* Number of kernels this handle launched inside run() so far. */
 uint64_t splbcu_sim_launch_count(const splbcu_sim* s);
+/* The kernel the bulk (Inner+Wall mid-range) plain launch uses now, chosen
+ * online: 0 just-in-time table loads, 1 table prefetch after the
+ * divisions, -1 another (forced variant or uncompressed table). */
+int32_t splbcu_sim_bulk_kernel(const splbcu_sim* s);
 /* Bytes the iolet series moves device -> host per step (0 unless
  * observe_iolets): reduced rows plus the entries of iolets the host reduces. */
 uint64_t splbcu_sim_series_d2h_bytes(const splbcu_sim* s);

@@ -454,6 +454,7 @@ uint64_t splbcu_sim_series_d2h_bytes(const splbcu_sim*) { return 0; }
 uint64_t splbcu_sim_n_sites(const splbcu_sim* s) { return s->dom_n; }
 
 uint64_t splbcu_sim_launch_count(const splbcu_sim*) { return 0; }
+int32_t splbcu_sim_bulk_kernel(const splbcu_sim*) { return -1; }
 void splbcu_sim_destroy(splbcu_sim* s) { delete s; }
 
 }  // extern "C"

@@ -1316,6 +1316,10 @@ uint64_t splbcu_sim_launch_count(const splbcu_sim* S) {
     (void)S;
     return 0;
 }
+int32_t splbcu_sim_bulk_kernel(const splbcu_sim* S) {
+    (void)S;
+    return -1;
+}
 void splbcu_sim_destroy(splbcu_sim* S) {
     if (!S) return;
     for (int w = 0; w < S->part->W; ++w) {

@@ -112,6 +112,7 @@ SIGNATURES = [
     ("splbcu_sim_set_kernel_timing", c_int, [_P, c_int]),
     ("splbcu_sim_kernel_stats", c_int, [_P, c_dp, c_u64p, c_u64p]),
     ("splbcu_sim_launch_count", C.c_uint64, [_P]),
+    ("splbcu_sim_bulk_kernel", C.c_int32, [_P]),
     ("splbcu_sim_series_d2h_bytes", C.c_uint64, [_P]),
     ("splbcu_sim_destroy", None, [_P]),
 ]

@@ -608,6 +608,8 @@ int splbcu_sim_kernel_stats(const splbcu_sim* s, double* secs, uint64_t* launche
 
 uint64_t splbcu_sim_launch_count(const splbcu_sim* s) { return s ? s->s->launch_count() : 0; }
 
+int32_t splbcu_sim_bulk_kernel(const splbcu_sim* s) { return s ? s->s->bulk_kernel() : -1; }
+
 void splbcu_sim_destroy(splbcu_sim* s) { delete s; }
 
 }  // extern "C"

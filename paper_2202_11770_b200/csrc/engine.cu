@@ -1249,6 +1249,20 @@ class Engine {
                                                               wk.PG, b, e, omega, pl);
     }
 
+    // Which kernel the bulk (mid) plain range launches now on this process's
+    // first worker: 0 just-in-time table loads (<256,2,2,6>), 1 the prefetch
+    // kernel (<256,2,2,4102>), -1 any other (forced variant, u32 table).
+    int bulk_kernel() const {
+        for (const auto& wp : W) {
+            if (!wp) continue;
+            if (!wp->ctab_ok) return -1;
+            if (plain_variant == 43) return 0;
+            if (plain_variant == 59) return 1;
+            return plain_variant == 0 ? wp->mid_pick : -1;
+        }
+        return -1;
+    }
+
     // The bulk plain launch through the online kernel choice (WorkerDev::mid_pick).
     void launch_mid_tuned(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia) {
         // prior before the first measurement: the prefetch kernel on large ranges
@@ -2310,6 +2324,7 @@ uint64_t Simulation::plain_kernel_launches() const { return e_->plain_launches; 
 uint64_t Simulation::plain_kernel_sites() const { return e_->plain_sites; }
 void Simulation::set_kernel_timing(bool on) { e_->kernel_timing = on; }
 uint64_t Simulation::launch_count() const { return e_->launches; }
+int Simulation::bulk_kernel() const { return e_->bulk_kernel(); }
 void Simulation::snapshot(double* out) { e_->snapshot(out); }
 int Simulation::n_workers() const { return e_->prm.workers; }
 bool Simulation::is_local(int w) const {

@@ -75,6 +75,7 @@ class Simulation {
     uint64_t plain_kernel_sites() const;
     void set_kernel_timing(bool on);
     uint64_t launch_count() const;
+    int bulk_kernel() const;
     void snapshot(double* out4n);
     int n_workers() const;
     bool is_local(int w) const;

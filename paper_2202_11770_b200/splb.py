@@ -582,6 +582,10 @@ class Simulation:
     def launch_count(self) -> int:
         return int(lib.splbcu_sim_launch_count(self._h))
 
+    def bulk_kernel(self) -> int:
+        """0: just-in-time table kernel, 1: prefetch kernel, -1: other."""
+        return int(lib.splbcu_sim_bulk_kernel(self._h))
+
     def series_d2h_bytes(self) -> int:
         return int(lib.splbcu_sim_series_d2h_bytes(self._h))
 
