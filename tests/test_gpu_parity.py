@@ -277,3 +277,27 @@ def test_output_files_match_reference(product, reference, tmp_path):
         outs.append((open(p, "rb").read(), res["sim"].series_csv(1e-3)))
     assert outs[0][0] == outs[1][0]
     assert outs[0][1] == outs[1][1]
+
+
+def test_online_bulk_kernel_choice(product, monkeypatch):
+    """The engine times the two bulk kernels online (every 500 launches) and
+    keeps the faster; switching between them mid-run leaves the bits alone,
+    and splbcu_sim_bulk_kernel reports the choice (forced variants included)."""
+    d = product.build_pipe(16, 128)
+    bcs = cases.make_bcs(product, ("pressure", cases.CS2 * 1.001, cases.CS2 * 0.999))
+
+    def run(variant, steps=1010):
+        if variant is None:
+            monkeypatch.delenv("SPLBCU_PLAIN_VARIANT", raising=False)
+        else:
+            monkeypatch.setenv("SPLBCU_PLAIN_VARIANT", variant)
+        s = product.Simulation(d, bcs, product.EngineParams())
+        s.run(steps)
+        return s.bulk_kernel(), s.snapshot_fields()
+
+    k_auto, f_auto = run(None)
+    k43, f43 = run("43")
+    k59, f59 = run("59")
+    k1, _ = run("1", 2)
+    assert k_auto in (0, 1) and (k43, k59, k1) == (0, 1, -1)
+    assert np.array_equal(f_auto, f43) and np.array_equal(f43, f59)
