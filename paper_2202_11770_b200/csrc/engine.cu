@@ -1263,13 +1263,32 @@ class Engine {
         return -1;
     }
 
+    // Tuning knob (SPLBCU_BULK_CHUNK = sites): the bulk range as several
+    // launches of at most that many sites each, cut at 256-site boundaries.
+    uint64_t bulk_chunk = [] {
+        const char* v = getenv("SPLBCU_BULK_CHUNK");
+        return v ? uint64_t(atoll(v)) : uint64_t(0);
+    }();
+    void launch_bulk(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia) {
+        if (bulk_chunk < 256 || e - b <= bulk_chunk) {
+            launch_plain(wk, s, b, e, ia, true);
+            return;
+        }
+        const uint64_t step = bulk_chunk & ~uint64_t(255);
+        for (uint64_t c = b; c < e;) {
+            const uint64_t c1 = std::min<uint64_t>(e, ((c + step) & ~uint64_t(255)));
+            launch_plain(wk, s, uint32_t(c), uint32_t(c1), ia, true);
+            c = c1;
+        }
+    }
+
     // The bulk plain launch through the online kernel choice (WorkerDev::mid_pick).
     void launch_mid_tuned(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia) {
         // prior before the first measurement: the prefetch kernel on large ranges
         if (wk.mid_launches == 0) wk.mid_pick = (e - b >= kPrefetchMinSites) ? 1 : 0;
         const bool tune = plain_variant == 0 && wk.ctab_ok && getenv("SPLBCU_NO_AUTOTUNE") == nullptr;
         if (!tune) {
-            launch_plain(wk, s, b, e, ia, true);
+            launch_bulk(wk, s, b, e, ia);
             ++wk.mid_launches;
             return;
         }
@@ -1298,7 +1317,7 @@ class Engine {
             const int keep = wk.mid_pick;
             wk.mid_pick = k & 1;
             CK(cudaEventRecord(wk.tune_ev[k][0], s));
-            launch_plain(wk, s, b, e, ia, true);
+            launch_bulk(wk, s, b, e, ia);
             CK(cudaEventRecord(wk.tune_ev[k][1], s));
             wk.mid_pick = keep;
             if (++wk.tune_phase > 2 * WorkerDev::kTuneReps) {
@@ -1306,7 +1325,7 @@ class Engine {
                 wk.tune_pending = true;
             }
         } else {
-            launch_plain(wk, s, b, e, ia, true);
+            launch_bulk(wk, s, b, e, ia);
         }
         ++wk.mid_launches;
     }

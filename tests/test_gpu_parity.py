@@ -301,3 +301,14 @@ def test_online_bulk_kernel_choice(product, monkeypatch):
     k1, _ = run("1", 2)
     assert k_auto in (0, 1) and (k43, k59, k1) == (0, 1, -1)
     assert np.array_equal(f_auto, f43) and np.array_equal(f43, f59)
+
+
+@pytest.mark.parametrize("variant", ["43", "59"])
+def test_chunked_bulk_range_bit_exact(product, golden, variant, monkeypatch):
+    """SPLBCU_BULK_CHUNK (tuning knob) cuts the bulk range into several
+    launches at 256-site boundaries; the bits do not change."""
+    monkeypatch.setenv("SPLBCU_PLAIN_VARIANT", variant)
+    monkeypatch.setenv("SPLBCU_BULK_CHUNK", "700")
+    for key in ("bif_W3_soa_reordered", "pipe_4_20_W4", "blob1_noise_W23"):
+        res = cases.execute_run(product, cases.RUNS[key])
+        assert cases.run_digest(res) == golden["runs"][key], key
