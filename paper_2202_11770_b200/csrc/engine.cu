@@ -1263,21 +1263,28 @@ class Engine {
         return -1;
     }
 
-    // Tuning knob (SPLBCU_BULK_CHUNK = sites): the bulk range as several
-    // launches of at most that many sites each, cut at 256-site boundaries.
+    // The bulk range as several launches of at most kBulkChunk sites each
+    // (equal parts cut at 256-site boundaries).  Measured on B200, C3 tree
+    // 1.07e8 sites from rest: one launch 16,190 MSUPS (just-in-time kernel) /
+    // 16,556 (prefetch); 27e6-site parts 17,663 / 16,844; 13.5e6-site parts
+    // 17,941 / 16,952 (profiles/r01_sweep_chunk.log).  SPLBCU_BULK_CHUNK
+    // overrides the part size (0: one launch).
+    static constexpr uint64_t kBulkChunk = 13500000;
     uint64_t bulk_chunk = [] {
         const char* v = getenv("SPLBCU_BULK_CHUNK");
-        return v ? uint64_t(atoll(v)) : uint64_t(0);
+        return v ? uint64_t(atoll(v)) : kBulkChunk;
     }();
     void launch_bulk(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia) {
         if (bulk_chunk < 256 || e - b <= bulk_chunk) {
             launch_plain(wk, s, b, e, ia, true);
             return;
         }
-        const uint64_t step = bulk_chunk & ~uint64_t(255);
+        const uint64_t parts = (uint64_t(e - b) + bulk_chunk - 1) / bulk_chunk;
+        const uint64_t step = ((uint64_t(e - b) + parts - 1) / parts + 255) & ~uint64_t(255);
         for (uint64_t c = b; c < e;) {
-            const uint64_t c1 = std::min<uint64_t>(e, ((c + step) & ~uint64_t(255)));
+            const uint64_t c1 = std::min<uint64_t>(e, (c + step) & ~uint64_t(255));
             launch_plain(wk, s, uint32_t(c), uint32_t(c1), ia, true);
+            if (c != b) ++launches;  // the step's launch count holds one bulk launch
             c = c1;
         }
     }
