@@ -143,32 +143,40 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(sm)}
 
 
-def cpu_reference_run(name, steps_cap, seconds, scale, warmup=1):
-    """The unmodified reference (oracle/_ref) on all host cores."""
+# Bounded samples of the bench geometries for the reference engine, as
+# (generator, args, description).  The reference has no tree/channel builder:
+# oracle/geometry_gen.py restates the product's voxelisation in numpy and the
+# reference's own classify_sites classifies it (tests/test_host.py pins that
+# this equals the product's build_tree / build_channel), so the reference
+# process never maps the product library.
+REF_SAMPLES = {
+    # reference arm: as large as the reference's setup allows within a few
+    # minutes (its Simulation ctor runs ~5 s per 1e6 sites)
+    "arm": {"c3": ("tree", (48, 240, 6, 0.8, 0.8), "C3-shaped tree sample R0=48 L0=240, 6 levels, 65 pressure iolets"),
+            "c5": ("tree", (32, 480, 7, 0.8, 0.8), "C5-shaped tree sample R0=32 L0=480, 7 levels, 129 pressure iolets"),
+            "c4": ("channel", (192, 192, 300), "C4-shaped channel sample 192x192x300")},
+    # cpu_baseline beside our N=1 line: ~10-30 s of CPU work in total
+    "baseline": {"c3": ("tree", (32, 160, 6, 0.8, 0.8), "C3-shaped tree sample R0=32 L0=160, 6 levels, 65 pressure iolets"),
+                 "c5": ("tree", (32, 320, 7, 0.8, 0.8), "C5-shaped tree sample R0=32 L0=320, 7 levels, 129 pressure iolets"),
+                 "c4": ("channel", (128, 128, 200), "C4-shaped channel sample 128x128x200")},
+}
+
+
+def cpu_reference_run(name, steps_cap, seconds, scale, warmup=1, sample="baseline"):
+    """The unmodified reference (oracle/_ref) on all host cores, on a bounded
+    sample of workload `name`; returns (MSUPS, cores, steps, sites, desc)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import impls
     R = impls.reference()
-    if name in ("c3", "c4", "c5"):
-        # The reference has no tree/channel generator: the product's
-        # generator makes the (bounded) sample, handed over as plain arrays
-        # (SparseDomain fields) — the reference's own engine runs it.
-        import paper_2202_11770_b200 as Pm
-        if name == "c3":
-            dp = Pm.build_tree(32, 160, 6, 0.8, 0.8)
-            desc = "C3-shaped tree sample R0=32 L0=160, 6 levels (product generator -> reference SparseDomain)"
-        elif name == "c5":
-            dp = Pm.build_tree(32, 320, 7, 0.8, 0.8)
-            desc = "C5-shaped tree sample R0=32 L0=320, 7 levels (product generator -> reference SparseDomain)"
-        else:
-            dp = Pm.build_channel(128, 128, 200)
-            desc = "C4-shaped channel sample 128x128x200 (product generator -> reference SparseDomain)"
-        e = dp.export()
-        d = R.SparseDomain.from_arrays(e["coords"], e["types"], e["link_kind"], e["link_iolet"],
-                                       [R.Iolet(i.kind, i.center, i.normal, i.radius) for i in e["iolets"]],
-                                       e["type_ranges"])
+    if name in REF_SAMPLES[sample]:
+        import geometry_gen as G
+        kind, gargs, desc = REF_SAMPLES[sample][name]
+        vox, io = getattr(G, kind)(*gargs)
+        d = G.classify(R, vox, io)
+        del vox
         ents = [R.BCEntry(R.PRESSURE, R.TimeTable.constant(CS2 * 1.001))]
-        ents += [R.BCEntry(R.PRESSURE, R.TimeTable.constant(CS2 * 0.999)) for _ in e["iolets"][1:]]
+        ents += [R.BCEntry(R.PRESSURE, R.TimeTable.constant(CS2 * 0.999)) for _ in io[1:]]
         bcs, p = R.BCSet(ents), dict(tau=0.8, dt_s=1.0)
-        del dp, e
     else:
         d, bcs, p, desc = workload(R, name, scale)
     cores = os.cpu_count() or 1
@@ -186,26 +194,25 @@ def cpu_reference_run(name, steps_cap, seconds, scale, warmup=1):
 BULK_KERNELS = {0: "void lbm_push_tmc<256, 2, 2, 6>", 1: "void lbm_push_tmc<256, 2, 2, 4102>"}
 
 
-def load_profile_traffic(name, kernel=None):
+def load_profile_traffic(name, kernel=None, developed=False):
     """DRAM bytes per site of the bulk plain kernel from the committed ncu
-    capture of this workload (profiles/ncu_summary.json), or None.  With
-    `kernel` (the template the engine's online choice launched), an entry of
-    the same workload captured on that kernel ("c3", "c3_jit", ...) is
-    preferred."""
+    capture of this workload (profiles/ncu_summary.json), or None.  Entries of
+    the same workload ("c3", "c3_jit", "c3_dev_jit", ...) captured on the
+    kernel the engine's online choice launched (`kernel`) and in the same
+    flow state (developed: keys containing "_dev") are preferred."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
             s = json.load(f)
     except Exception:
         return None, None
     cands = [k for k in s if k == name or k.startswith(name + "_")]
-    for k in cands:
-        if kernel and s[k].get("kernel") == kernel:
-            return s[k].get("traffic_bytes_per_site"), k
-    e = s.get(name, {})
-    return e.get("traffic_bytes_per_site"), (name if e else None)
+    cands.sort(key=lambda k: (("_dev" in k) != developed, s[k].get("kernel") != kernel))
+    if cands:
+        return s[cands[0]].get("traffic_bytes_per_site"), cands[0]
+    return None, None
 
 
-def timed_loop(sim, n, steps, warmup, bps, barrier, max_over_ranks, gpu, name):
+def timed_loop(sim, n, steps, warmup, bps, barrier, max_over_ranks, gpu, name, developed=False):
     """W untimed steps, then K steps timed by CUDA events on the launching
     streams (max over ranks), with per-launch events on the bulk plain kernel
     and nvidia-smi clocks sampled during the timed region."""
@@ -226,7 +233,7 @@ def timed_loop(sim, n, steps, warmup, bps, barrier, max_over_ranks, gpu, name):
     ks, kl, kn = k1[0] - k0[0], k1[1] - k0[1], k1[2] - k0[2]
     hbm, src = peaks()
     kernel = BULK_KERNELS.get(sim.bulk_kernel())
-    traffic, traffic_key = load_profile_traffic(name, kernel)
+    traffic, traffic_key = load_profile_traffic(name, kernel, developed)
     # The default kernel reads a compressed table (int16 deltas + a u32 base per
     # 32 sites): its algorithmic bytes are 304 + 18*(2 + 4/32) = 342.25 B/site
     # (AA storage: even steps 304, odd steps 376 -> 340 on average).
@@ -255,7 +262,7 @@ def run_reference_arm(args):
         return
     name = args.workload or "c3"
     scale = 1.0 if name == "c2" else 0.25
-    v, cores, steps, n, desc = cpu_reference_run(name, max(args.steps, 1), 60.0, scale, args.warmup)
+    v, cores, steps, n, desc = cpu_reference_run(name, max(args.steps, 1), 60.0, scale, args.warmup, "arm")
     line = {"impl": "reference", "metric": "MSUPS", "value": v, "unit": "MSUPS", "n_gpus": args.gpus,
             "steps": steps, "warmup": args.warmup, "ms_per_step": n / (v * 1e6) * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -264,6 +271,21 @@ def run_reference_arm(args):
                              "sample": f"{steps} steps of {desc} ({n} sites)"},
             "e2e": {"value": v, "unit": "MSUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def spawn_ranks(n):
+    """`python bench.py --gpus N` outside torchrun: relaunch this command as
+    N ranks (one per GPU, rendezvous on 127.0.0.1), the way the driver's
+    scaling run launches it; rank 0 prints the line."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    rc = subprocess.call(cmd)
+    if rc != 0:
+        raise SystemExit(rc)
 
 
 def main():
@@ -281,17 +303,25 @@ def main():
                     help="two buffers (push) or one buffer in place (AA pattern)")
     ap.add_argument("--halo", default="p2p", choices=["nccl", "p2p"],
                     help="N>1 halo exchange: NCCL send/recv + PostReceive, or fused NVLink P2P stores")
+    ap.add_argument("--develop", type=int, default=3000,
+                    help="untimed steps before the warm-up so the headline is measured in a developed flow "
+                         "(0: from rest); the from-rest number is reported beside it")
     ap.add_argument("--geometry", default="source", choices=["source", "domain"],
                     help="N>1: each rank classifies only its own slab of the generator (source) "
                          "or every rank builds the whole domain")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if args.impl == "reference":
         return run_reference_arm(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # launched without torchrun: spawn one rank per GPU ourselves
+        return spawn_ranks(args.gpus)
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} ranks were launched")
 
     import paper_2202_11770_b200 as P
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     name = args.workload or "c3"
@@ -339,18 +369,43 @@ def main():
         return float(t.item())
 
     bps = 340.0 if args.storage == "aa" else DESIGN_BYTES_PER_SITE
+
+    def develop(sim, steps, chunk=None):
+        """Untimed steps that take the flow from rest to a developed state
+        (chunked so observation buffers stay small)."""
+        left = steps
+        while left > 0:
+            k = min(left, chunk or left)
+            sim.run(k)
+            left -= k
+
+    # from rest (f = equilibrium(rho0, 0) everywhere): secondary number
+    rest = None
+    if args.develop > 0:
+        rv, rdev, _, rroof, rclk = timed_loop(sim, n, args.steps, args.warmup, bps, barrier, max_over_ranks, local,
+                                              name)
+        rest = {"value": rv, "unit": "MSUPS", "ms_per_step": rdev / args.steps * 1e3,
+                "frac": rroof["frac"], "kernel_template": rroof["kernel_template"], "clocks": rclk.summary(),
+                "note": f"the first {args.warmup + args.steps} steps from rest"}
+        develop(sim, args.develop)
+        barrier()
+    state = f"developed flow: {args.develop + (args.warmup + args.steps if rest else 0)} untimed steps first" \
+        if args.develop > 0 else "from rest"
     value, dev_s, launches, roof, clk = timed_loop(sim, n, args.steps, args.warmup, bps, barrier, max_over_ranks, local,
-                                                  name)
+                                                  name, developed=args.develop > 0)
 
     if args.quick:
         if rank == 0:
-            print(json.dumps({"value": value, "roofline": roof, "launches": launches, "clocks": clk.summary()}))
+            print(json.dumps({"value": value, "roofline": roof, "launches": launches, "clocks": clk.summary(),
+                              "from_rest": rest}))
         return
-    # e2e through the public API: run(1) per step with the iolet series on
+    # e2e through the public API: run(1) per step with the iolet series on,
+    # in the same (developed) state as the device-timed number
     sim.close()
     params_e = P.EngineParams(workers=world, devices=[local], observe_iolets=True, halo_mode=halo_mode,
                               storage=storage, **p)
     sim = make_sim(params_e)
+    develop(sim, args.develop, chunk=100)
     for _ in range(args.warmup):
         sim.run(1)
     barrier()
@@ -361,7 +416,6 @@ def main():
     ser = sim.series()  # completes the last row (the host part of the reduction is lazy)
     barrier()
     e2e_s = max_over_ranks(time.perf_counter() - t0)
-    n_obs = sum(1 for _ in ser["flow"])
     # the series row's device -> host bytes (reduced values + the entries of
     # the iolets the host reduces)
     d2h = sim.series_d2h_bytes()
@@ -369,7 +423,7 @@ def main():
            "h2d_bytes_per_step": 8 * len(bcs.entries), "d2h_bytes_per_step": d2h,
            "note": "Simulation.run(1) per step via the C-ABI with the iolet series on: per-step BC values "
                    "H2D, the step, the series row (all-gathered across ranks, reduced in the reference's order) "
-                   "D2H, host wall clock"}
+                   "D2H, host wall clock; " + state}
     sim.close()
 
     secondary = None
@@ -378,11 +432,12 @@ def main():
         d, bcs, p, desc2 = workload(P, "c2")
         sim = P.Simulation(d, bcs, P.EngineParams(workers=1, devices=[local], storage=storage, **p))
         n2 = sim.n_sites()
+        develop(sim, args.develop)
         v2, dev2, _, roof2, clk2 = timed_loop(sim, n2, max(args.steps, 50), args.warmup, bps, barrier,
-                                              max_over_ranks, local, "c2")
+                                              max_over_ranks, local, "c2", developed=args.develop > 0)
         sim.close()
         del d
-        secondary = {"workload": desc2, "sites": n2, "value": v2, "unit": "MSUPS",
+        secondary = {"workload": desc2, "sites": n2, "value": v2, "unit": "MSUPS", "state": state,
                      "ms_per_step": dev2 / max(args.steps, 50) * 1e3, "roofline": roof2, "clocks": clk2.summary()}
 
     cpu = None
@@ -403,12 +458,14 @@ def main():
                            "halo": (("NCCL send/recv + PostReceive" if halo_mode == 0 else "fused NVLink P2P stores")
                                     if world > 1 else "none"),
                            "l2": f"inputs (f, table) {n * 376 / 1e9:.1f} GB per step >> 126 MB L2; no flush needed",
-                           "setup_s": round(setup_s, 2),
+                           "setup_s": round(setup_s, 2), "state": state,
                            "geometry": ("slab-local (each rank classifies its own slices)" if sim_slab
                                         else "whole domain on every rank")},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(launches),
                 "clocks": clk.summary()}
+        if rest:
+            line["from_rest"] = rest
         if secondary:
             line["secondary"] = secondary
         print(json.dumps(line), flush=True)

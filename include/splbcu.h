@@ -281,7 +281,9 @@ const splbcu_partition* splbcu_sim_partition(const splbcu_sim* s);
 uint64_t splbcu_sim_n_captures(const splbcu_sim* s);
 int splbcu_sim_capture(const splbcu_sim* s, uint64_t k, uint64_t* step,
                        double* fields4n);
-/* series() (engine.hpp:145, 70-78): rows and per-iolet columns. */
+/* series() (engine.hpp:145, 70-78): rows and per-iolet columns.  series_rows
+ * completes the pending reduction; on failure it returns 0 and records the
+ * error (splbcu_last_error). */
 uint64_t splbcu_sim_series_rows(const splbcu_sim* s);
 int splbcu_sim_series(const splbcu_sim* s, uint32_t iolet, double* max_speed,
                       double* pressure, double* flow);

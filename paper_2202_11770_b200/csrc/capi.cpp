@@ -470,23 +470,36 @@ double splbcu_sim_step_loop_seconds(const splbcu_sim* s) { return s ? s->s->step
 double splbcu_sim_device_loop_seconds(const splbcu_sim* s) { return s ? s->s->device_loop_seconds() : 0.0; }
 
 int splbcu_sim_snapshot(splbcu_sim* s, double* out) {
-    return guard([&] { s->s->snapshot(out); });
+    return guard([&] {
+        check_ptr(s, "simulation");
+        s->s->snapshot(out);
+    });
 }
 int32_t splbcu_sim_n_workers(const splbcu_sim* s) { return s ? s->s->n_workers() : 0; }
 int32_t splbcu_sim_worker_is_local(const splbcu_sim* s, int32_t w) { return s && s->s->is_local(w) ? 1 : 0; }
 
 int splbcu_sim_store_shape(const splbcu_sim* s, int32_t w, uint32_t* n, uint32_t* shared) {
-    return guard([&] { s->s->store_shape(w, n, shared); });
+    return guard([&] {
+        check_ptr(s, "simulation");
+        s->s->store_shape(w, n, shared);
+    });
 }
 int splbcu_sim_get_f(splbcu_sim* s, int32_t w, int32_t which, double* host) {
-    return guard([&] { s->s->get_f(w, which, host); });
+    return guard([&] {
+        check_ptr(s, "simulation");
+        s->s->get_f(w, which, host);
+    });
 }
 int splbcu_sim_set_f(splbcu_sim* s, int32_t w, int32_t which, const double* host) {
-    return guard([&] { s->s->set_f(w, which, host); });
+    return guard([&] {
+        check_ptr(s, "simulation");
+        s->s->set_f(w, which, host);
+    });
 }
 
 int splbcu_sim_map_shape(const splbcu_sim* s, int32_t w, uint32_t* n_local, uint32_t* shared, uint32_t* n_seg) {
     return guard([&] {
+        check_ptr(s, "simulation");
         uint32_t n = 0, sh = 0;
         s->s->store_shape(w, &n, &sh);
         if (n_local) *n_local = n;
@@ -499,6 +512,7 @@ int splbcu_sim_export_map(splbcu_sim* s, int32_t w, uint32_t* dest, uint8_t* op,
                           uint32_t* recv_dest, uint32_t* send_site, uint8_t* send_dir, int32_t* seg_nb,
                           uint32_t* seg_base, uint32_t* seg_count) {
     return guard([&] {
+        check_ptr(s, "simulation");
         const ExportedMap m = s->s->export_map(w);
         if (dest) std::memcpy(dest, m.dest.data(), m.dest.size() * 4);
         if (op) std::memcpy(op, m.op.data(), m.op.size());
@@ -525,6 +539,7 @@ const splbcu_partition* splbcu_sim_partition(const splbcu_sim* s) {
 uint64_t splbcu_sim_n_captures(const splbcu_sim* s) { return s ? s->s->captures().size() : 0; }
 int splbcu_sim_capture(const splbcu_sim* s, uint64_t k, uint64_t* step, double* fields) {
     return guard([&] {
+        check_ptr(s, "simulation");
         const auto& c = s->s->captures();
         if (k >= c.size()) config_error("capture index out of range");
         if (step) *step = c[k].step;
@@ -532,9 +547,20 @@ int splbcu_sim_capture(const splbcu_sim* s, uint64_t k, uint64_t* step, double* 
     });
 }
 
-uint64_t splbcu_sim_series_rows(const splbcu_sim* s) { return s ? s->s->series().rows : 0; }
+// The series accessor completes the pending host reduction (it can
+// allocate): guarded like every other entry, 0 with the error recorded.
+uint64_t splbcu_sim_series_rows(const splbcu_sim* s) {
+    uint64_t rows = 0;
+    if (guard([&] {
+            check_ptr(s, "simulation");
+            rows = s->s->series().rows;
+        }) != SPLBCU_OK)
+        return 0;
+    return rows;
+}
 int splbcu_sim_series(const splbcu_sim* s, uint32_t k, double* max_speed, double* pressure, double* flow) {
     return guard([&] {
+        check_ptr(s, "simulation");
         const Series& sr = s->s->series();
         if (k >= sr.max_speed.size()) config_error("series: iolet out of range");
         if (max_speed) std::memcpy(max_speed, sr.max_speed[k].data(), sr.max_speed[k].size() * 8);

@@ -324,17 +324,20 @@ struct WorkerDev {
     uint64_t obs_row_base = 0, obs_rows = 0;
     // kernel timing
     std::vector<cudaEvent_t> tev;
+    // end of each step in flight (ring of Engine::kDepth): the run()
+    // watchdog's progress marks
+    std::vector<cudaEvent_t> prog;
     // Online choice of the bulk (mid) plain kernel: just-in-time table loads
     // (mid_pick 0) or the prefetch kernel (1).  Both give the same bits; which
     // is faster depends on the geometry and on the flow (from rest vs developed,
     // DESIGN §3), so every kTuneEvery mid launches the next 2 x kTuneReps
     // launches alternate the two under CUDA events and the faster is kept.
-    static constexpr int kTuneReps = 2;
+    static constexpr int kTuneReps = 3;
     static constexpr uint64_t kTuneEvery = 500;
     int mid_pick = 0;
     int tune_phase = 0;         // 0: exploit; k > 0: measuring launch k-1
     bool tune_pending = false;  // measured, events not read yet
-    uint64_t mid_launches = 0, tune_next = 0;
+    uint64_t mid_launches = 0;
     cudaEvent_t tune_ev[2 * kTuneReps][2] = {};
     // 2-D tensor maps over the direction-major planes (per f buffer, table)
     CUtensorMap tm_f[2][2];  // [buffer][box T variant: 0 -> 128 sites, 1 -> 256 sites]
@@ -509,6 +512,9 @@ class Engine {
 
     void begin(int rank_, int nranks_, const void* nccl_id) {
         dist = nccl_id != nullptr;
+        if (!variant_built(plain_variant))
+            config_error("engine: SPLBCU_PLAIN_VARIANT " + std::to_string(plain_variant) +
+                         " is a tuning variant, not built (make TUNING=1)");
         rank = rank_;
         nranks = nranks_;
         aa_mode = prm.storage == 1;
@@ -738,7 +744,7 @@ class Engine {
     }
 
     ~Engine() {
-        if (p2p_mode && dist && comm) {
+        if (p2p_mode && dist && comm && !failed) {
             try {
                 dist_barrier();  // no neighbour still stores into our buffers
             } catch (...) {
@@ -752,6 +758,7 @@ class Engine {
             if (!wp) continue;
             cudaSetDevice(wp->dev);
             for (auto e : wp->tev) cudaEventDestroy(e);
+            for (auto e : wp->prog) cudaEventDestroy(e);
             for (auto& pr : wp->tune_ev)
                 for (auto ev : pr)
                     if (ev) cudaEventDestroy(ev);
@@ -1214,6 +1221,23 @@ class Engine {
         const char* v = getenv("SPLBCU_PLAIN_VARIANT");
         return v ? atoi(v) : 0;
     }();
+    // online choice of the bulk kernel (off: keep the prior; forced variants never tune)
+    bool autotune = plain_variant == 0 && getenv("SPLBCU_NO_AUTOTUNE") == nullptr;
+    // Resident CTAs per device for a persistent kernel (occupancy x SMs),
+    // with its dynamic shared-memory limit raised once per (kernel, device).
+    std::map<std::pair<const void*, int>, int> resident_;
+    template <class Fn>
+    int resident_ctas(Fn* fn, int dev, int threads, uint32_t smem) {
+        const auto key = std::make_pair(reinterpret_cast<const void*>(fn), dev);
+        const auto it = resident_.find(key);
+        if (it != resident_.end()) return it->second;
+        CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        int per_sm = 0, sms = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem));
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        return resident_[key] = std::max(1, per_sm) * sms;
+    }
+
     template <int T, int B>
     void launch_plain_t(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia) {
         lbm_push<false, T, B><<<unsigned((e - b + T - 1) / T), T, 0, s>>>(
@@ -1226,19 +1250,7 @@ class Engine {
         // + the int16 delta planes per stage when H & 8
         constexpr uint32_t kBytes = S * (L0::kF + ((H & 8) ? uint32_t(kQ - 1) * T * 2 : 0u) +
                                          ((H & 136) == 136 ? uint32_t(kQ - 1) * (T / 32) * 4 : 0u)) + S * 8;
-        static int cfg_dev = -1, resident = 0;
-        if (cfg_dev != wk.dev) {
-            CK(cudaFuncSetAttribute(lbm_push_tmc<T, S, B, H>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    int(kBytes)));
-            if (const char* c = getenv("SPLBCU_CARVEOUT"))  // tuning: shared-memory share of L1 (percent)
-                CK(cudaFuncSetAttribute(lbm_push_tmc<T, S, B, H>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                        atoi(c)));
-            int per_sm = 0, sms = 0;
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lbm_push_tmc<T, S, B, H>, T, kBytes));
-            CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, wk.dev));
-            resident = std::max(1, per_sm) * sms;
-            cfg_dev = wk.dev;
-        }
+        const int resident = resident_ctas(lbm_push_tmc<T, S, B, H>, wk.dev, T, kBytes);
         const uint32_t base = b & ((H & 136) == 136 ? ~127u : ~31u);
         const uint32_t ntiles = (e - base + T - 1) / T;
         const unsigned grid = unsigned(std::min<uint32_t>(ntiles, uint32_t(resident)));
@@ -1263,26 +1275,24 @@ class Engine {
         return -1;
     }
 
-    // The bulk range as several launches of at most kBulkChunk sites each
-    // (equal parts cut at 256-site boundaries).  Measured on B200, C3 tree
-    // 1.07e8 sites from rest: one launch 16,190 MSUPS (just-in-time kernel) /
-    // 16,556 (prefetch); 27e6-site parts 17,663 / 16,844; 13.5e6-site parts
-    // 17,941 / 16,952 (profiles/r01_sweep_chunk.log).  SPLBCU_BULK_CHUNK
-    // overrides the part size (0: one launch).
+    // The bulk range as `parts` launches of about equal size (at most
+    // ~kBulkChunk sites each), cut at absolute 256-site boundaries.  Measured
+    // on B200, C3 tree 1.07e8 sites from rest: one launch 16,190 MSUPS
+    // (just-in-time kernel) / 16,556 (prefetch); 27e6-site parts 17,663 /
+    // 16,844; 13.5e6-site parts 17,941 / 16,952 (profiles/r01_sweep_chunk.log).
+    // SPLBCU_BULK_CHUNK overrides the part size (0: one launch).
     static constexpr uint64_t kBulkChunk = 13500000;
     uint64_t bulk_chunk = [] {
         const char* v = getenv("SPLBCU_BULK_CHUNK");
         return v ? uint64_t(atoll(v)) : kBulkChunk;
     }();
     void launch_bulk(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia) {
-        if (bulk_chunk < 256 || e - b <= bulk_chunk) {
-            launch_plain(wk, s, b, e, ia, true);
-            return;
-        }
-        const uint64_t parts = (uint64_t(e - b) + bulk_chunk - 1) / bulk_chunk;
-        const uint64_t step = ((uint64_t(e - b) + parts - 1) / parts + 255) & ~uint64_t(255);
-        for (uint64_t c = b; c < e;) {
-            const uint64_t c1 = std::min<uint64_t>(e, (c + step) & ~uint64_t(255));
+        const uint64_t n = uint64_t(e - b);
+        const uint64_t parts = bulk_chunk < 256 ? 1 : (n + bulk_chunk - 1) / bulk_chunk;
+        uint64_t c = b;
+        for (uint64_t k = 1; k <= parts; ++k) {
+            const uint64_t c1 = k == parts ? uint64_t(e) : ((uint64_t(b) + k * n / parts) & ~uint64_t(255));
+            if (c1 <= c) continue;
             launch_plain(wk, s, uint32_t(c), uint32_t(c1), ia, true);
             if (c != b) ++launches;  // the step's launch count holds one bulk launch
             c = c1;
@@ -1290,11 +1300,15 @@ class Engine {
     }
 
     // The bulk plain launch through the online kernel choice (WorkerDev::mid_pick).
+    // Measurement windows start at every multiple of kTuneEvery bulk launches
+    // (0, 500, 1000, ...): 2 x kTuneReps launches alternate the two kernels
+    // under CUDA events, each kernel's fastest launch counts (the first launch
+    // of a template also carries its one-time setup), and the faster kernel
+    // is kept from the moment the events have completed.
     void launch_mid_tuned(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia) {
         // prior before the first measurement: the prefetch kernel on large ranges
         if (wk.mid_launches == 0) wk.mid_pick = (e - b >= kPrefetchMinSites) ? 1 : 0;
-        const bool tune = plain_variant == 0 && wk.ctab_ok && getenv("SPLBCU_NO_AUTOTUNE") == nullptr;
-        if (!tune) {
+        if (!autotune || !wk.ctab_ok) {
             launch_bulk(wk, s, b, e, ia);
             ++wk.mid_launches;
             return;
@@ -1303,20 +1317,20 @@ class Engine {
             // read the measurement once its last launch has finished (no sync)
             const cudaError_t q = cudaEventQuery(wk.tune_ev[2 * WorkerDev::kTuneReps - 1][1]);
             if (q == cudaSuccess) {
-                float t[2] = {0.f, 0.f};
+                float t[2] = {3.4e38f, 3.4e38f};
                 for (int k = 0; k < 2 * WorkerDev::kTuneReps; ++k) {
                     float ms = 0.f;
                     CK(cudaEventElapsedTime(&ms, wk.tune_ev[k][0], wk.tune_ev[k][1]));
-                    t[k & 1] += ms;
+                    t[k & 1] = std::min(t[k & 1], ms);
                 }
                 wk.mid_pick = t[1] < t[0] ? 1 : 0;
                 wk.tune_pending = false;
-                wk.tune_next = wk.mid_launches + WorkerDev::kTuneEvery;
             } else if (q != cudaErrorNotReady) {
                 CK(q);
             }
         }
-        if (wk.tune_phase == 0 && !wk.tune_pending && wk.mid_launches >= wk.tune_next) wk.tune_phase = 1;
+        if (wk.tune_phase == 0 && !wk.tune_pending && wk.mid_launches % WorkerDev::kTuneEvery == 0)
+            wk.tune_phase = 1;
         if (wk.tune_phase > 0) {
             const int k = wk.tune_phase - 1;
             for (auto& ev : wk.tune_ev[k])
@@ -1337,32 +1351,70 @@ class Engine {
         ++wk.mid_launches;
     }
 
+    // The plain (Inner+Wall) range.  Built kernels: the bulk mid range runs
+    // the compressed-table TMA kernel, just-in-time table loads (<256,2,2,6>)
+    // or the next tile's table prefetched after the divisions
+    // (<256,2,2,4102>), chosen online (launch_mid_tuned; both measured best
+    // somewhere); edge ranges and workers without a compressed
+    // table run the u32-table TMA kernel.  Forced: SPLBCU_PLAIN_VARIANT 43 /
+    // 59 (one bulk kernel), 24 (u32 table everywhere).  The measured-slower
+    // launch shapes and hints of the tuning sweeps are built with
+    // `make TUNING=1` only (profiles/sweep_variants.py).
+    static bool variant_built(int v) {
+#ifdef SPLBCU_TUNING
+        (void)v;
+        return true;
+#else
+        return v == 0 || v == 24 || v == 43 || v == 59 || v == 60;
+#endif
+    }
     void launch_plain(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia, bool mid) {
+#ifdef SPLBCU_TUNING
+        if (launch_tuning_variant(wk, s, b, e, ia, mid)) return;
+#endif
+        if (plain_variant == 24) return launch_tma<256, 2, 2, false, 2>(wk, s, b, e);
+        if (mid && wk.ctab_ok) {
+            const bool pf = plain_variant == 59 || (plain_variant == 0 && wk.mid_pick == 1);
+            if (pf) launch_tmc<256, 2, 2, 4102>(wk, s, b, e);
+            else launch_tmc<256, 2, 2, 6>(wk, s, b, e);
+        } else {
+            launch_tma<256, 2, 2, false, 6>(wk, s, b, e);
+        }
+    }
+
+#ifdef SPLBCU_TUNING
+    // Tuning sweep variants (SPLBCU_PLAIN_VARIANT; measured slower than the
+    // defaults, profiles/r01_sweep_*.log).  Returns false for the built-in ones.
+    bool launch_tuning_variant(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia, bool mid) {
+        if (plain_variant == 0 || plain_variant == 24 || plain_variant == 43 || plain_variant == 59 ||
+            plain_variant == 60)
+            return false;
         if (plain_variant >= 40 && plain_variant < 60) {
             if (mid && wk.ctab_ok) {
                 switch (plain_variant) {
-                    case 40: launch_tmc<256, 2, 2>(wk, s, b, e); return;
-                    case 41: launch_tmc<128, 2, 4>(wk, s, b, e); return;
-                    case 42: launch_tmc<128, 2, 3>(wk, s, b, e); return;
-                    case 43: launch_tmc<256, 2, 2, 6>(wk, s, b, e); return;
-                    case 44: launch_tmc<256, 2, 2, 0>(wk, s, b, e); return;
-                    case 45: launch_tmc<192, 2, 3, 6>(wk, s, b, e); return;
-                    case 46: launch_tmc<128, 2, 4, 6>(wk, s, b, e); return;
-                    case 47: launch_tmc<128, 3, 3, 6>(wk, s, b, e); return;
-                    case 48: launch_tmc<96, 2, 5, 6>(wk, s, b, e); return;
-                    case 49: launch_tmc<256, 2, 2, 10>(wk, s, b, e); return;
-                    case 52: launch_tmc<256, 2, 2, 38>(wk, s, b, e); return;   // 43 + evict-last stores
-                    case 53: launch_tmc<256, 2, 2, 36>(wk, s, b, e); return;   // evict-first loads, evict-last stores
-                    case 54: launch_tmc<256, 2, 2, 102>(wk, s, b, e); return;  // 52 with fraction 0.5
-                    case 55: launch_tmc<256, 2, 2, 100>(wk, s, b, e); return;  // 53 with fraction 0.5
-                    case 56: launch_tmc<256, 2, 2, 142>(wk, s, b, e); return;  // deltas + group bases by TMA
-                    case 57: launch_tmc<256, 2, 2, 138>(wk, s, b, e); return;  // 56, evict-first bulk loads
-                    case 58: launch_tmc<128, 3, 3, 142>(wk, s, b, e); return;  // 56, 3 stages of 128
-                    case 59: launch_tmc<256, 2, 2, 4102>(wk, s, b, e); return;  // 43 + table prefetch after the divisions
-                    default: launch_tmc<256, 2, 2>(wk, s, b, e); return;
+                    case 40: launch_tmc<256, 2, 2>(wk, s, b, e); return true;
+                    case 41: launch_tmc<128, 2, 4>(wk, s, b, e); return true;
+                    case 42: launch_tmc<128, 2, 3>(wk, s, b, e); return true;
+                    case 43: launch_tmc<256, 2, 2, 6>(wk, s, b, e); return true;
+                    case 44: launch_tmc<256, 2, 2, 0>(wk, s, b, e); return true;
+                    case 45: launch_tmc<192, 2, 3, 6>(wk, s, b, e); return true;
+                    case 46: launch_tmc<128, 2, 4, 6>(wk, s, b, e); return true;
+                    case 47: launch_tmc<128, 3, 3, 6>(wk, s, b, e); return true;
+                    case 48: launch_tmc<96, 2, 5, 6>(wk, s, b, e); return true;
+                    case 49: launch_tmc<256, 2, 2, 10>(wk, s, b, e); return true;
+                    case 52: launch_tmc<256, 2, 2, 38>(wk, s, b, e); return true;   // 43 + evict-last stores
+                    case 53: launch_tmc<256, 2, 2, 36>(wk, s, b, e); return true;   // evict-first loads, evict-last stores
+                    case 54: launch_tmc<256, 2, 2, 102>(wk, s, b, e); return true;  // 52 with fraction 0.5
+                    case 55: launch_tmc<256, 2, 2, 100>(wk, s, b, e); return true;  // 53 with fraction 0.5
+                    case 56: launch_tmc<256, 2, 2, 142>(wk, s, b, e); return true;  // deltas + group bases by TMA
+                    case 57: launch_tmc<256, 2, 2, 138>(wk, s, b, e); return true;  // 56, evict-first bulk loads
+                    case 58: launch_tmc<128, 3, 3, 142>(wk, s, b, e); return true;  // 56, 3 stages of 128
+                    case 59: launch_tmc<256, 2, 2, 4102>(wk, s, b, e); return true;  // 43 + table prefetch after the divisions
+                    default: launch_tmc<256, 2, 2>(wk, s, b, e); return true;
                 }
             }
-            return launch_tma<256, 2, 2, false, 2>(wk, s, b, e);
+            launch_tma<256, 2, 2, false, 2>(wk, s, b, e);
+            return true;
         }
         switch (plain_variant) {
             case 1: launch_plain_t<256, 1>(wk, s, b, e, ia); break;
@@ -1399,24 +1451,13 @@ class Engine {
             case 35: launch_ws<128, 3, 3, false>(wk, s, b, e); break;
             case 36: launch_ws<128, 4, 2, false>(wk, s, b, e); break;
             case 37: launch_plain_t<128, 4>(wk, s, b, e, ia); break;
-            // default: measured best on B200 (C2: 86% of the HBM copy roofline)
-            // default: measured best on B200 — compressed table for the bulk
-            // (mid) range, u32 table elsewhere; L2 evict-normal bulk loads and
-            // read-only-path table loads (C2 ~93 %, C3 ~89 % of the copy roofline)
-            // The bulk mid range: just-in-time table loads or the next tile's
-            // table prefetched after the divisions, chosen online
-            // (launch_mid_tuned); both measured best somewhere.
-            default:
-                if (mid && wk.ctab_ok) {
-                    if (wk.mid_pick == 1) launch_tmc<256, 2, 2, 4102>(wk, s, b, e);
-                    else launch_tmc<256, 2, 2, 6>(wk, s, b, e);
-                } else {
-                    launch_tma<256, 2, 2, false, 6>(wk, s, b, e);
-                }
-                break;
+            default: return false;
         }
+        return true;
     }
+#endif
 
+#ifdef SPLBCU_TUNING
     // Warp-specialised 2-D TMA launch (producer warp + T/32 consumer warps).
     template <int T, int S, int B, bool TS>
     void launch_ws(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e) {
@@ -1425,16 +1466,7 @@ class Engine {
             IoletArgs ia{};
             return launch_plain_t<128, 4>(wk, s, b, e, ia);
         }
-        static int cfg_dev = -1, resident = 0;
-        if (cfg_dev != wk.dev) {
-            CK(cudaFuncSetAttribute(lbm_push_ws<T, S, B, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    int(Lm::kBytes)));
-            int per_sm = 0, sms = 0;
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lbm_push_ws<T, S, B, TS>, T + 32, Lm::kBytes));
-            CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, wk.dev));
-            resident = std::max(1, per_sm) * sms;
-            cfg_dev = wk.dev;
-        }
+        const int resident = resident_ctas(lbm_push_ws<T, S, B, TS>, wk.dev, T + 32, Lm::kBytes);
         const int v = T == 128 ? 0 : 1;
         const uint32_t base = b & ~3u;
         const uint32_t ntiles = (e - base + T - 1) / T;
@@ -1442,22 +1474,13 @@ class Engine {
         lbm_push_ws<T, S, B, TS><<<grid, T + 32, Lm::kBytes, s>>>(wk.tm_f[wk.old][v], wk.tm_t[v], wk.f_new(),
                                                                    wk.tab.get<uint32_t>(), wk.P, b, e, omega);
     }
+#endif
 
     // Persistent TMA-pipelined launch: grid = resident CTAs (occupancy x SMs).
     template <int T, int S, int B, bool TS = true, int H = 0, bool P2 = false>
     void launch_tma(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const HaloArgs& halo = HaloArgs{}) {
         using Lm = PushTmaSmem<T, S, TS>;
-        static int cfg_dev = -1, resident = 0;
-        if (cfg_dev != wk.dev) {
-            CK(cudaFuncSetAttribute(lbm_push_tma<T, S, B, TS, H, P2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    int(Lm::kBytes)));
-            int per_sm = 0, sms = 0;
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lbm_push_tma<T, S, B, TS, H, P2>, T,
-                                                             Lm::kBytes));
-            CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, wk.dev));
-            resident = std::max(1, per_sm) * sms;
-            cfg_dev = wk.dev;
-        }
+        const int resident = resident_ctas(lbm_push_tma<T, S, B, TS, H, P2>, wk.dev, T, Lm::kBytes);
         const uint32_t base = b & ~3u;
         const uint32_t ntiles = (e - base + T - 1) / T;
         const unsigned grid = unsigned(std::min<uint32_t>(ntiles, uint32_t(resident)));
@@ -1652,6 +1675,7 @@ class Engine {
     }
 
     void run(uint64_t n) {
+        if (failed) runtime_error("engine: an exchange failure left this simulation unusable");
         const size_t caps_before = caps.size();
         const bool first_run = steps_run == 0;
         prepare_records(n);
@@ -1692,8 +1716,15 @@ class Engine {
                 CK(cudaEventRecord(t0[w], W[w]->sM));
                 CK(cudaStreamWaitEvent(W[w]->sE, t0[w], 0));
             }
+        last_progress = std::chrono::steady_clock::now();
         try {
-            for (uint64_t k = 0; k < n; ++k) step_once(k, k * n_io);
+            for (uint64_t k = 0; k < n; ++k) {
+                // at most kDepth steps in flight: the host waits for step
+                // k - kDepth first, under the exchange watchdog
+                if (k >= kDepth) wait_step(k - kDepth);
+                step_once(k, k * n_io);
+                mark_step(k);
+            }
         } catch (const Error& e) {
             if (e.kind == ErrKind::Comm) throw Error(ErrKind::Comm, "worker " + std::to_string(rank) + ": " + e.what());
             throw;
@@ -1733,7 +1764,13 @@ class Engine {
             }
         // the previous run's long iolets, on the host while these steps run
         flush_series();
-        wait_all(done, n);
+        try {
+            for (uint64_t k = n > kDepth ? n - kDepth : 0; k < n; ++k) wait_step(k);
+            wait_all(done);
+        } catch (const Error& e) {
+            if (e.kind == ErrKind::Comm) throw Error(ErrKind::Comm, "worker " + std::to_string(rank) + ": " + e.what());
+            throw;
+        }
         const auto h1 = std::chrono::steady_clock::now();
         double dmax = 0.0;
         for (size_t w = 0; w < W.size(); ++w)
@@ -1767,40 +1804,93 @@ class Engine {
         }
     }
 
-    // Waits for the step loop; in dist mode polls for async comm errors and
-    // applies the reference's exchange timeout (engine.hpp:92-101), scaled to
-    // the run: exchange_timeout_s * (1 + n_steps / 100) for the whole run.
-    void wait_all(const std::vector<cudaEvent_t>& ev, uint64_t n_steps) {
-        const double limit = prm.exchange_timeout_s * (1.0 + double(n_steps) / 100.0);
-        const auto start = std::chrono::steady_clock::now();
-        for (size_t w = 0; w < W.size(); ++w) {
-            if (!W[w]) continue;
-            CK(cudaSetDevice(W[w]->dev));
-            if (!dist) {
-                CK(cudaEventSynchronize(ev[w]));
-                continue;
+    // ---- progress watchdog (Mailbox::take, engine.hpp:92-101) ----------------
+    // The reference fails a worker whose neighbour's message does not arrive
+    // within exchange_timeout_s.  Here every step ends with a progress event
+    // per local worker; the host keeps at most kDepth steps in flight and, in
+    // dist mode, fails the run when no step has completed for
+    // exchange_timeout_s (a dead or stuck neighbour), checking NCCL's
+    // asynchronous errors while it waits.
+    static constexpr uint64_t kDepth = 64;
+    bool failed = false;  // an exchange failure left the streams unusable
+    std::chrono::steady_clock::time_point last_progress;
+
+    void mark_step(uint64_t k) {
+        for (auto& wp : W) {
+            if (!wp) continue;
+            WorkerDev& wk = *wp;
+            CK(cudaSetDevice(wk.dev));
+            if (wk.prog.empty()) {
+                wk.prog.resize(kDepth, nullptr);
+                for (auto& ev : wk.prog) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
             }
-            for (;;) {
-                cudaError_t q = cudaEventQuery(ev[w]);
-                if (q == cudaSuccess) break;
-                if (q != cudaErrorNotReady) CK(q);
-                ncclResult_t ar = ncclSuccess;
-                NK(nccl().CommGetAsyncError(comm, &ar));
-                if (ar != ncclSuccess && ar != ncclInProgress)
-                    fail(ErrKind::Comm, std::string("exchange failure: NCCL async error: ") + nccl().GetErrorString(ar));
-                const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - start).count();
-                if (el > limit) {
-                    nccl().CommAbort(comm);
-                    comm = nullptr;
-                    const int nb = W[w]->segs.empty() ? -1 : W[w]->segs.front().nb;
-                    fail(ErrKind::Comm, "exchange failure: worker " + std::to_string(w) +
-                                            " timed out waiting for neighbor " + std::to_string(nb));
+            CK(cudaEventRecord(wk.prog[k % kDepth], wk.sM));
+        }
+    }
+
+    void wait_step(uint64_t k) {
+        for (size_t w = 0; w < W.size(); ++w)
+            if (W[w]) wait_event(int(w), W[w]->prog[k % kDepth]);
+    }
+
+    void wait_event(int w, cudaEvent_t ev) {
+        CK(cudaSetDevice(W[size_t(w)]->dev));
+        if (!dist) {
+            CK(cudaEventSynchronize(ev));
+            return;
+        }
+        for (int spins = 0;; ++spins) {
+            const cudaError_t q = cudaEventQuery(ev);
+            if (q == cudaSuccess) {
+                last_progress = std::chrono::steady_clock::now();
+                return;
+            }
+            if (q != cudaErrorNotReady) CK(q);
+            ncclResult_t ar = ncclSuccess;
+            NK(nccl().CommGetAsyncError(comm, &ar));
+            if (ar != ncclSuccess && ar != ncclInProgress)
+                fail(ErrKind::Comm, std::string("exchange failure: NCCL async error: ") + nccl().GetErrorString(ar));
+            const double el =
+                std::chrono::duration<double>(std::chrono::steady_clock::now() - last_progress).count();
+            if (el > prm.exchange_timeout_s) exchange_timeout(w);
+            if (spins < 2000) std::this_thread::yield();
+            else std::this_thread::sleep_for(std::chrono::microseconds(50));
+        }
+    }
+
+    // No progress for exchange_timeout_s: abort the communicator, release the
+    // streams blocked on flag words (so teardown does not wait on them), and
+    // report the neighbour whose halo is missing (the lowest halo_in flag).
+    [[noreturn]] void exchange_timeout(int w) {
+        failed = true;
+        WorkerDev& wk = *W[size_t(w)];
+        int nb = wk.segs.empty() ? -1 : wk.segs.front().nb;
+        if (comm) nccl().CommAbort(comm);
+        comm = nullptr;
+        if (wk.flags.p) {
+            cudaStream_t t = nullptr;
+            if (cudaStreamCreateWithFlags(&t, cudaStreamNonBlocking) == cudaSuccess) {
+                const size_t nf = 2 * size_t(prm.workers);
+                std::vector<uint32_t> h(nf, 0);
+                if (cudaMemcpyAsync(h.data(), wk.flags.p, nf * 4, cudaMemcpyDeviceToHost, t) == cudaSuccess &&
+                    cudaStreamSynchronize(t) == cudaSuccess) {
+                    uint32_t lo = UINT32_MAX;
+                    for (const Seg& sg : wk.segs)
+                        if (h[size_t(sg.nb)] < lo) lo = h[size_t(sg.nb)], nb = sg.nb;
                 }
-                // spin (yielding) for short runs, then back off
-                if (el < 0.02) std::this_thread::yield();
-                else std::this_thread::sleep_for(std::chrono::microseconds(50));
+                cudaMemsetAsync(wk.flags.p, 0xFF, nf * 4, t);
+                cudaStreamSynchronize(t);
+                cudaStreamDestroy(t);
             }
         }
+        fail(ErrKind::Comm, "exchange failure: worker " + std::to_string(w) + " timed out waiting for neighbor " +
+                                std::to_string(nb));
+    }
+
+    // Waits for this run's trailing work (observation copies) under the same watchdog.
+    void wait_all(const std::vector<cudaEvent_t>& ev) {
+        for (size_t w = 0; w < W.size(); ++w)
+            if (W[w]) wait_event(int(w), ev[w]);
     }
 
     // advance_one (engine.hpp:330-363) for every local worker.
@@ -1808,41 +1898,25 @@ class Engine {
     template <int T, int S, int B>
     void launch_aa_even_tma(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e) {
         using Lm = PushTmaSmem<T, S, false>;
-        static int cfg_dev = -1, resident = 0;
-        if (cfg_dev != wk.dev) {
-            CK(cudaFuncSetAttribute(lbm_aa_even_tma<T, S, B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    int(Lm::kBytes)));
-            int per_sm = 0, sms = 0;
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lbm_aa_even_tma<T, S, B>, T, Lm::kBytes));
-            CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, wk.dev));
-            resident = std::max(1, per_sm) * sms;
-            cfg_dev = wk.dev;
-        }
+        const int resident = resident_ctas(lbm_aa_even_tma<T, S, B>, wk.dev, T, Lm::kBytes);
         const uint32_t base = b & ~3u;
         const uint32_t ntiles = (e - base + T - 1) / T;
         const unsigned grid = unsigned(std::min<uint32_t>(ntiles, uint32_t(resident)));
         lbm_aa_even_tma<T, S, B><<<grid, T, Lm::kBytes, s>>>(wk.f_old(), wk.P, b, e, omega);
     }
 
+#ifdef SPLBCU_TUNING
     template <int T, int S, int B>
     void launch_aa_odd_tmc(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e) {
         using Lm = AaOddSmem<T, S, B>;
-        static int cfg_dev = -1, resident = 0;
-        if (cfg_dev != wk.dev) {
-            CK(cudaFuncSetAttribute(lbm_aa_odd_tmc<T, S, B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    int(Lm::kBytes)));
-            int per_sm = 0, sms = 0;
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lbm_aa_odd_tmc<T, S, B>, T, Lm::kBytes));
-            CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, wk.dev));
-            resident = std::max(1, per_sm) * sms;
-            cfg_dev = wk.dev;
-        }
+        const int resident = resident_ctas(lbm_aa_odd_tmc<T, S, B>, wk.dev, T, Lm::kBytes);
         const uint32_t base = b & ~127u;
         const uint32_t ntiles = (e - base + T - 1) / T;
         const unsigned grid = unsigned(std::min<uint32_t>(ntiles, uint32_t(resident)));
         lbm_aa_odd_tmc<T, S, B><<<grid, T, Lm::kBytes, s>>>(wk.f_old(), wk.dtab.get<int16_t>(), wk.gbase.get<uint32_t>(),
                                                              wk.tab.get<uint32_t>(), wk.P, wk.PG, b, e, omega);
     }
+#endif
 
     void launch_aa_range(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, bool iolet, const double* staged,
                          const int32_t* coords, bool timed, bool edge, bool odd) {
@@ -1875,20 +1949,22 @@ class Engine {
         } else {
             const int v = plain_variant;
             if (iolet) lbm_aa_odd<true, false, 128, 4><<<nb, 128, 0, s>>>(F, tab, wk.P, b, e, omega, ia, h);
-            else if (timed && wk.ctab_ok && v >= 61 && v <= 63) {
+#ifdef SPLBCU_TUNING
+            else if (timed && wk.ctab_ok && v >= 61 && v <= 64) {
                 if (v == 61) launch_aa_odd_tmc<128, 2, 4>(wk, s, b, e);
                 else if (v == 62) launch_aa_odd_tmc<256, 3, 2>(wk, s, b, e);
-                else launch_aa_odd_tmc<256, 2, 2>(wk, s, b, e);
-            } else if (timed && wk.ctab_ok && v != 60) {
+                else if (v == 63) launch_aa_odd_tmc<256, 2, 2>(wk, s, b, e);
+                else
+                    lbm_aa_odd_c<256, 2><<<unsigned((e - (b & ~31u) + 255) / 256), 256, 0, s>>>(
+                        F, wk.dtab.get<int16_t>(), wk.gbase.get<uint32_t>(), tab, wk.P, wk.PG, b, e, omega);
+            }
+#endif
+            else if (timed && wk.ctab_ok && v != 60) {
                 // default: compressed table, one thread per site, branch-free
                 // address selects (C3: 15.9k MSUPS vs 15.4k for the u32 gather)
                 const uint32_t b0 = b & ~31u;
-                if (v == 64)
-                    lbm_aa_odd_c<256, 2><<<unsigned((e - b0 + 255) / 256), 256, 0, s>>>(
-                        F, wk.dtab.get<int16_t>(), wk.gbase.get<uint32_t>(), tab, wk.P, wk.PG, b, e, omega);
-                else
-                    lbm_aa_odd_c<128, 4><<<unsigned((e - b0 + 127) / 128), 128, 0, s>>>(
-                        F, wk.dtab.get<int16_t>(), wk.gbase.get<uint32_t>(), tab, wk.P, wk.PG, b, e, omega);
+                lbm_aa_odd_c<128, 4><<<unsigned((e - b0 + 127) / 128), 128, 0, s>>>(
+                    F, wk.dtab.get<int16_t>(), wk.gbase.get<uint32_t>(), tab, wk.P, wk.PG, b, e, omega);
             } else lbm_aa_odd<false, false, 128, 4><<<nb, 128, 0, s>>>(F, tab, wk.P, b, e, omega, ia, h);
         }
         if (timed) {

@@ -84,7 +84,7 @@ __device__ __forceinline__ void store_shared(double* fn, uint64_t P, uint32_t sl
 template <bool kIolets, int kThreads, int kMinBlocks, bool kP2P = false>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
 lbm_push(const double* __restrict__ fo, double* __restrict__ fn, const uint32_t* __restrict__ tab,
-         uint64_t P, uint32_t begin, uint32_t end, double omega, IoletArgs ia, HaloArgs halo) {
+         uint64_t P, uint32_t begin, uint32_t end, double omega, IoletArgs ia, const __grid_constant__ HaloArgs halo) {
     const uint32_t s = begin + blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= end) return;
     double f[kQ];
@@ -204,7 +204,8 @@ struct PushTmaSmem {
 template <int T, int S, int kMinBlocks, bool kTabSmem = true, int kHints = 0, bool kP2P = false>
 __global__ void __launch_bounds__(T, kMinBlocks)
 lbm_push_tma(const double* __restrict__ fo, double* __restrict__ fn, const uint32_t* __restrict__ tab,
-             uint64_t P, uint32_t begin, uint32_t end, double omega, HaloArgs halo = HaloArgs{}) {
+             uint64_t P, uint32_t begin, uint32_t end, double omega,
+             const __grid_constant__ HaloArgs halo = HaloArgs{}) {
     using L = PushTmaSmem<T, S, kTabSmem>;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S * L::kStage);
@@ -739,7 +740,7 @@ lbm_aa_even_tma(double* __restrict__ F, uint64_t P, uint32_t begin, uint32_t end
 template <bool kIolets, bool kP2P, int kThreads, int kMinBlocks>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
 lbm_aa_odd(double* __restrict__ F, const uint32_t* __restrict__ tab, uint64_t P, uint32_t begin, uint32_t end,
-           double omega, IoletArgs ia, HaloArgs halo) {
+           double omega, IoletArgs ia, const __grid_constant__ HaloArgs halo) {
     const uint32_t s = begin + blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= end) return;
     uint32_t t[kQ - 1];
@@ -947,7 +948,7 @@ __device__ __forceinline__ void aa_gather(const double* F, const uint32_t* tab, 
 
 template <bool kP2P>
 __global__ void lbm_aa_capture(const double* __restrict__ F, const uint32_t* __restrict__ tab, uint64_t P,
-                               uint32_t n, int state_s, HaloArgs h, double* __restrict__ out4) {
+                               uint32_t n, int state_s, const __grid_constant__ HaloArgs h, double* __restrict__ out4) {
     const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= n) return;
     double fl[kQ];
@@ -963,7 +964,7 @@ __global__ void lbm_aa_capture(const double* __restrict__ F, const uint32_t* __r
 // f in the reference's meaning for every (site, direction): 19 planes of n.
 template <bool kP2P>
 __global__ void lbm_aa_export(const double* __restrict__ F, const uint32_t* __restrict__ tab, uint64_t P, uint32_t n,
-                              int state_s, HaloArgs h, double* __restrict__ out) {
+                              int state_s, const __grid_constant__ HaloArgs h, double* __restrict__ out) {
     const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= n) return;
     double fl[kQ];
@@ -992,7 +993,7 @@ __global__ void lbm_aa_import(double* __restrict__ F, const uint32_t* __restrict
 
 template <bool kP2P>
 __global__ void lbm_aa_observe(const double* __restrict__ F, const uint32_t* __restrict__ tab, uint64_t P,
-                               uint32_t n_obs, int state_s, HaloArgs h, const uint32_t* __restrict__ obs_site,
+                               uint32_t n_obs, int state_s, const __grid_constant__ HaloArgs h, const uint32_t* __restrict__ obs_site,
                                const uint16_t* __restrict__ obs_iolet, const IoletDev* __restrict__ io,
                                double* __restrict__ out_row) {
     const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;

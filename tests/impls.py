@@ -17,25 +17,40 @@ import types
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 PORT_LIB = os.path.join(ROOT, "oracle", "liboracle.so")
 REF_LIB = os.path.join(ROOT, "oracle", "_ref", "libsplbref.so")
+PKG = os.path.join(ROOT, "paper_2202_11770_b200")
 
 _cache = {}
 
 
+def _load_file(path: str, name: str):
+    """Imports a module by file path (no package __init__, so nothing that
+    dlopens libsplbcu.so runs)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(name, path)
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
 def _bind(path: str, name: str):
-    from paper_2202_11770_b200 import _lib as L
-    from paper_2202_11770_b200 import splb as S
+    """The product's Python mirror (splb.py) executed over another library
+    implementing the same C-ABI.  Only `_abi.py` (pure ctypes declarations)
+    and the mirror's source are read from the package: the product library
+    is never mapped into a process that only uses the oracles."""
+    A = _load_file(os.path.join(PKG, "_abi.py"), name + "_abi")
     lib = ctypes.CDLL(path)
-    for fn, res, args in L.SIGNATURES:
+    for fn, res, args in A.SIGNATURES:
         f = getattr(lib, fn)
         f.restype = res
         f.argtypes = args
-    shim = types.SimpleNamespace(lib=lib, Iolet=L.Iolet, BC=L.BC, Params=L.Params)
-    src = open(S.__file__).read().replace("from . import _lib as L\n", "")
+    shim = types.SimpleNamespace(lib=lib, Iolet=A.Iolet, BC=A.BC, Params=A.Params)
+    spath = os.path.join(PKG, "splb.py")
+    src = open(spath).read().replace("from . import _lib as L\n", "")
     mod = types.ModuleType(name)
     mod.__dict__["L"] = shim
     mod.__dict__["__name__"] = name
     sys.modules[name] = mod
-    exec(compile(src, S.__file__, "exec"), mod.__dict__)
+    exec(compile(src, spath, "exec"), mod.__dict__)
     return mod
 
 

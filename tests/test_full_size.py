@@ -67,9 +67,11 @@ def test_c2_full_size_kernels_and_workers_agree(product):
 
 
 def test_c3_full_size_kernels_and_workers_agree(product):
-    """C3 (1.07e8-site tree, 65 pressure iolets): the default kernel (prefetch,
-    the mid range is >= 2e7 sites), the just-in-time kernel and a 2-worker
-    split give the same bits after 40 steps."""
+    """C3 (1.07e8-site tree, 65 pressure iolets): the default (online choice),
+    the just-in-time and prefetch compressed-table kernels, the u32-table
+    kernel and a 2-worker split give the same bits after 40 steps (the
+    compressed table is pinned to the reference on C3-shaped samples in
+    test_bench_geometries.py)."""
     P = product
     d = P.build_tree(80, 800, 6, 0.8, 0.8)
     assert d.n_sites() == 107037564
@@ -77,7 +79,8 @@ def test_c3_full_size_kernels_and_workers_agree(product):
     ents += [P.BCEntry(P.PRESSURE, P.TimeTable.constant(CS2 * 0.999)) for _ in range(64)]
     bcs = P.BCSet(ents)
     runs = {}
-    for name, variant, workers in (("default", None, 1), ("jit", "43", 1), ("w2", None, 2)):
+    for name, variant, workers in (("default", None, 1), ("jit", "43", 1), ("prefetch", "59", 1), ("u32", "24", 1),
+                                   ("w2", None, 2)):
         prm = P.EngineParams(tau=0.8, dt_s=1.0, workers=workers, devices=[0])
         runs[name] = _run(P, d, bcs, prm, 40, variant)
     want = runs["default"][0]

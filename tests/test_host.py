@@ -142,6 +142,26 @@ def test_generators_validate(product, reference):
             assert cases.partition_digest(product.partition(d, W)) == cases.partition_digest(reference.partition(r, W))
 
 
+@pytest.mark.parametrize("spec", [("tree", 6, 24, 3, 0.8, 0.8), ("tree", 8, 40, 5, 0.8, 0.8),
+                                  ("tree", 5, 20, 6, 0.8, 0.8), ("tree", 12, 30, 2, 0.7, 0.6),
+                                  ("channel", 10, 12, 30), ("channel", 7, 5, 9)])
+def test_generators_match_reference_classifier(product, reference, spec):
+    """The bench geometries (C3/C5 trees with up to 65 iolets, the C4
+    channel) from the product's generator + classifier are bit-identical to
+    the reference's classify_sites (geometry.hpp:139-208) run on the same
+    voxels (oracle/geometry_gen.py restates the voxelisation): coordinates,
+    types, every link's kind and iolet id, type ranges and iolet discs."""
+    import geometry_gen as G
+    kind, args = spec[0], spec[1:]
+    vox, io = getattr(G, kind)(*args)
+    r = G.classify(reference, vox, io)
+    d = getattr(product, "build_" + kind)(*args)
+    assert cases.domain_digest(d) == cases.domain_digest(r)
+    got = [(i.kind, tuple(i.center), tuple(i.normal), i.radius) for i in d.export()["iolets"]]
+    want = [(i.kind, tuple(i.center), tuple(i.normal), i.radius) for i in r.export()["iolets"]]
+    assert got == want
+
+
 def test_tree_size_model(product):
     d = product.build_tree(8, 40, 4, 0.8, 0.8)
     e = d.export()
