@@ -301,6 +301,8 @@ def main():
     ap.add_argument("--quick", action="store_true", help="kernel-only number (tuning runs)")
     ap.add_argument("--storage", default="two", choices=["two", "aa"],
                     help="two buffers (push) or one buffer in place (AA pattern)")
+    ap.add_argument("--scheme", default="push", choices=["push", "pull"],
+                    help="push (fused collide + scatter) or the reference's pull gather (update_pull)")
     ap.add_argument("--halo", default="p2p", choices=["nccl", "p2p"],
                     help="N>1 halo exchange: NCCL send/recv + PostReceive, or fused NVLink P2P stores")
     ap.add_argument("--develop", type=int, default=3000,
@@ -349,7 +351,9 @@ def main():
     d, bcs, p, desc = workload(P, name, args.scale, source=slab_src)
     halo_mode = 1 if args.halo == "p2p" else 0
     storage = 1 if args.storage == "aa" else 0
-    sim = make_sim(P.EngineParams(workers=world, devices=[local], halo_mode=halo_mode, storage=storage, **p))
+    scheme = P.PULL if args.scheme == "pull" else P.PUSH
+    sim = make_sim(P.EngineParams(workers=world, devices=[local], halo_mode=halo_mode, storage=storage, scheme=scheme,
+                                  **p))
     n = sim.n_sites()
     sim_slab = sim.slab_local()
     setup_s = time.time() - t_setup
@@ -403,7 +407,7 @@ def main():
     # in the same (developed) state as the device-timed number
     sim.close()
     params_e = P.EngineParams(workers=world, devices=[local], observe_iolets=True, halo_mode=halo_mode,
-                              storage=storage, **p)
+                              storage=storage, scheme=scheme, **p)
     sim = make_sim(params_e)
     develop(sim, args.develop, chunk=100)
     for _ in range(args.warmup):
@@ -455,6 +459,7 @@ def main():
                 "warmup": args.warmup, "ms_per_step": dev_s / args.steps * 1e3, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": desc, "sites": n, "parallelism": f"slab decomposition x{world}",
+                           "scheme": args.scheme, "storage": "AA single buffer" if storage else "two buffers",
                            "halo": (("NCCL send/recv + PostReceive" if halo_mode == 0 else "fused NVLink P2P stores")
                                     if world > 1 else "none"),
                            "l2": f"inputs (f, table) {n * 376 / 1e9:.1f} GB per step >> 126 MB L2; no flush needed",

@@ -274,6 +274,12 @@ int splbcu_sim_export_map(splbcu_sim* s, int32_t w, uint32_t* dest, uint8_t* op,
                           uint32_t* send_src_site, uint8_t* send_src_dir,
                           int32_t* seg_neighbor, uint32_t* seg_base,
                           uint32_t* seg_count);
+/* map(w).sources (layout.hpp:104-119, 237-282): the pull-side source of every
+ * slot [site*18 + (j-1)] in the reference encoding — src_site (local index;
+ * FromLocal only, else the site itself / 0), op (GatherOp: 0 FromLocal,
+ * 1 FromRemote, 2 SelfBounce, 3 SelfIolet) and iolet id.  Arrays of 18*n. */
+int splbcu_sim_export_sources(splbcu_sim* s, int32_t worker, uint32_t* src_site,
+                              uint8_t* op, uint16_t* iolet);
 /* assignment() (engine.hpp:143): the partition the simulation uses (borrowed,
  * valid for the simulation's lifetime); NULL when slab-local. */
 const splbcu_partition* splbcu_sim_partition(const splbcu_sim* s);

@@ -357,6 +357,16 @@ int splbcu_sim_export_map(splbcu_sim* s, int32_t w, uint32_t* dest, uint8_t* op,
         }
     });
 }
+int splbcu_sim_export_sources(splbcu_sim* s, int32_t w, uint32_t* src, uint8_t* op, uint16_t* iol) {
+    return guard([&] {
+        const StreamingMap& m = s->s->map(w);
+        for (size_t q = 0; q < m.sources.size(); ++q) {
+            if (src) src[q] = m.sources[q].src_site;
+            if (op) op[q] = uint8_t(m.sources[q].op);
+            if (iol) iol[q] = m.sources[q].iolet;
+        }
+    });
+}
 const splbcu_partition* splbcu_sim_partition(const splbcu_sim* s) {
     auto* ss = const_cast<splbcu_sim*>(s);
     ss->view.p = s->s->assignment();

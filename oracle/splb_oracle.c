@@ -1172,6 +1172,33 @@ int splbcu_sim_export_map(splbcu_sim* S, int32_t w, uint32_t* dest, uint8_t* op,
     if (sc) memcpy(sc, wk->seg_count, 4 * wk->n_seg);
     return 0;
 }
+/* StreamingMap::sources (layout.hpp:104-119, 237-282): the pull-side source
+ * of slot (s, inverse(i)) follows from link i of s. */
+int splbcu_sim_export_sources(splbcu_sim* S, int32_t w, uint32_t* src, uint8_t* op, uint16_t* iol) {
+    const worker_t* wk = &S->wk[w];
+    const int lay = S->prm.layout;
+    for (uint32_t s = 0; s < wk->n; ++s)
+        for (int i = 1; i < Q; ++i) {
+            const size_t q = 18 * (size_t)s + (size_t)(i - 1);
+            const size_t g = 18 * (size_t)s + (size_t)(INV[i] - 1);
+            uint32_t site = s;
+            uint8_t o;
+            uint16_t io = 0;
+            switch (wk->op[q]) {
+                case 0: /* ToLocal: dest = idx(local(tg), i) */
+                    site = lay == 0 ? wk->dest[q] / Q : wk->dest[q] - (uint32_t)i * wk->n;
+                    o = 0;
+                    break;
+                case 1: site = 0; o = 1; break; /* FromRemote */
+                case 2: o = 2; break;            /* SelfBounce */
+                default: o = 3; io = wk->iol[q]; break;
+            }
+            if (src) src[g] = site;
+            if (op) op[g] = o;
+            if (iol) iol[g] = io;
+        }
+    return 0;
+}
 const splbcu_partition* splbcu_sim_partition(const splbcu_sim* S) {
     S->part->borrowed = 1;
     return S->part;

@@ -99,6 +99,7 @@ SIGNATURES = [
     ("splbcu_sim_map_shape", c_int, [_P, c_int, c_u32p, c_u32p, c_u32p]),
     ("splbcu_sim_export_map", c_int, [_P, c_int, c_u32p, c_u8p, c_u16p, c_u32p, c_u32p, c_u8p, c_i32p,
                                       c_u32p, c_u32p]),
+    ("splbcu_sim_export_sources", c_int, [_P, c_int, c_u32p, c_u8p, c_u16p]),
     ("splbcu_sim_partition", _P, [_P]),
     ("splbcu_sim_n_captures", C.c_uint64, [_P]),
     ("splbcu_sim_capture", c_int, [_P, C.c_uint64, c_u64p, c_dp]),

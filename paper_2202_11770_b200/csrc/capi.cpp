@@ -528,6 +528,16 @@ int splbcu_sim_export_map(splbcu_sim* s, int32_t w, uint32_t* dest, uint8_t* op,
     });
 }
 
+int splbcu_sim_export_sources(splbcu_sim* s, int32_t w, uint32_t* src_site, uint8_t* op, uint16_t* iolet) {
+    return guard([&] {
+        check_ptr(s, "simulation");
+        const ExportedMap m = s->s->export_map(w);
+        if (src_site) std::memcpy(src_site, m.src_site.data(), m.src_site.size() * 4);
+        if (op) std::memcpy(op, m.src_op.data(), m.src_op.size());
+        if (iolet) std::memcpy(iolet, m.src_iolet.data(), m.src_iolet.size() * 2);
+    });
+}
+
 const splbcu_partition* splbcu_sim_partition(const splbcu_sim* s) {
     if (!s || s->s->slab_local()) return nullptr;
     auto* ss = const_cast<splbcu_sim*>(s);

@@ -415,6 +415,7 @@ class Engine {
     bool kernel_timing = false;
     bool p2p_mode = false;
     bool aa_mode = false;  // single-buffer AA storage (params.storage == 1)
+    bool pull_mode = false;  // scheme == pull with two buffers: update_pull + fill_send_slots
     std::vector<IoletDev> io_host;
     std::unique_ptr<Window> win;  // slab-local build: dom holds this rank's window only
     uint64_t n_global = 0;        // sites of the whole domain
@@ -518,6 +519,7 @@ class Engine {
         rank = rank_;
         nranks = nranks_;
         aa_mode = prm.storage == 1;
+        pull_mode = prm.scheme == 1 && !aa_mode;
         if (prm.devices.empty()) {
             int cur = 0;
             CK(cudaGetDevice(&cur));
@@ -1498,6 +1500,31 @@ class Engine {
         return h;
     }
 
+    // Records the start event of a timed bulk launch; returns its end event.
+    cudaEvent_t timing_begin(WorkerDev& wk, cudaStream_t s) {
+        if (wk.tev_used + 2 > wk.tev.size())
+            for (int k = 0; k < 2; ++k) {
+                cudaEvent_t ev;
+                CK(cudaEventCreate(&ev));
+                wk.tev.push_back(ev);
+            }
+        CK(cudaEventRecord(wk.tev[wk.tev_used++], s));
+        return wk.tev[wk.tev_used++];
+    }
+
+    // fill_send_slots (engine.hpp:489-502), pull scheme only.
+    void fill_send_slots(WorkerDev& wk, cudaStream_t s) {
+        if (!wk.shared) return;
+        if (p2p_mode)
+            lbm_fill_send_slots<true><<<blocks_for(wk.shared), 256, 0, s>>>(
+                wk.f_old(), wk.f_new(), wk.send_pos.get<uint64_t>(), wk.P, wk.shared, omega, halo_args(wk));
+        else
+            lbm_fill_send_slots<false><<<blocks_for(wk.shared), 256, 0, s>>>(
+                wk.f_old(), wk.f_new(), wk.send_pos.get<uint64_t>(), wk.P, wk.shared, omega, HaloArgs{});
+        launches++;
+        CK(cudaGetLastError());
+    }
+
     // `timed`: the bulk (mid-group) plain launch, whose CUDA-event duration
     // feeds the roofline; the small edge launches overlap it on another stream.
     // `edge` launches store cut-crossing links to the neighbours in P2P mode.
@@ -1505,6 +1532,20 @@ class Engine {
                       const int32_t* coords, bool timed, bool edge = false) {
         if (e <= b) return;
         IoletArgs ia{wk.io_geo.get<IoletDev>(), staged, coords};
+        if (pull_mode) {
+            cudaEvent_t e1 = timed && kernel_timing ? timing_begin(wk, s) : nullptr;
+            const unsigned nb = blocks_for(e - b, 128);
+            if (iolet) lbm_pull<true><<<nb, 128, 0, s>>>(wk.f_old(), wk.f_new(), wk.tab.get<uint32_t>(), wk.P, b, e, omega, ia);
+            else lbm_pull<false><<<nb, 128, 0, s>>>(wk.f_old(), wk.f_new(), wk.tab.get<uint32_t>(), wk.P, b, e, omega, ia);
+            if (e1) CK(cudaEventRecord(e1, s));
+            if (timed) {
+                plain_launches++;
+                plain_sites += e - b;
+            }
+            launches++;
+            CK(cudaGetLastError());
+            return;
+        }
         const unsigned nb = blocks_for(e - b);
         const bool p2p = edge && p2p_mode && wk.shared > 0;
         if (iolet) {
@@ -1549,6 +1590,7 @@ class Engine {
         if (edge) {
             launch_range(wk, s, 0, wk.ep, false, staged, ioc, false, true);
             launch_range(wk, s, wk.ep, wk.n_edge, true, staged, ioc, false, true);
+            if (pull_mode) fill_send_slots(wk, s);
         } else {
             launch_range(wk, s, wk.n_edge, wk.n_edge + wk.mp, false, staged, ioc, true);
             launch_range(wk, s, wk.n_edge + wk.mp, wk.n, true, staged, ioc + 3 * uint64_t(wk.n_edge - wk.ep), false);
@@ -2355,6 +2397,9 @@ class Engine {
         m.dest.resize(18 * uint64_t(wk.n));
         m.op.resize(18 * uint64_t(wk.n));
         m.iolet.resize(18 * uint64_t(wk.n));
+        m.src_site.resize(18 * uint64_t(wk.n));
+        m.src_op.resize(18 * uint64_t(wk.n));
+        m.src_iolet.resize(18 * uint64_t(wk.n));
         for (uint32_t j = 0; j < wk.n; ++j) {
             const uint32_t r = wk.ref_of_int[j];
             for (int i = 1; i < kQ; ++i) {
@@ -2383,6 +2428,12 @@ class Engine {
                 m.dest[q] = dest;
                 m.op[q] = op;
                 m.iolet[q] = io;
+                // the pull-side source of (r, inverse(i)) follows from link i
+                // (layout.hpp:243-282): FromLocal / FromRemote / SelfBounce / SelfIolet
+                const uint64_t g = 18 * uint64_t(r) + uint64_t(inv(i) - 1);
+                m.src_site[g] = op == 0 ? wk.ref_of_int[v] : (op == 1 ? 0u : r);
+                m.src_op[g] = op;
+                m.src_iolet[g] = io;
             }
         }
         m.recv_dest.resize(wk.shared);

@@ -46,6 +46,10 @@ struct ExportedMap {
     std::vector<uint8_t> send_dir;
     std::vector<int> seg_neighbor;
     std::vector<uint32_t> seg_base, seg_count;
+    // pull side (GatherSource, layout.hpp:104-108), [site*18 + j-1]
+    std::vector<uint32_t> src_site;
+    std::vector<uint8_t> src_op;
+    std::vector<uint16_t> src_iolet;
 };
 
 class Engine;  // defined in engine.cu

@@ -128,6 +128,86 @@ lbm_push(const double* __restrict__ fo, double* __restrict__ fn, const uint32_t*
     }
 }
 
+// ---- pull scheme (update_pull + fill_send_slots, engine.hpp:435-502) ------
+// One thread per destination site d.  Population j of d is gathered from the
+// site the push step streams it from — the target of d's own link inverse(j)
+// in the push table (layout.hpp:243-282 derives GatherSource the same way) —
+// recomputing that source's collision as the reference does (its 19 x 19
+// gather); wall and iolet links reconstruct it from d's own post-collision
+// values.  FromRemote slots are left to the exchange (PostReceive or the
+// neighbour's direct store).  Bitwise equal to the push step
+// (test_engine.cpp:269-300): the same expression trees on the same inputs.
+template <bool kIolets>
+__global__ void __launch_bounds__(128)
+lbm_pull(const double* __restrict__ fo, double* __restrict__ fn, const uint32_t* __restrict__ tab, uint64_t P,
+         uint32_t begin, uint32_t end, double omega, IoletArgs ia) {
+    const uint32_t d = begin + blockIdx.x * blockDim.x + threadIdx.x;
+    if (d >= end) return;
+    double fp[kQ];
+    Macro md;
+    {
+        double f[kQ];
+#pragma unroll
+        for (int i = 0; i < kQ; ++i) f[i] = ld_f(fo + uint64_t(i) * P + d);
+        md = macro_of(f);
+        double feq[kQ];
+        feq_all(md.rho, md.ux, md.uy, md.uz, feq);
+#pragma unroll
+        for (int i = 0; i < kQ; ++i) fp[i] = relax(f[i], feq[i], omega);
+    }
+    fn[d] = fp[0];
+#pragma unroll
+    for (int j = 1; j < kQ; ++j) {
+        const int i = inv(j);
+        const uint32_t v = __ldg(tab + uint64_t(i - 1) * P + d);
+        double out;
+        if (v < kSpecial) {  // FromLocal: the source's collision, recomputed
+            double fs[kQ];
+#pragma unroll
+            for (int q = 0; q < kQ; ++q) fs[q] = __ldg(fo + uint64_t(q) * P + v);
+            const Macro ms = macro_of(fs);
+            out = relax(fs[j], feq_one(j, ms.rho, ms.ux, ms.uy, ms.uz), omega);
+        } else {
+            const uint32_t op = (v >> kOpShift) & 3u;
+            if (op == kOpShared) continue;  // FromRemote
+            out = fp[i];                    // SelfBounce
+            if constexpr (kIolets) {
+                if (op == kOpIolet) {       // SelfIolet
+                    const uint32_t k = v & kPayload;
+                    const int32_t* c = ia.coords + 3 * uint64_t(d - begin);
+                    out = iolet_link_value(i, fp[i], md, ia.io[k], ia.staged[k], c[0], c[1], c[2]);
+                }
+            }
+        }
+        fn[uint64_t(j) * P + d] = out;
+    }
+}
+
+// fill_send_slots (engine.hpp:489-502): the post-collision value of every
+// outgoing shared slot (send site s, direction i) into the send tail, or
+// straight into the neighbour's f_new in the fused P2P mode.
+template <bool kP2P>
+__global__ void lbm_fill_send_slots(const double* __restrict__ fo, double* __restrict__ fn,
+                                    const uint64_t* __restrict__ send_pos, uint64_t P, uint32_t n, double omega,
+                                    const __grid_constant__ HaloArgs halo) {
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const uint64_t tp = send_pos[k];  // (i - 1) * P + s
+    const int i = int(tp / P) + 1;
+    const uint64_t s = tp % P;
+    double f[kQ];
+#pragma unroll
+    for (int q = 0; q < kQ; ++q) f[q] = fo[uint64_t(q) * P + s];
+    const Macro m = macro_of(f);
+    double feq[kQ];
+    feq_all(m.rho, m.ux, m.uy, m.uz, feq);  // feq_all[i] == feq(i, m, usq_term(m)) bit for bit
+    double fi = f[1], fe = feq[1];
+#pragma unroll
+    for (int q = 2; q < kQ; ++q)
+        if (q == i) fi = f[q], fe = feq[q];
+    store_shared<kP2P>(fn, P, k, relax(fi, fe, omega), halo);
+}
+
 // ---- TMA-pipelined persistent variant -------------------------------------
 // The plain-site kernel is bound by HBM latency (ncu: long-scoreboard stalls
 // dominate at the register-limited occupancy).  This version decouples loads

@@ -406,6 +406,10 @@ class StreamingMap:
     send_src_site: np.ndarray
     send_src_dir: np.ndarray
     segments: List[tuple]
+    # pull side (GatherSource, layout.hpp:104-108): per slot [site*18 + j-1]
+    src_site: np.ndarray = None
+    src_op: np.ndarray = None
+    src_iolet: np.ndarray = None
 
 
 @dataclass
@@ -625,8 +629,13 @@ class Simulation:
                                          _ptr(io, C.c_uint16), _ptr(rd, C.c_uint32), _ptr(ss, C.c_uint32),
                                          _ptr(sd, C.c_uint8), _ptr(sn, C.c_int32), _ptr(sb, C.c_uint32),
                                          _ptr(sc, C.c_uint32)))
+        gs = np.zeros(18 * n, np.uint32)
+        go = np.zeros(18 * n, np.uint8)
+        gi = np.zeros(18 * n, np.uint16)
+        _check(lib.splbcu_sim_export_sources(self._h, w, _ptr(gs, C.c_uint32), _ptr(go, C.c_uint8),
+                                             _ptr(gi, C.c_uint16)))
         return StreamingMap(n, sh, dest, op, io, rd[:sh], ss[:sh], sd[:sh],
-                            [(int(sn[k]), int(sb[k]), int(sc[k])) for k in range(ns)])
+                            [(int(sn[k]), int(sb[k]), int(sc[k])) for k in range(ns)], gs, go, gi)
 
     def cache(self) -> List[Capture]:
         out = []

@@ -195,7 +195,7 @@ def total_mass(M, sim):
 def execute_run(M, run, devices=None, halo_mode=None, storage=None):
     d = make_domain(M, DOMAINS[run["domain"]])
     p = M.EngineParams(tau=run.get("tau", 0.9), dt_s=run.get("dt", 1.0), workers=run["W"],
-                       layout=run.get("layout", 0), sequence=run.get("sequence", 0),
+                       layout=run.get("layout", 0), sequence=run.get("sequence", 0), scheme=run.get("scheme", 0),
                        capture_period=run.get("capture", 0), observe_iolets=run.get("observe", False))
     if devices is not None:
         p.devices = devices
@@ -239,7 +239,9 @@ def partition_digest(p):
 def map_digest(m):
     return dict(n_local=m.n_local, shared=m.shared_size, dest=h(m.dest), op=h(m.op),
                 iolet=h(np.where(m.op == 3, m.iolet, 0).astype(np.uint16)), recv_dest=h(m.recv_dest),
-                send_site=h(m.send_src_site), send_dir=h(m.send_src_dir), segments=[list(s) for s in m.segments])
+                send_site=h(m.send_src_site), send_dir=h(m.send_src_dir), segments=[list(s) for s in m.segments],
+                sources=dict(site=h(m.src_site), op=h(m.src_op),
+                             iolet=h(np.where(m.src_op == 3, m.src_iolet, 0).astype(np.uint16))))
 
 
 def run_digest(res):

@@ -60,6 +60,18 @@ def test_kernel_variants_bit_exact(product, golden, variant, monkeypatch):
         assert cases.run_digest(res) == golden["runs"][key], key
 
 
+@pytest.mark.parametrize("key", sorted(cases.RUNS))
+@pytest.mark.parametrize("halo", [0, 1])
+def test_pull_scheme_bit_exact(product, golden, key, halo):
+    """scheme=pull (update_pull + fill_send_slots, engine.hpp:435-502): every
+    population gathered from its source with the source's collision
+    recomputed; cut links through the send tail + PostReceive (halo 0) or
+    stored straight into the neighbour (halo 1).  The reference's bits
+    (its push/pull contract, test_engine.cpp:269-300)."""
+    res = cases.execute_run(product, dict(cases.RUNS[key], scheme=1), halo_mode=halo)
+    assert cases.run_digest(res) == golden["runs"][key]
+
+
 @pytest.mark.parametrize("key", ["bif_W3_soa_reordered", "bif_W4_noise", "pipe_4_20_W4", "pipe_3_8_obs_W2",
                                  "blob0_noise_W5", "pipe_beat_6_30", "box8_noise_W2_1000"])
 def test_fused_p2p_halo_bit_exact(product, golden, key):
