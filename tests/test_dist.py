@@ -83,7 +83,8 @@ GLOO_SCRIPT = textwrap.dedent("""
         for nb in v["nb"]:
             assert w in views[nb]["nb"], "neighbour relation not symmetric"
     td.barrier()
-    print("OK", rank)
+    td.destroy_process_group()
+    print("OK", rank, flush=True)
 """)
 
 
