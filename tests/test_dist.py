@@ -112,10 +112,12 @@ NCCL_SCRIPT = textwrap.dedent("""
     d = cases.make_domain(P, cases.DOMAINS[run["domain"]])
     kw = dict(tau=0.8, dt_s=1e-3, workers=world, capture_period=20, observe_iolets=True)
     # 0 NCCL, 1 fused P2P, 2 AA single buffer (P2P in place); 3/4/5 the same
-    # three built slab-locally from a geometry source
+    # three built slab-locally from a geometry source; 6/7 the pull scheme
+    # (update_pull + fill_send_slots) over NCCL / fused P2P
     mode = int(os.environ["HALO"])
-    base = mode % 3
-    prm = P.EngineParams(devices=[rank], halo_mode=min(base, 1), storage=1 if base == 2 else 0, **kw)
+    base = mode % 3 if mode < 6 else mode - 6
+    prm = P.EngineParams(devices=[rank], halo_mode=min(base, 1), storage=1 if base == 2 else 0,
+                         scheme=1 if mode >= 6 else 0, **kw)
     pa = None
     if mode >= 3:
         src = P.Source.bifurcation(4, 3, 12, 12)
@@ -146,12 +148,13 @@ NCCL_SCRIPT = textwrap.dedent("""
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("halo", ["0", "1", "2", "3", "4", "5"])
+@pytest.mark.parametrize("halo", ["0", "1", "2", "3", "4", "5", "6", "7"])
 def test_nccl_ranks_match_single_process(halo):
     """halo 0: NCCL send/recv + PostReceive; 1: fused NVLink P2P stores into
     IPC-mapped neighbour buffers, flag-synchronised; 2: AA single buffer.
     3/4/5: the same built slab-locally (each rank classifies only its own
-    slices of a geometry source)."""
+    slices of a geometry source).  6/7: the pull scheme over
+    NCCL / fused P2P."""
     import torch
     n = torch.cuda.device_count()
     if n < 2:
@@ -161,3 +164,56 @@ def test_nccl_ranks_match_single_process(halo):
     for rc, out in outs:
         assert rc == 0, out
         assert "OK" in out
+
+
+DEAD_RANK_SCRIPT = textwrap.dedent("""
+    import os, time
+    import torch, torch.distributed as td
+    import cases, impls
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    torch.cuda.set_device(rank)
+    td.init_process_group("gloo")
+    P = impls.product()
+    uid = P.Simulation.nccl_unique_id() if rank == 0 else bytes(128)
+    obj = [uid]
+    td.broadcast_object_list(obj, 0)
+    d = P.build_pipe(6, 60)
+    bcs = cases.make_bcs(P, ("pressure", 0.34, cases.CS2))
+    prm = P.EngineParams(devices=[rank], workers=world, halo_mode=int(os.environ["HALO"]), exchange_timeout_s=5.0)
+    sim = P.Simulation.distributed(d, bcs, prm, rank, world, obj[0])
+    sim.run(3)
+    td.barrier()
+    if rank == world - 1:
+        os._exit(0)  # this worker dies between steps
+    t0 = time.time()
+    try:
+        sim.run(500)
+        print("NO ERROR")
+    except P.Error as e:
+        print("ERROR after %.1f s: %s" % (time.time() - t0, e), flush=True)
+    sim.close()  # teardown must not hang on streams blocked by the dead peer
+    print("CLOSED", flush=True)
+    os._exit(0)
+""")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("halo", ["0", "1"])
+def test_dead_rank_fails_within_timeout(halo):
+    """A worker that dies is reported by its neighbour within
+    exchange_timeout_s of the last completed step, with the reference's
+    message (Mailbox::take, engine.hpp:92-101), and the survivor's teardown
+    completes."""
+    import re
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs")
+    outs = _run_ranks(DEAD_RANK_SCRIPT, 2, env_extra={"HALO": halo}, timeout=120)
+    rc, out = outs[0]
+    assert rc == 0 and "CLOSED" in out, out
+    m = re.search(r"ERROR after ([0-9.]+) s: (.*)", out)
+    assert m, out
+    assert float(m.group(1)) < 30.0, out
+    assert "exchange failure" in m.group(2), out
+    if halo == "1":
+        assert "timed out waiting for neighbor 1" in m.group(2), out

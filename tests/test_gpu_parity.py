@@ -135,6 +135,24 @@ def test_fused_p2p_multi_gpu_in_process(product, golden):
         assert cases.run_digest(res) == golden["runs"][key], (key, "aa")
 
 
+@pytest.mark.parametrize("mode", ["peer copies", "fused P2P", "AA", "pull"])
+def test_eight_slabs_over_all_devices(product, golden, mode):
+    """8 workers (8 z-slabs, the 8-GPU decomposition) spread over every
+    visible device — 2 per GPU on a 4-GPU box, 8 on one GPU — give the
+    single-worker reference bits on C1 (1000 steps) and on the 60-bpm pipe
+    with the series (test_engine.cpp:302-368: invariance to worker count)."""
+    import torch
+    n = torch.cuda.device_count()
+    kw = {"peer copies": dict(halo_mode=0), "fused P2P": dict(halo_mode=1), "AA": dict(storage=1),
+          "pull": dict(halo_mode=1)}[mode]
+    for key in ("C1_pipe_16_128", "pipe_beat_6_30"):
+        run = dict(cases.RUNS[key], W=8)
+        if mode == "pull":
+            run["scheme"] = 1
+        res = cases.execute_run(product, run, devices=list(range(n)), **kw)
+        assert cases.run_digest(res) == golden["runs"][key], (key, mode)
+
+
 def test_live_reference_random_case(product, reference):
     """A case outside the golden set, against the reference run live."""
     run = dict(domain="bif_3_2_6_8", bcs=("bif", "bif_inlet"), tau=0.7, dt=2e-3, W=3, layout=1, steps=30,
