@@ -8,12 +8,13 @@
 // decomp.hpp:16-188, boundary.hpp:18-74, engine.hpp:37-205); the time step runs
 // in the B200 kernels behind the C-ABI.  Differences: SparseDomain is an
 // opaque owner of the site arrays (export() copies them out), and store(w)
-// returns a host copy (DistributionStore with f_old()/f_new() vectors) that
-// set_f_old()/set_f_new() write back, because the populations live in HBM.
+// is a host mirror of the HBM-resident populations that the simulation keeps
+// coherent (fetched on read, written back before its next operation).
 #pragma once
 
 #include <array>
 #include <cstdint>
+#include <map>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -207,18 +208,74 @@ struct IoletSeries {
     std::vector<std::vector<double>> max_speed, pressure, flow;
 };
 
-// Host copy of store(w) (layout.hpp:19-62).
+// store(w) (layout.hpp:19-62, engine.hpp:149): worker w's two f buffers in
+// the reference layout.  The populations live in HBM, so the object the
+// simulation hands out is a host mirror kept coherent with the device: it is
+// fetched when first read after a step, and pointers taken through f_old() /
+// f_new() may be written — the simulation writes the mirror back before its
+// next operation (run, snapshot_fields, cache, series), as the reference's
+// mutable DistributionStore& would be seen.  A copy (DistributionStore s =
+// sim.store(w)) is a detached snapshot; set_f_old/set_f_new write it back.
+class Simulation;
 struct DistributionStore {
     Layout layout = Layout::AoS;
     uint32_t n_sites = 0, shared_size = 0;
-    std::vector<double> old_, new_;
+
+    DistributionStore() = default;
+    DistributionStore(const DistributionStore& o) { *this = o; }
+    DistributionStore& operator=(const DistributionStore& o) {
+        if (this == &o) return *this;
+        o.sync_();
+        layout = o.layout, n_sites = o.n_sites, shared_size = o.shared_size;
+        old_ = o.old_, new_ = o.new_;
+        h_ = nullptr, fresh_ = true, dirty_ = false;  // detached
+        return *this;
+    }
     size_t idx(uint32_t s, int i) const {
         return layout == Layout::AoS ? size_t(19) * s + size_t(i) : size_t(i) * n_sites + s;
     }
     size_t shared_base() const { return size_t(19) * n_sites; }
     size_t total_size() const { return shared_base() + shared_size; }
-    double* f_old() { return old_.data(); }
-    double* f_new() { return new_.data(); }
+    double* f_old() {
+        sync_();
+        dirty_ = true;
+        return old_.data();
+    }
+    double* f_new() {
+        sync_();
+        dirty_ = true;
+        return new_.data();
+    }
+    const double* f_old() const {
+        sync_();
+        return old_.data();
+    }
+    const double* f_new() const {
+        sync_();
+        return new_.data();
+    }
+
+  private:
+    friend class Simulation;
+    mutable std::vector<double> old_, new_;
+    splbcu_sim* h_ = nullptr;  // owning simulation (null: detached copy)
+    int w_ = 0;
+    mutable bool fresh_ = true;
+    bool dirty_ = false;
+    void sync_() const {
+        if (h_ && !fresh_) {
+            detail::check(splbcu_sim_get_f(h_, w_, 0, old_.data()));
+            detail::check(splbcu_sim_get_f(h_, w_, 1, new_.data()));
+            fresh_ = true;
+        }
+    }
+    void write_back_() {
+        if (h_ && dirty_) {
+            detail::check(splbcu_sim_set_f(h_, w_, 0, old_.data()));
+            detail::check(splbcu_sim_set_f(h_, w_, 1, new_.data()));
+        }
+        dirty_ = false;
+    }
 };
 
 // engine.hpp:121-205
@@ -282,7 +339,11 @@ class Simulation {
         return Simulation(nullptr, p, uint32_t(bcs.entries.size()), s);
     }
 
-    void run(uint64_t n_steps) { detail::check(splbcu_sim_run(h_.get(), n_steps)); }
+    void run(uint64_t n_steps) {
+        flush_stores_();
+        detail::check(splbcu_sim_run(h_.get(), n_steps));
+        stale_stores_();
+    }
     uint64_t steps_run() const { return splbcu_sim_steps_run(h_.get()); }
     double step_loop_seconds() const { return splbcu_sim_step_loop_seconds(h_.get()); }
     uint64_t n_sites() const { return splbcu_sim_n_sites(h_.get()); }
@@ -293,25 +354,41 @@ class Simulation {
     }
 
     std::vector<double> snapshot_fields() const {
+        flush_stores_();
         std::vector<double> out(4 * n_sites());
         detail::check(splbcu_sim_snapshot(h_.get(), out.data()));
         return out;
     }
 
-    DistributionStore store(int w) {
-        DistributionStore st;
-        st.layout = params_.layout;
-        detail::check(splbcu_sim_store_shape(h_.get(), w, &st.n_sites, &st.shared_size));
-        st.old_.resize(st.total_size());
-        st.new_.resize(st.total_size());
-        detail::check(splbcu_sim_get_f(h_.get(), w, 0, st.old_.data()));
-        detail::check(splbcu_sim_get_f(h_.get(), w, 1, st.new_.data()));
-        return st;
+    // store(w) (engine.hpp:149): the mutable view described at DistributionStore.
+    DistributionStore& store(int w) {
+        std::unique_ptr<DistributionStore>& m = stores_[w];
+        if (!m) {
+            auto st = std::make_unique<DistributionStore>();
+            st->layout = params_.layout;
+            detail::check(splbcu_sim_store_shape(h_.get(), w, &st->n_sites, &st->shared_size));
+            st->old_.resize(st->total_size());
+            st->new_.resize(st->total_size());
+            st->h_ = h_.get();
+            st->w_ = w;
+            st->fresh_ = false;
+            m = std::move(st);
+        }
+        return *m;
     }
-    void set_f_old(int w, const DistributionStore& st) { detail::check(splbcu_sim_set_f(h_.get(), w, 0, st.old_.data())); }
-    void set_f_new(int w, const DistributionStore& st) { detail::check(splbcu_sim_set_f(h_.get(), w, 1, st.new_.data())); }
+    void set_f_old(int w, const DistributionStore& st) {
+        flush_stores_();
+        detail::check(splbcu_sim_set_f(h_.get(), w, 0, st.f_old()));
+        stale_stores_();
+    }
+    void set_f_new(int w, const DistributionStore& st) {
+        flush_stores_();
+        detail::check(splbcu_sim_set_f(h_.get(), w, 1, st.f_new()));
+        stale_stores_();
+    }
 
     PropertyCache cache() const {
+        flush_stores_();
         PropertyCache c;
         c.capture_period = params_.capture_period;
         const uint64_t n = splbcu_sim_n_captures(h_.get());
@@ -325,6 +402,7 @@ class Simulation {
     }
 
     IoletSeries series() const {
+        flush_stores_();
         IoletSeries s;
         s.rows = splbcu_sim_series_rows(h_.get());
         if (!s.rows) return s;
@@ -342,7 +420,16 @@ class Simulation {
     struct Del {
         void operator()(splbcu_sim* s) const { splbcu_sim_destroy(s); }
     };
+    // user writes through store(w) reach the device before the next operation;
+    // after a step the mirrors are refetched on their next read
+    void flush_stores_() const {
+        for (auto& kv : stores_) kv.second->write_back_();
+    }
+    void stale_stores_() const {
+        for (auto& kv : stores_) kv.second->fresh_ = false;
+    }
     std::shared_ptr<SparseDomain> domain_;  // null when slab-local
+    mutable std::map<int, std::unique_ptr<DistributionStore>> stores_;
     EngineParams params_;
     uint32_t n_io_ = 0;
     std::unique_ptr<splbcu_sim, Del> h_;

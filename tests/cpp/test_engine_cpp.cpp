@@ -56,17 +56,16 @@ int main() {
         std::uniform_real_distribution<double> noise(0.0, 0.05);
         double m0 = 0.0;
         for (int w = 0; w < 2; ++w) {
-            DistributionStore s = sim.store(w);
+            DistributionStore& s = sim.store(w);  // mutable, as the reference's store(w)
             for (uint32_t site = 0; site < s.n_sites; ++site)
                 for (int i = 0; i < 19; ++i) s.f_old()[s.idx(site, i)] += noise(rng);
             for (uint32_t site = 0; site < s.n_sites; ++site)
                 for (int i = 0; i < 19; ++i) m0 += s.f_old()[s.idx(site, i)];
-            sim.set_f_old(w, s);
         }
         sim.run(1000);
         double m1 = 0.0;
         for (int w = 0; w < 2; ++w) {
-            DistributionStore s = sim.store(w);
+            const DistributionStore& s = sim.store(w);
             for (uint32_t site = 0; site < s.n_sites; ++site)
                 for (int i = 0; i < 19; ++i) m1 += s.f_old()[s.idx(site, i)];
         }
@@ -125,6 +124,26 @@ int main() {
         CHECK(a.n_sites() == b.domain().n_sites());
         CHECK(a.snapshot_fields() == b.snapshot_fields());
         CHECK(a.series().flow == b.series().flow);
+    }
+    {  // store(w) is a live, mutable view (engine.hpp:149): a write through it
+       // reaches the next step, and the same reference reads the new state
+        Simulation a(closed_box(5), BCSet{}, params(2)), b(closed_box(5), BCSet{}, params(2));
+        DistributionStore& sb = b.store(1);
+        const size_t k = sb.idx(3, 3);
+        const double v0 = sb.f_old()[k];
+        sb.f_old()[k] += 0.01;
+        a.run(1);
+        b.run(1);
+        CHECK(a.snapshot_fields() != b.snapshot_fields());
+        CHECK(sb.f_old()[k] != v0 + 0.01);  // refetched after the step
+        const DistributionStore copy = b.store(1);  // detached snapshot of the same state
+        bool same = true;
+        for (size_t q = 0; q < copy.total_size(); ++q) same &= copy.f_old()[q] == sb.f_old()[q];
+        CHECK(same);
+        double ma = 0.0, mb = 0.0;
+        for (int w = 0; w < 2; ++w)
+            for (size_t q = 0; q < a.store(w).shared_base(); ++q) ma += a.store(w).f_old()[q], mb += b.store(w).f_old()[q];
+        CHECK(std::abs((mb - ma) - 0.01) <= 1e-12);  // the poke is conserved
     }
     std::printf("%d check(s) failed\n", g_fail);
     return g_fail;
