@@ -59,7 +59,10 @@ def peaks():
         return 6650.0, "fallback"
 
 
-def workload(M, name, scale=1.0, source=False):
+C4W_SITES_PER_GPU = 3.5e8
+
+
+def workload(M, name, scale=1.0, source=False, world=1):
     """Returns (domain, bcs, params, description).  source=True returns the
     geometry as a Source instead (slab-local construction on each rank)."""
     def geo(kind, *args):
@@ -92,8 +95,11 @@ def workload(M, name, scale=1.0, source=False):
         ents = [M.BCEntry(M.PRESSURE, M.TimeTable.constant(CS2 * 1.001))]
         ents += [M.BCEntry(M.PRESSURE, M.TimeTable.constant(CS2 * 0.999)) for _ in range(2 ** levels)]
         return d, M.BCSet(ents), dict(tau=0.8, dt_s=1.0), f"C5 sparse vascular tree R0=160 L0={L0}, {levels} levels, pressure iolets"
-    if name == "c4":
-        nz = int(round(2400 * scale))
+    if name in ("c4", "c4w"):
+        # c4w: weak scaling (BASELINE configs[3]) — the channel grows along z
+        # with the GPU count, C4W_SITES_PER_GPU sites per GPU (two f buffers +
+        # u32 and compressed tables: ~414 B/site, ~145 GB of the 180 GB HBM)
+        nz = int(round(2400 * scale)) if name == "c4" else int(round(C4W_SITES_PER_GPU / 65536 * world * scale))
         d = geo("channel", 256, 256, nz)
         bcs = M.BCSet([M.BCEntry(M.PRESSURE, M.TimeTable.constant(CS2 * 1.001)),
                        M.BCEntry(M.PRESSURE, M.TimeTable.constant(CS2 * 0.999))])
@@ -348,7 +354,7 @@ def main():
 
     t_setup = time.time()
     slab_src = world > 1 and args.geometry == "source"
-    d, bcs, p, desc = workload(P, name, args.scale, source=slab_src)
+    d, bcs, p, desc = workload(P, name, args.scale, source=slab_src, world=world)
     halo_mode = 1 if args.halo == "p2p" else 0
     storage = 1 if args.storage == "aa" else 0
     scheme = P.PULL if args.scheme == "pull" else P.PUSH
@@ -457,7 +463,7 @@ def main():
     if rank == 0:
         line = {"metric": "MSUPS", "value": value, "unit": "MSUPS", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": dev_s / args.steps * 1e3, "higher_is_better": True,
-                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "scaling": "weak" if name == "c4w" else "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": desc, "sites": n, "parallelism": f"slab decomposition x{world}",
                            "scheme": args.scheme, "storage": "AA single buffer" if storage else "two buffers",
                            "halo": (("NCCL send/recv + PostReceive" if halo_mode == 0 else "fused NVLink P2P stores")

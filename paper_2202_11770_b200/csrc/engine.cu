@@ -1005,6 +1005,11 @@ class Engine {
             assign_slots<<<blocks_for(wk.shared), 256, 0, s>>>(ovals2, ivals2, wk.shared, tab, rf, sp);
         CK(cudaGetLastError());
 
+        // the table build's device temporaries go before the big allocations
+        CK(cudaStreamSynchronize(s));
+        for (DevMem* m : {&d_coords, &d_kind, &d_gidx, &d_lk, &d_lo, &d_ll, &d_lg, &d_row, &d_iop, &d_ioi, &ok_, &ov_,
+                          &ik_, &iv_, &cnt, &ok2, &ov2, &ik2, &iv2})
+            m->release();
         // distribution store, f_old = equilibrium(rho0, 0) (engine.hpp:243-260);
         // the AA scheme keeps a single buffer
         for (int b = 0; b < (aa_mode ? 1 : 2); ++b) {
@@ -1026,7 +1031,6 @@ class Engine {
             for (int a = 0; a < 3; ++a) ioc.push_back(coords[3 * uint64_t(j) + a]);
         upload(wk.io_coords, ioc, s);
         upload(wk.io_geo, io_host, s);
-        wk.cap4.alloc<double>(4 * uint64_t(std::max<uint32_t>(wk.n, 1)));
         // tensor maps for the warp-specialised TMA kernel
         wk.tma_ok = wk.P >= 256;
         for (int v = 0; v < 2 && wk.tma_ok; ++v) {
@@ -1655,6 +1659,7 @@ class Engine {
     // storage scheme; `steps` = steps completed (AA state parity).
     void moments_to_cap4(WorkerDev& wk, cudaStream_t s, const double* f, uint64_t steps) {
         if (!wk.n) return;
+        wk.cap4.reserve<double>(4 * uint64_t(wk.n));  // first capture / snapshot only
         if (aa_mode) {
             const int st = int(steps & 1);
             if (p2p_mode)
