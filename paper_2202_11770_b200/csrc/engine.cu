@@ -19,12 +19,22 @@
 #include <thread>
 
 #include <cub/device/device_radix_sort.cuh>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: host ranges for Nsight tools, no-ops otherwise
 
 #include "engine.hpp"
 #include "kernels.cuh"
 #include "nccl_dyn.hpp"
 
 namespace splbcu {
+
+// Host-side NVTX range (setup, run, each step's enqueue) for Nsight Systems /
+// ncu --nvtx filtering (SURVEY §5 tracing).
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 #define CK(x)                                                                                \
     do {                                                                                     \
@@ -537,6 +547,7 @@ class Engine {
     }
 
     void finish_setup() {
+        NvtxRange nv("splbcu::setup");
         omega = 1.0 / prm.tau;  // RelaxationParams (lattice.hpp:83-84), dt = 1
         for (auto& g : dom.iolets) {
             IoletDev x{};
@@ -1243,6 +1254,17 @@ class Engine {
         CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
         return resident_[key] = std::max(1, per_sm) * sms;
     }
+    // The persistent TMA kernels copy whole tiles: the last tile may run past
+    // `end` into the tail pad (f: shared tail + kTilePad; deltas: 4 kTilePad;
+    // group bases: PG slack).  Checked on the host at every launch (a bad
+    // range would otherwise read past the allocation; compute-sanitizer is
+    // not available on this pool).
+    static void check_tiles(const WorkerDev& wk, uint32_t base, uint32_t ntiles, uint32_t T) {
+        const uint64_t last = uint64_t(base) + uint64_t(ntiles) * T;
+        if (last > wk.P + kTilePad || (wk.ctab_ok && (last + 31) / 32 > wk.PG))
+            runtime_error("engine: tile range [" + std::to_string(base) + ", " + std::to_string(last) +
+                          ") exceeds the padded planes (P = " + std::to_string(wk.P) + ")");
+    }
 
     template <int T, int B>
     void launch_plain_t(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia) {
@@ -1260,6 +1282,7 @@ class Engine {
         const uint32_t base = b & ((H & 136) == 136 ? ~127u : ~31u);
         const uint32_t ntiles = (e - base + T - 1) / T;
         const unsigned grid = unsigned(std::min<uint32_t>(ntiles, uint32_t(resident)));
+        check_tiles(wk, base, ntiles, T);
         Planes19 pl;
         for (int i = 0; i < kQ; ++i) pl.p[i] = wk.f_new() + uint64_t(i) * wk.P;
         lbm_push_tmc<T, S, B, H><<<grid, T, kBytes, s>>>(wk.f_old(), wk.f_new(), wk.dtab.get<int16_t>(),
@@ -1292,17 +1315,21 @@ class Engine {
         const char* v = getenv("SPLBCU_BULK_CHUNK");
         return v ? uint64_t(atoll(v)) : kBulkChunk;
     }();
-    void launch_bulk(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia) {
+    template <class Fn>
+    void for_parts(uint32_t b, uint32_t e, Fn&& fn) {
         const uint64_t n = uint64_t(e - b);
         const uint64_t parts = bulk_chunk < 256 ? 1 : (n + bulk_chunk - 1) / bulk_chunk;
         uint64_t c = b;
         for (uint64_t k = 1; k <= parts; ++k) {
             const uint64_t c1 = k == parts ? uint64_t(e) : ((uint64_t(b) + k * n / parts) & ~uint64_t(255));
             if (c1 <= c) continue;
-            launch_plain(wk, s, uint32_t(c), uint32_t(c1), ia, true);
+            fn(uint32_t(c), uint32_t(c1));
             if (c != b) ++launches;  // the step's launch count holds one bulk launch
             c = c1;
         }
+    }
+    void launch_bulk(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia) {
+        for_parts(b, e, [&](uint32_t c, uint32_t c1) { launch_plain(wk, s, c, c1, ia, true); });
     }
 
     // The bulk plain launch through the online kernel choice (WorkerDev::mid_pick).
@@ -1371,7 +1398,7 @@ class Engine {
         (void)v;
         return true;
 #else
-        return v == 0 || v == 24 || v == 43 || v == 59 || v == 60;
+        return v == 0 || v == 24 || v == 43 || v == 59 || v == 60 || v == 64;
 #endif
     }
     void launch_plain(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia, bool mid) {
@@ -1393,7 +1420,7 @@ class Engine {
     // defaults, profiles/r01_sweep_*.log).  Returns false for the built-in ones.
     bool launch_tuning_variant(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia, bool mid) {
         if (plain_variant == 0 || plain_variant == 24 || plain_variant == 43 || plain_variant == 59 ||
-            plain_variant == 60)
+            plain_variant == 60 || plain_variant == 64)
             return false;
         if (plain_variant >= 40 && plain_variant < 60) {
             if (mid && wk.ctab_ok) {
@@ -1477,6 +1504,7 @@ class Engine {
         const uint32_t base = b & ~3u;
         const uint32_t ntiles = (e - base + T - 1) / T;
         const unsigned grid = unsigned(std::min<uint32_t>(ntiles, uint32_t(resident)));
+        check_tiles(wk, base, ntiles, T);
         lbm_push_ws<T, S, B, TS><<<grid, T + 32, Lm::kBytes, s>>>(wk.tm_f[wk.old][v], wk.tm_t[v], wk.f_new(),
                                                                    wk.tab.get<uint32_t>(), wk.P, b, e, omega);
     }
@@ -1490,6 +1518,7 @@ class Engine {
         const uint32_t base = b & ~3u;
         const uint32_t ntiles = (e - base + T - 1) / T;
         const unsigned grid = unsigned(std::min<uint32_t>(ntiles, uint32_t(resident)));
+        check_tiles(wk, base, ntiles, T);
         lbm_push_tma<T, S, B, TS, H, P2><<<grid, T, Lm::kBytes, s>>>(wk.f_old(), wk.f_new(), wk.tab.get<uint32_t>(),
                                                                    wk.P, b, e, omega, halo);
     }
@@ -1723,6 +1752,7 @@ class Engine {
 
     void run(uint64_t n) {
         if (failed) runtime_error("engine: an exchange failure left this simulation unusable");
+        NvtxRange nv("splbcu::run");
         const size_t caps_before = caps.size();
         const bool first_run = steps_run == 0;
         prepare_records(n);
@@ -1949,6 +1979,7 @@ class Engine {
         const uint32_t base = b & ~3u;
         const uint32_t ntiles = (e - base + T - 1) / T;
         const unsigned grid = unsigned(std::min<uint32_t>(ntiles, uint32_t(resident)));
+        check_tiles(wk, base, ntiles, T);
         lbm_aa_even_tma<T, S, B><<<grid, T, Lm::kBytes, s>>>(wk.f_old(), wk.P, b, e, omega);
     }
 
@@ -1960,10 +1991,25 @@ class Engine {
         const uint32_t base = b & ~127u;
         const uint32_t ntiles = (e - base + T - 1) / T;
         const unsigned grid = unsigned(std::min<uint32_t>(ntiles, uint32_t(resident)));
+        check_tiles(wk, base, ntiles, T);
         lbm_aa_odd_tmc<T, S, B><<<grid, T, Lm::kBytes, s>>>(wk.f_old(), wk.dtab.get<int16_t>(), wk.gbase.get<uint32_t>(),
                                                              wk.tab.get<uint32_t>(), wk.P, wk.PG, b, e, omega);
     }
 #endif
+
+    template <int T, int B>
+    void launch_aa_odd_async(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e) {
+        using Lm = AaAsyncSmem<T>;
+        const int resident = resident_ctas(lbm_aa_odd_async<T, B>, wk.dev, T, Lm::kBytes);
+        const uint32_t base = b & ~127u;
+        const uint32_t ntiles = (e - base + T - 1) / T;
+        const unsigned grid = unsigned(std::min<uint32_t>(ntiles, uint32_t(resident)));
+        check_tiles(wk, base, ntiles, T);
+        Planes19 pl;
+        for (int i = 0; i < kQ; ++i) pl.p[i] = wk.f_old() + uint64_t(i) * wk.P;
+        lbm_aa_odd_async<T, B><<<grid, T, Lm::kBytes, s>>>(wk.f_old(), wk.dtab.get<int16_t>(), wk.gbase.get<uint32_t>(),
+                                                             wk.tab.get<uint32_t>(), wk.P, wk.PG, b, e, omega, pl);
+    }
 
     void launch_aa_range(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, bool iolet, const double* staged,
                          const int32_t* coords, bool timed, bool edge, bool odd) {
@@ -1988,6 +2034,8 @@ class Engine {
         const unsigned nb = blocks_for(e - b, 128);
         if (!odd) {
             if (iolet) lbm_aa_even<true><<<blocks_for(e - b), 256, 0, s>>>(F, tab, wk.P, b, e, omega, ia);
+            else if (wk.tma_ok && timed)
+                for_parts(b, e, [&](uint32_t c, uint32_t c1) { launch_aa_even_tma<256, 2, 2>(wk, s, c, c1); });
             else if (wk.tma_ok) launch_aa_even_tma<256, 2, 2>(wk, s, b, e);
             else lbm_aa_even<false><<<blocks_for(e - b), 256, 0, s>>>(F, tab, wk.P, b, e, omega, ia);
         } else if (remote) {
@@ -1997,7 +2045,7 @@ class Engine {
             const int v = plain_variant;
             if (iolet) lbm_aa_odd<true, false, 128, 4><<<nb, 128, 0, s>>>(F, tab, wk.P, b, e, omega, ia, h);
 #ifdef SPLBCU_TUNING
-            else if (timed && wk.ctab_ok && v >= 61 && v <= 64) {
+            else if (timed && wk.ctab_ok && v >= 61 && v <= 65 && v != 64) {
                 if (v == 61) launch_aa_odd_tmc<128, 2, 4>(wk, s, b, e);
                 else if (v == 62) launch_aa_odd_tmc<256, 3, 2>(wk, s, b, e);
                 else if (v == 63) launch_aa_odd_tmc<256, 2, 2>(wk, s, b, e);
@@ -2006,12 +2054,15 @@ class Engine {
                         F, wk.dtab.get<int16_t>(), wk.gbase.get<uint32_t>(), tab, wk.P, wk.PG, b, e, omega);
             }
 #endif
-            else if (timed && wk.ctab_ok && v != 60) {
-                // default: compressed table, one thread per site, branch-free
-                // address selects (C3: 15.9k MSUPS vs 15.4k for the u32 gather)
+            else if (timed && wk.ctab_ok && v == 64) {
+                // round-1 default: compressed table, one thread per site,
+                // register gather (C3 developed: 13.6k MSUPS, 0.71 of copy BW)
                 const uint32_t b0 = b & ~31u;
                 lbm_aa_odd_c<128, 4><<<unsigned((e - b0 + 127) / 128), 128, 0, s>>>(
                     F, wk.dtab.get<int16_t>(), wk.gbase.get<uint32_t>(), tab, wk.P, wk.PG, b, e, omega);
+            } else if (timed && wk.ctab_ok && v != 60) {
+                // default: gathers as cp.async into shared memory, software-pipelined
+                for_parts(b, e, [&](uint32_t c, uint32_t c1) { launch_aa_odd_async<256, 2>(wk, s, c, c1); });
             } else lbm_aa_odd<false, false, 128, 4><<<nb, 128, 0, s>>>(F, tab, wk.P, b, e, omega, ia, h);
         }
         if (timed) {
@@ -2125,6 +2176,7 @@ class Engine {
     }
 
     void step_once(uint64_t k, uint64_t staged_off) {
+        NvtxRange nv("splbcu::step");
         if (aa_mode) return step_once_aa(k, staged_off);
         if (p2p_mode) return step_once_p2p(k, staged_off);
         const bool classic = prm.sequence == 0;

@@ -1011,6 +1011,136 @@ lbm_aa_odd_c(double* __restrict__ F, const int16_t* __restrict__ dtab, const uin
     }
 }
 
+// Odd step, mid-group plain range: the gathers as asynchronous copies.
+// The odd step reads f_inv(i)(y) from the location its push would write h_i
+// to, loc_i(y) = (i, target_i(y)) or (inv(i), y) for a bounce-back link, and
+// writes h_i(y) back to that same location — scattered loads AND scattered
+// stores, latency-bound as a register gather (one tile of gathers per thread
+// in flight, 128 registers: ~0.7 of the copy roofline).  Here a persistent
+// CTA runs a software pipeline over tiles of T sites:
+//   * the compressed table (int16 deltas + u32 group bases) of tile k+2 is
+//     streamed into shared memory by the TMA engine (cp.async.bulk, 3 stages);
+//   * the 19 gathers of tile k+1 are issued as cp.async (LDGSTS, 8 B each)
+//     straight into shared memory — in flight without holding registers;
+//   * tile k collides from shared memory and stores its 19 results to the
+//     same locations (addresses recomputed from the staged table).
+// Every location is owned by one (site, direction), so the in-place update
+// needs no ordering between tiles or CTAs; the arithmetic is the push step's.
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int T>
+struct AaAsyncSmem {
+    static constexpr uint32_t kF = uint32_t(kQ) * T * 8;                 // gathered f, one tile
+    static constexpr uint32_t kD = uint32_t(kQ - 1) * T * 2;             // int16 deltas
+    static constexpr uint32_t kB = uint32_t(kQ - 1) * (T / 32) * 4;      // group bases
+    static constexpr uint32_t kTab = (kD + kB + 127) / 128 * 128;
+    static constexpr int kFS = 2, kTS = 3;                               // f stages, table stages
+    static constexpr uint32_t kBytes = kFS * kF + kTS * kTab + kTS * 8;
+};
+
+template <int T, int kMinBlocks>
+__global__ void __launch_bounds__(T, kMinBlocks)
+lbm_aa_odd_async(double* __restrict__ F, const int16_t* __restrict__ dtab, const uint32_t* __restrict__ gbase,
+                 const uint32_t* __restrict__ tab, uint64_t P, uint64_t PG, uint32_t begin, uint32_t end, double omega,
+                 const __grid_constant__ Planes19 planes) {
+    using L = AaAsyncSmem<T>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    unsigned char* fsm = smem;                       // [kFS][19][T] doubles
+    unsigned char* tsm = smem + L::kFS * L::kF;      // [kTS] x (deltas [18][T], bases [18][T/32])
+    uint64_t* bar = reinterpret_cast<uint64_t*>(tsm + L::kTS * L::kTab);
+    const uint32_t base = begin & ~127u;  // 16-byte aligned group-base copies (PG is a multiple of 4)
+    const uint32_t ntiles = (end - base + T - 1) / T;
+    const uint32_t G = gridDim.x;
+    const uint32_t tid = threadIdx.x;
+    const int lane = int(tid & 31), warp = int(tid >> 5);
+    if (tid == 0) {
+        for (int s = 0; s < L::kTS; ++s) mbar_init(&bar[s], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    const uint64_t policy = evict_normal_policy();
+    auto issue_table = [&](uint32_t k) {  // thread 0: TMA of tile k's table
+        const uint32_t tile = blockIdx.x + k * G;
+        if (tile >= ntiles) return;
+        const int st = int(k % L::kTS);
+        unsigned char* buf = tsm + st * L::kTab;
+        const uint64_t t0 = uint64_t(base) + uint64_t(tile) * T;
+        mbar_expect_tx(&bar[st], L::kD + L::kB);
+#pragma unroll 1
+        for (int i = 0; i < kQ - 1; ++i) {
+            bulk_g2s(buf + i * T * 2, dtab + uint64_t(i) * P + t0, T * 2, &bar[st], policy);
+            bulk_g2s(buf + L::kD + i * (T / 32) * 4, gbase + uint64_t(i) * PG + (t0 >> 5), (T / 32) * 4, &bar[st],
+                     policy);
+        }
+    };
+    // location of direction j (1..18) of site s from a staged table (plane
+    // bases from the constant bank, branch-free selects; the rare escape is
+    // a predicated load of the u32 table)
+    auto loc = [&](const unsigned char* tb, int j, uint32_t s) -> double* {
+        const int16_t* ds = reinterpret_cast<const int16_t*>(tb);
+        const uint32_t* bs = reinterpret_cast<const uint32_t*>(tb + L::kD);
+        const int d = ds[(j - 1) * T + tid];
+        uint32_t t = bs[(j - 1) * (T / 32) + warp] + uint32_t(lane) + uint32_t(d);
+        const uint32_t esc = d == kDeltaEscape;
+        asm("{\n .reg .pred p;\n setp.ne.u32 p, %1, 0;\n @p ld.global.nc.u32 %0, [%2];\n}"
+            : "+r"(t)
+            : "r"(esc), "l"(tab + uint64_t(j - 1) * P + s));
+        const bool bb = d == kDeltaBounce;
+        const uintptr_t pb = reinterpret_cast<uintptr_t>(bb ? planes.p[inv(j)] : planes.p[j]);
+        return reinterpret_cast<double*>(pb) + (bb ? s : t);
+    };
+    // gathers of tile k into f stage k % kFS (own slots only)
+    auto issue_gathers = [&](uint32_t k) {
+        const uint32_t tile = blockIdx.x + k * G;
+        if (tile >= ntiles) return;
+        const uint32_t s = base + tile * T + tid;
+        if (s < begin || s >= end) return;
+        mbar_wait(&bar[k % L::kTS], (k / L::kTS) & 1u);
+        const unsigned char* tb = tsm + (k % L::kTS) * L::kTab;
+        double* fs = reinterpret_cast<double*>(fsm + (k % L::kFS) * L::kF);
+        cp_async8(fs + tid, F + s);
+#pragma unroll
+        for (int i = 1; i < kQ; ++i) cp_async8(fs + inv(i) * T + tid, loc(tb, i, s));  // f_inv(i)(s)
+    };
+    if (tid == 0) {
+        issue_table(0);
+        issue_table(1);
+    }
+    issue_gathers(0);
+    cp_async_commit();
+    for (uint32_t k = 0;; ++k) {
+        const uint32_t tile = blockIdx.x + k * G;
+        if (tile >= ntiles) break;
+        issue_gathers(k + 1);
+        cp_async_commit();
+        if (tid == 0) issue_table(k + 2);  // into the stage tile k - 1 released
+        cp_async_wait<1>();                // this thread's gathers of tile k have landed
+        const uint32_t s = base + tile * T + tid;
+        if (s >= begin && s < end) {
+            const unsigned char* tb = tsm + (k % L::kTS) * L::kTab;
+            const double* fs = reinterpret_cast<const double*>(fsm + (k % L::kFS) * L::kF);
+            double f[kQ];
+#pragma unroll
+            for (int i = 0; i < kQ; ++i) f[i] = fs[i * T + tid];
+            const Macro m = macro_of(f);
+            double feq[kQ];
+            feq_all(m.rho, m.ux, m.uy, m.uz, feq);
+            F[s] = relax(f[0], feq[0], omega);
+#pragma unroll
+            for (int i = 1; i < kQ; ++i) *loc(tb, i, s) = relax(f[i], feq[i], omega);
+        }
+        __syncthreads();  // table stage k % kTS and f stage k % kFS are free
+    }
+    cp_async_wait<0>();
+}
+
 // Gather the 19 populations of site s in the current AA state (state N:
 // plain reads; state S: the rule above).
 template <bool kP2P>

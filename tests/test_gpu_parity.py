@@ -35,6 +35,42 @@ def test_device_table_bit_exact(product, golden, key):
     assert [cases.map_digest(s.map(w)) for w in range(run["W"])] == golden["maps"][key]
 
 
+def _writes_partition_store(m, layout):
+    """Every f_new location of a worker is written exactly once per step:
+    (s, 0) by s, each ToLocal / bounce-back / iolet link by its site, each
+    received slot by the exchange (recv_dest) — and the shared links fill
+    the tail exactly once (test_layout.cpp:173-191, injectivity and
+    coverage).  This is what makes the fused P2P stores, the AA in-place
+    update and the pull gather race-free."""
+    n = m.n_local
+    idx0 = np.arange(n, dtype=np.int64) * 19 if layout == 0 else np.arange(n, dtype=np.int64)
+    local = m.dest[m.op != 1].astype(np.int64)
+    writes = np.concatenate([idx0, local, m.recv_dest.astype(np.int64)])
+    assert writes.size == 19 * n
+    assert np.array_equal(np.sort(writes), np.arange(19 * n)), "f_new not partitioned by the step's writes"
+    tail = np.sort(m.dest[m.op == 1].astype(np.int64))
+    assert np.array_equal(tail, 19 * n + np.arange(m.shared_size))
+
+
+@pytest.mark.parametrize("spec", [("tree", (12, 48, 6, 0.8, 0.8), 4, 1), ("tree", (8, 40, 7, 0.8, 0.8), 3, 0),
+                                  ("blob", 20240808, 23, 0), ("pipe", (16, 128), 8, 1)])
+def test_step_writes_partition_the_store(product, spec):
+    """Write-disjointness of the device-built tables (the structural check
+    standing in for a race detector: compute-sanitizer is closed on this
+    GPU pool)."""
+    kind, args, W, layout = spec
+    if kind == "blob":
+        d = product.classify_sites(cases.random_blob(args), [])
+        bcs = product.BCSet([])
+    else:
+        d = getattr(product, "build_" + kind)(*args)
+        bcs = product.BCSet([product.BCEntry(product.PRESSURE, product.TimeTable.constant(cases.CS2))
+                             for _ in d.iolets])
+    s = product.Simulation(d, bcs, product.EngineParams(workers=W, layout=layout))
+    for w in range(W):
+        _writes_partition_store(s.map(w), layout)
+
+
 @pytest.mark.parametrize("key", FAST_RUNS)
 def test_runs_bit_exact(product, golden, golden_arrays, key):
     res = cases.execute_run(product, cases.RUNS[key])
@@ -94,8 +130,10 @@ def test_aa_single_buffer_bit_exact(product, golden, key):
 
 @pytest.mark.parametrize("variant", ["0", "60", "61", "62", "63", "64", "65"])
 def test_aa_odd_kernel_variants(product, golden, variant, monkeypatch):
-    """Odd-step kernels: register gather (60) and TMA-staged compressed-table
-    shapes (61, 62; default = 256x2x2) give the reference's bits."""
+    """Odd-step kernels: the default (cp.async gathers into shared memory,
+    software-pipelined), the round-1 register gather over the compressed table
+    (64) and over the u32 table (60), and the tuning shapes (61-63, 65, built
+    with TUNING=1) give the reference's bits."""
     monkeypatch.setenv("SPLBCU_PLAIN_VARIANT", variant)
     _skip_unbuilt(product)
     for key in ("bif_W3_soa_reordered", "pipe_beat_6_30", "C1_pipe_16_128"):
