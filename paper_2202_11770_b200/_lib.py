@@ -10,7 +10,9 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsplbcu.so")
+# SPLBCU_LIB: another build of the same library (e.g. libsplbcu_tuning.so,
+# `make -C csrc tuning`, which adds the tuning-sweep kernel variants)
+LIB_PATH = os.environ.get("SPLBCU_LIB") or os.path.join(_HERE, "libsplbcu.so")
 
 from ._abi import *  # noqa: F401,F403  (structs, SIGNATURES)
 from ._abi import SIGNATURES

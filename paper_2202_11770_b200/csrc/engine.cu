@@ -1398,7 +1398,7 @@ class Engine {
         (void)v;
         return true;
 #else
-        return v == 0 || v == 24 || v == 43 || v == 59 || v == 60 || v == 64;
+        return v == 0 || v == 24 || v == 43 || v == 59 || v == 60;
 #endif
     }
     void launch_plain(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia, bool mid) {
@@ -1420,7 +1420,7 @@ class Engine {
     // defaults, profiles/r01_sweep_*.log).  Returns false for the built-in ones.
     bool launch_tuning_variant(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia, bool mid) {
         if (plain_variant == 0 || plain_variant == 24 || plain_variant == 43 || plain_variant == 59 ||
-            plain_variant == 60 || plain_variant == 64)
+            plain_variant == 60)
             return false;
         if (plain_variant >= 40 && plain_variant < 60) {
             if (mid && wk.ctab_ok) {
@@ -1997,6 +1997,7 @@ class Engine {
     }
 #endif
 
+#ifdef SPLBCU_TUNING
     template <int T, int B>
     void launch_aa_odd_async(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e) {
         using Lm = AaAsyncSmem<T>;
@@ -2010,6 +2011,7 @@ class Engine {
         lbm_aa_odd_async<T, B><<<grid, T, Lm::kBytes, s>>>(wk.f_old(), wk.dtab.get<int16_t>(), wk.gbase.get<uint32_t>(),
                                                              wk.tab.get<uint32_t>(), wk.P, wk.PG, b, e, omega, pl);
     }
+#endif
 
     void launch_aa_range(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, bool iolet, const double* staged,
                          const int32_t* coords, bool timed, bool edge, bool odd) {
@@ -2034,9 +2036,7 @@ class Engine {
         const unsigned nb = blocks_for(e - b, 128);
         if (!odd) {
             if (iolet) lbm_aa_even<true><<<blocks_for(e - b), 256, 0, s>>>(F, tab, wk.P, b, e, omega, ia);
-            else if (wk.tma_ok && timed)
-                for_parts(b, e, [&](uint32_t c, uint32_t c1) { launch_aa_even_tma<256, 2, 2>(wk, s, c, c1); });
-            else if (wk.tma_ok) launch_aa_even_tma<256, 2, 2>(wk, s, b, e);
+            else if (wk.tma_ok) launch_aa_even_tma<256, 2, 2>(wk, s, b, e);  // one launch: parts measured no faster
             else lbm_aa_even<false><<<blocks_for(e - b), 256, 0, s>>>(F, tab, wk.P, b, e, omega, ia);
         } else if (remote) {
             if (iolet) lbm_aa_odd<true, true, 128, 4><<<nb, 128, 0, s>>>(F, tab, wk.P, b, e, omega, ia, h);
@@ -2045,24 +2045,24 @@ class Engine {
             const int v = plain_variant;
             if (iolet) lbm_aa_odd<true, false, 128, 4><<<nb, 128, 0, s>>>(F, tab, wk.P, b, e, omega, ia, h);
 #ifdef SPLBCU_TUNING
-            else if (timed && wk.ctab_ok && v >= 61 && v <= 65 && v != 64) {
+            else if (timed && wk.ctab_ok && v >= 61 && v <= 66) {
                 if (v == 61) launch_aa_odd_tmc<128, 2, 4>(wk, s, b, e);
                 else if (v == 62) launch_aa_odd_tmc<256, 3, 2>(wk, s, b, e);
                 else if (v == 63) launch_aa_odd_tmc<256, 2, 2>(wk, s, b, e);
+                else if (v == 66)  // cp.async gathers (C3 developed: 13.1k vs 13.6k default)
+                    for_parts(b, e, [&](uint32_t c, uint32_t c1) { launch_aa_odd_async<256, 2>(wk, s, c, c1); });
                 else
                     lbm_aa_odd_c<256, 2><<<unsigned((e - (b & ~31u) + 255) / 256), 256, 0, s>>>(
                         F, wk.dtab.get<int16_t>(), wk.gbase.get<uint32_t>(), tab, wk.P, wk.PG, b, e, omega);
             }
 #endif
-            else if (timed && wk.ctab_ok && v == 64) {
-                // round-1 default: compressed table, one thread per site,
-                // register gather (C3 developed: 13.6k MSUPS, 0.71 of copy BW)
+            else if (timed && wk.ctab_ok && v != 60) {
+                // default: compressed table, one thread per site, branch-free
+                // address selects, register gather (C3 developed: 13.6k MSUPS;
+                // the software-pipelined cp.async variant 66 measured 13.1k)
                 const uint32_t b0 = b & ~31u;
                 lbm_aa_odd_c<128, 4><<<unsigned((e - b0 + 127) / 128), 128, 0, s>>>(
                     F, wk.dtab.get<int16_t>(), wk.gbase.get<uint32_t>(), tab, wk.P, wk.PG, b, e, omega);
-            } else if (timed && wk.ctab_ok && v != 60) {
-                // default: gathers as cp.async into shared memory, software-pipelined
-                for_parts(b, e, [&](uint32_t c, uint32_t c1) { launch_aa_odd_async<256, 2>(wk, s, c, c1); });
             } else lbm_aa_odd<false, false, 128, 4><<<nb, 128, 0, s>>>(F, tab, wk.P, b, e, omega, ia, h);
         }
         if (timed) {
