@@ -1422,6 +1422,12 @@ class Engine {
         if (plain_variant == 0 || plain_variant == 24 || plain_variant == 43 || plain_variant == 59 ||
             plain_variant == 60)
             return false;
+        if (plain_variant == 67 || plain_variant == 68) {  // bounce-back as a signed offset in plane i
+            if (!(mid && wk.ctab_ok)) launch_tma<256, 2, 2, false, 6>(wk, s, b, e);
+            else if (plain_variant == 67) launch_tmc<256, 2, 2, 8198>(wk, s, b, e);
+            else launch_tmc<256, 2, 2, 12294>(wk, s, b, e);
+            return true;
+        }
         if (plain_variant >= 40 && plain_variant < 60) {
             if (mid && wk.ctab_ok) {
                 switch (plain_variant) {

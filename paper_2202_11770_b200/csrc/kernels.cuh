@@ -576,8 +576,17 @@ lbm_push_tmc(const double* __restrict__ fo, double* __restrict__ fn, const int16
                 : "+r"(t)
                 : "r"(esc), "l"(tab + uint64_t(i - 1) * P + s));
             const bool bb = d == kDeltaBounce;
-            const uintptr_t pb = reinterpret_cast<uintptr_t>(bb ? planes.p[inv(i)] : planes.p[i]);
-            double* dst = reinterpret_cast<double*>(pb) + (bb ? s : t);
+            double* dst;
+            if constexpr ((kHints & 8192) != 0) {
+                // one plane base per direction: a bounce-back target is site s
+                // of the inverse plane, i.e. s +- P from plane i (inverse pairs
+                // are adjacent indices), a signed 32-bit offset
+                const int32_t off = (i & 1) ? int32_t(P) : -int32_t(P);
+                dst = planes.p[i] + (bb ? int32_t(s) + off : int32_t(t));
+            } else {
+                const uintptr_t pb = reinterpret_cast<uintptr_t>(bb ? planes.p[inv(i)] : planes.p[i]);
+                dst = reinterpret_cast<double*>(pb) + (bb ? s : t);
+            }
             if constexpr ((kHints & 32) != 0) {
                 if (live) st_hint(dst, fpost, spolicy);
             } else {
