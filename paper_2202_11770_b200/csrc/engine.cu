@@ -355,6 +355,7 @@ struct WorkerDev {
     bool tma_ok = false;  // maps encoded (planes at least one box long)
     // compressed table of the mid-group plain range (kernels.cuh: compress_table)
     DevMem dtab, gbase;
+    DevMem ctile;  // tile-major copy of dtab/gbase (T = 256), see build_table_tiles
     uint64_t PG = 0;
     bool ctab_ok = false;
     // fused P2P halo: per shared slot the neighbour index and final flat
@@ -1271,21 +1272,40 @@ class Engine {
         lbm_push<false, T, B><<<unsigned((e - b + T - 1) / T), T, 0, s>>>(
             wk.f_old(), wk.f_new(), wk.tab.get<uint32_t>(), wk.P, b, e, omega, ia, HaloArgs{});
     }
+    // The tile-major compressed table (built on first use from dtab/gbase).
+    const int16_t* tile_table(WorkerDev& wk) {
+        if (!wk.ctile.p) {
+            constexpr uint32_t T = 256;
+            constexpr uint64_t kTab = uint64_t(kQ - 1) * T * 2 + uint64_t(kQ - 1) * (T / 32) * 4;
+            const uint32_t t0 = wk.n_edge / T, t1 = (wk.n_edge + wk.mp + T - 1) / T;
+            wk.ctile.alloc<unsigned char>(uint64_t(t1) * kTab);
+            const uint64_t work = uint64_t(t1 - t0) * (uint64_t(kQ - 1) * T + (kQ - 1) * (T / 32));
+            if (work)
+                build_table_tiles<T><<<unsigned((work + 255) / 256), 256, 0, wk.sM>>>(
+                    wk.dtab.get<int16_t>(), wk.gbase.get<uint32_t>(), wk.P, wk.PG, t0, t1, wk.ctile.get<unsigned char>());
+            CK(cudaGetLastError());
+            CK(cudaStreamSynchronize(wk.sM));
+        }
+        return wk.ctile.get<int16_t>();
+    }
+
     // Persistent TMA kernel over the compressed table (mid-group range only).
     template <int T, int S, int B, int H = 2>
     void launch_tmc(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e) {
         using L0 = PushTmaSmem<T, S, false>;
         // + the int16 delta planes per stage when H & 8
-        constexpr uint32_t kBytes = S * (L0::kF + ((H & 8) ? uint32_t(kQ - 1) * T * 2 : 0u) +
-                                         ((H & 136) == 136 ? uint32_t(kQ - 1) * (T / 32) * 4 : 0u)) + S * 8;
+        constexpr bool tm = (H & 16384) != 0;
+        constexpr uint32_t kBytes = S * (L0::kF + ((H & 8) || tm ? uint32_t(kQ - 1) * T * 2 : 0u) +
+                                         ((H & 136) == 136 || tm ? uint32_t(kQ - 1) * (T / 32) * 4 : 0u)) + S * 8;
         const int resident = resident_ctas(lbm_push_tmc<T, S, B, H>, wk.dev, T, kBytes);
-        const uint32_t base = b & ((H & 136) == 136 ? ~127u : ~31u);
+        const uint32_t base = b & ((H & 16384) ? ~uint32_t(T - 1) : ((H & 136) == 136 ? ~127u : ~31u));
         const uint32_t ntiles = (e - base + T - 1) / T;
         const unsigned grid = unsigned(std::min<uint32_t>(ntiles, uint32_t(resident)));
         check_tiles(wk, base, ntiles, T);
         Planes19 pl;
         for (int i = 0; i < kQ; ++i) pl.p[i] = wk.f_new() + uint64_t(i) * wk.P;
-        lbm_push_tmc<T, S, B, H><<<grid, T, kBytes, s>>>(wk.f_old(), wk.f_new(), wk.dtab.get<int16_t>(),
+        const int16_t* dt = (H & 16384) ? tile_table(wk) : wk.dtab.get<int16_t>();
+        lbm_push_tmc<T, S, B, H><<<grid, T, kBytes, s>>>(wk.f_old(), wk.f_new(), dt,
                                                               wk.gbase.get<uint32_t>(), wk.tab.get<uint32_t>(), wk.P,
                                                               wk.PG, b, e, omega, pl);
     }
@@ -1422,6 +1442,12 @@ class Engine {
         if (plain_variant == 0 || plain_variant == 24 || plain_variant == 43 || plain_variant == 59 ||
             plain_variant == 60)
             return false;
+        if (plain_variant == 69 || plain_variant == 70) {  // tile-major table, one bulk copy per tile
+            if (!(mid && wk.ctab_ok)) launch_tma<256, 2, 2, false, 6>(wk, s, b, e);
+            else if (plain_variant == 69) launch_tmc<256, 2, 2, 16386>(wk, s, b, e);
+            else launch_tmc<256, 2, 2, 16386 | 8192>(wk, s, b, e);
+            return true;
+        }
         if (plain_variant == 67 || plain_variant == 68) {  // bounce-back as a signed offset in plane i
             if (!(mid && wk.ctab_ok)) launch_tma<256, 2, 2, false, 6>(wk, s, b, e);
             else if (plain_variant == 67) launch_tmc<256, 2, 2, 8198>(wk, s, b, e);

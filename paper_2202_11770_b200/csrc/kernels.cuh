@@ -422,6 +422,29 @@ __global__ void compress_table(const uint32_t* __restrict__ tab, uint64_t P, uin
     if (lane == 0) gbase[uint64_t(i1) * PG + g] = uint32_t(uint64_t(base));
 }
 
+// Tile-major copy of the compressed table (lbm_push_tmc kHints & 16384):
+// tile j (sites [j*T, (j+1)*T)) = int16 deltas [18][T] then u32 group bases
+// [18][T/32], contiguous, so one bulk copy per tile brings all of it.
+template <int T>
+__global__ void build_table_tiles(const int16_t* __restrict__ dtab, const uint32_t* __restrict__ gbase, uint64_t P,
+                                  uint64_t PG, uint32_t tile0, uint32_t tile1, unsigned char* __restrict__ out) {
+    constexpr uint32_t kD = uint32_t(kQ - 1) * T, kB = uint32_t(kQ - 1) * (T / 32);
+    constexpr uint32_t kTab = kD * 2 + kB * 4;
+    const uint64_t idx = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint32_t per = kD + kB;
+    const uint64_t tile = tile0 + idx / per;
+    if (tile >= tile1) return;
+    const uint32_t e = uint32_t(idx % per);
+    unsigned char* o = out + tile * kTab;
+    if (e < kD) {
+        const uint32_t i = e / T, j = e % T;
+        reinterpret_cast<int16_t*>(o)[e] = dtab[uint64_t(i) * P + tile * T + j];
+    } else {
+        const uint32_t q = e - kD, i = q / (T / 32), g = q % (T / 32);
+        reinterpret_cast<uint32_t*>(o + kD * 2)[q] = gbase[uint64_t(i) * PG + tile * (T / 32) + g];
+    }
+}
+
 // TMA-pipelined persistent plain kernel reading the compressed table.  All
 // 32 lanes run the direction loop (bases travel by warp shuffle); only loads
 // and stores are predicated on the site being in range.
@@ -434,17 +457,22 @@ lbm_push_tmc(const double* __restrict__ fo, double* __restrict__ fn, const int16
     // kHints & 8: the tile's int16 deltas travel with its f planes (bulk
     // copies into the same stage) and the group bases are loaded one tile
     // ahead, so no table load latency is exposed in the direction loop
-    constexpr bool kDS = (kHints & 8) != 0;
+    // kHints & 16384: the tile's whole compressed table (deltas then group
+    // bases, the kGS shared-memory layout) is ONE contiguous block of a
+    // tile-major copy of the table (`dtab` then points at it; tiles aligned
+    // to T sites), so one bulk copy per tile brings it with the f planes
+    constexpr bool kTM = (kHints & 16384) != 0;
+    constexpr bool kDS = (kHints & 8) != 0 || kTM;
     // kHints & 128 (with 8): the group bases too — 18 bulk copies of T/32 u32
     // per tile, so the loop body issues no global load at all
-    constexpr bool kGS = kDS && (kHints & 128) != 0;
+    constexpr bool kGS = (kDS && (kHints & 128) != 0) || kTM;
     constexpr uint32_t kDOff = L::kF, kGOff = L::kF + uint32_t(kQ - 1) * T * 2;
     constexpr uint32_t kStage = L::kF + (kDS ? uint32_t(kQ - 1) * T * 2 : 0u) + (kGS ? uint32_t(kQ - 1) * (T / 32) * 4 : 0u);
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S * kStage);
     // warps cover aligned 32-site groups; kGS: tiles start on 128 sites so the
     // group-base copies are 16-byte aligned
-    const uint32_t base = begin & (kGS ? ~127u : ~31u);
+    const uint32_t base = begin & (kTM ? ~uint32_t(T - 1) : (kGS ? ~127u : ~31u));
     const uint32_t ntiles = (end - base + T - 1) / T;
     const uint32_t G = gridDim.x;
     const uint32_t tid = threadIdx.x;
@@ -468,12 +496,15 @@ lbm_push_tmc(const double* __restrict__ fo, double* __restrict__ fn, const int16
         mbar_expect_tx(&bar[st], kStage);
 #pragma unroll 1
         for (int i = 0; i < kQ; ++i) bulk_g2s(buf + i * T * 8, fo + uint64_t(i) * P + t0, T * 8, &bar[st], policy);
-        if constexpr (kDS) {
+        if constexpr (kTM) {
+            constexpr uint32_t kTab = uint32_t(kQ - 1) * T * 2 + uint32_t(kQ - 1) * (T / 32) * 4;
+            bulk_g2s(buf + kDOff, reinterpret_cast<const unsigned char*>(dtab) + (t0 / T) * kTab, kTab, &bar[st], policy);
+        } else if constexpr (kDS) {
 #pragma unroll 1
             for (int i = 0; i < kQ - 1; ++i)
                 bulk_g2s(buf + kDOff + i * T * 2, dtab + uint64_t(i) * P + t0, T * 2, &bar[st], policy);
         }
-        if constexpr (kGS) {
+        if constexpr (kGS && !kTM) {
 #pragma unroll 1
             for (int i = 0; i < kQ - 1; ++i)
                 bulk_g2s(buf + kGOff + i * (T / 32) * 4, gbase + uint64_t(i) * PG + (t0 >> 5), (T / 32) * 4, &bar[st],
