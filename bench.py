@@ -229,7 +229,8 @@ def timed_loop(sim, n, steps, warmup, bps, barrier, max_over_ranks, gpu, name, d
     l0 = sim.launch_count()
     d0 = sim.device_loop_seconds()
     with ClockSampler(gpu) as clk:
-        sim.run(steps)  # run() syncs its streams before returning
+        sim.run(steps)
+        sim.device_loop_seconds()  # run() returns while its last steps execute: wait inside the sampled window
     barrier()
     dev_s = max_over_ranks(sim.device_loop_seconds() - d0)
     k1 = sim.kernel_stats()

@@ -317,7 +317,8 @@ struct WorkerDev {
     int w = 0, dev = 0;
     cudaStream_t sE = nullptr, sM = nullptr;
     cudaEvent_t evSend = nullptr, evMid = nullptr, evEnd = nullptr;
-    cudaEvent_t evRun0 = nullptr, evRun1 = nullptr, evDone = nullptr;  // run() bracket + host-copy completion
+    // run() bracket + host-copy completion, one set per run in flight (Engine::run_par)
+    cudaEvent_t evRun0[2] = {}, evRun1[2] = {}, evDone[2] = {};
     PinnedMem h_obs;                                                   // observation rows, D2H target
     uint32_t n = 0, n_edge = 0, ep = 0, mp = 0;  // ranges: [0,ep) [ep,n_edge) [n_edge,n_edge+mp) [.., n)
     uint64_t P = 0;
@@ -332,8 +333,8 @@ struct WorkerDev {
     std::vector<uint32_t> obs_off;  // flattened offsets per iolet
     uint32_t n_obs = 0;
     uint64_t obs_row_base = 0, obs_rows = 0;
-    // kernel timing
-    std::vector<cudaEvent_t> tev;
+    // kernel timing (bulk launches), one list per run in flight
+    std::vector<cudaEvent_t> tev[2];
     // end of each step in flight (ring of Engine::kDepth): the run()
     // watchdog's progress marks
     std::vector<cudaEvent_t> prog;
@@ -364,7 +365,7 @@ struct WorkerDev {
     std::vector<std::array<double*, 2>> peer_f;  // by segment index
     std::vector<uint32_t*> peer_flags;           // by segment index
     std::vector<void*> ipc_opened;               // dist mode: handles to close
-    size_t tev_used = 0;
+    size_t tev_used[2] = {0, 0};
 
     double* f_old() const { return fbuf[old].get<double>(); }
     double* f_new() const { return fbuf[1 - old].get<double>(); }
@@ -384,7 +385,6 @@ class Engine {
     ncclComm_t comm = nullptr;
     std::vector<Capture> caps;
     Series series;
-    PinnedMem h_staged;  // per-run iolet values (run() staging)
     DevMem obs_gather;   // dist mode: every rank's observation rows (padded)
     PinnedMem h_gather;
     // device-side series (reduce_series_async): entry lists in series order
@@ -758,6 +758,10 @@ class Engine {
     }
 
     ~Engine() {
+        try {
+            complete();  // a run still in flight
+        } catch (...) {
+        }
         if (p2p_mode && dist && comm && !failed) {
             try {
                 dist_barrier();  // no neighbour still stores into our buffers
@@ -771,7 +775,8 @@ class Engine {
         for (auto& wp : W) {
             if (!wp) continue;
             cudaSetDevice(wp->dev);
-            for (auto e : wp->tev) cudaEventDestroy(e);
+            for (auto& v : wp->tev)
+                for (auto e : v) cudaEventDestroy(e);
             for (auto e : wp->prog) cudaEventDestroy(e);
             for (auto& pr : wp->tune_ev)
                 for (auto ev : pr)
@@ -779,9 +784,11 @@ class Engine {
             if (wp->evSend) cudaEventDestroy(wp->evSend);
             if (wp->evMid) cudaEventDestroy(wp->evMid);
             if (wp->evEnd) cudaEventDestroy(wp->evEnd);
-            if (wp->evRun0) cudaEventDestroy(wp->evRun0);
-            if (wp->evRun1) cudaEventDestroy(wp->evRun1);
-            if (wp->evDone) cudaEventDestroy(wp->evDone);
+            for (int b = 0; b < 2; ++b) {
+                if (wp->evRun0[b]) cudaEventDestroy(wp->evRun0[b]);
+                if (wp->evRun1[b]) cudaEventDestroy(wp->evRun1[b]);
+                if (wp->evDone[b]) cudaEventDestroy(wp->evDone[b]);
+            }
             if (wp->sE) cudaStreamDestroy(wp->sE);
             if (wp->sM) cudaStreamDestroy(wp->sM);
         }
@@ -842,9 +849,11 @@ class Engine {
         CK(cudaEventCreateWithFlags(&wk.evSend, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&wk.evMid, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&wk.evEnd, cudaEventDisableTiming));
-        CK(cudaEventCreate(&wk.evRun0));
-        CK(cudaEventCreate(&wk.evRun1));
-        CK(cudaEventCreateWithFlags(&wk.evDone, cudaEventDisableTiming));
+        for (int b = 0; b < 2; ++b) {
+            CK(cudaEventCreate(&wk.evRun0[b]));
+            CK(cudaEventCreate(&wk.evRun1[b]));
+            CK(cudaEventCreateWithFlags(&wk.evDone[b], cudaEventDisableTiming));
+        }
         cudaStream_t s = wk.sM;
 
         const WorkerPart& wp = part.parts[size_t(w)];
@@ -1567,14 +1576,16 @@ class Engine {
 
     // Records the start event of a timed bulk launch; returns its end event.
     cudaEvent_t timing_begin(WorkerDev& wk, cudaStream_t s) {
-        if (wk.tev_used + 2 > wk.tev.size())
+        std::vector<cudaEvent_t>& tv = wk.tev[run_par];
+        size_t& used = wk.tev_used[run_par];
+        if (used + 2 > tv.size())
             for (int k = 0; k < 2; ++k) {
                 cudaEvent_t ev;
                 CK(cudaEventCreate(&ev));
-                wk.tev.push_back(ev);
+                tv.push_back(ev);
             }
-        CK(cudaEventRecord(wk.tev[wk.tev_used++], s));
-        return wk.tev[wk.tev_used++];
+        CK(cudaEventRecord(tv[used++], s));
+        return tv[used++];
     }
 
     // fill_send_slots (engine.hpp:489-502), pull scheme only.
@@ -1628,21 +1639,9 @@ class Engine {
         } else if (!timed) {
             launch_plain(wk, s, b, e, ia, false);
         } else {
-            cudaEvent_t e0 = nullptr, e1 = nullptr;
-            if (kernel_timing) {
-                if (wk.tev_used + 2 > wk.tev.size()) {
-                    for (int k = 0; k < 2; ++k) {
-                        cudaEvent_t ev;
-                        CK(cudaEventCreate(&ev));
-                        wk.tev.push_back(ev);
-                    }
-                }
-                e0 = wk.tev[wk.tev_used++];
-                e1 = wk.tev[wk.tev_used++];
-                CK(cudaEventRecord(e0, s));
-            }
+            cudaEvent_t e1 = kernel_timing ? timing_begin(wk, s) : nullptr;
             launch_mid_tuned(wk, s, b, e, ia);
-            if (kernel_timing) CK(cudaEventRecord(e1, s));
+            if (e1) CK(cudaEventRecord(e1, s));
             plain_launches++;
             plain_sites += e - b;
         }
@@ -1782,9 +1781,37 @@ class Engine {
         }
     }
 
+    // ---- run(n): enqueue, then complete the previous run ---------------------
+    // A run is enqueued in full (steps, observation gather, series kernels and
+    // copies) and then the PREVIOUS run is completed — so consecutive run()
+    // calls keep the GPU busy while the host waits for, times and reduces the
+    // run before (its long iolets' series on the host overlap these steps).
+    // Every accessor of results completes the pending run first.  Runs that
+    // do host work inside the loop (captures) or reduce the series from a
+    // single host buffer complete before returning.
+    struct PendingRun {
+        bool active = false, timing = false, series = false;
+        int par = 0, ser_buf = 0;
+        uint64_t ser_rows = 0;
+        size_t caps_before = 0;
+        bool first_run = false;
+        std::chrono::steady_clock::time_point h0;
+    };
+    PendingRun pend;
+    int run_par = 0;                                     // event / staging set of the run being enqueued
+    PinnedMem h_staged2[2];                              // per-run iolet values, one per run in flight
+    std::chrono::steady_clock::time_point last_done{};  // host clock at the last completion
+
     void run(uint64_t n) {
         if (failed) runtime_error("engine: an exchange failure left this simulation unusable");
         NvtxRange nv("splbcu::run");
+        bool has_caps = false;
+        if (prm.capture_period > 0)
+            for (uint64_t st = steps_run == 0 ? 0 : steps_run + 1; st <= steps_run + n && !has_caps; ++st)
+                has_caps = st % prm.capture_period == 0;
+        const bool sync_run = has_caps || (prm.observe_iolets && !dev_series);
+        if (sync_run) complete();
+        const int par = run_par;
         const size_t caps_before = caps.size();
         const bool first_run = steps_run == 0;
         prepare_records(n);
@@ -1794,12 +1821,12 @@ class Engine {
                     CK(cudaSetDevice(wp->dev));
                     record_state(*wp, wp->sM, 0, wp->f_old());
                 }
-        // host staging of the per-step iolet values (engine.hpp:332-341)
-        // into a pinned buffer, copied stream-ordered ahead of the step loop (the
-        // previous run() has completed, so the buffer is free to overwrite)
+        // host staging of the per-step iolet values (engine.hpp:332-341) into
+        // this run's pinned buffer (the run that used it before has completed),
+        // copied stream-ordered ahead of the step loop
         const size_t n_io = bcs.size();
         const size_t n_staged = std::max<size_t>(n * n_io, 1);
-        double* staged = h_staged.reserve<double>(n_staged);
+        double* staged = h_staged2[par].reserve<double>(n_staged);
         staged[0] = 0.0;
         for (uint64_t k = 0; k < n; ++k) {
             const double t = double(steps_run + k + 1) * prm.dt_s;
@@ -1813,17 +1840,14 @@ class Engine {
             CK(cudaSetDevice(wp->dev));
             double* d = wp->staged.reserve<double>(n_staged);
             CK(cudaMemcpyAsync(d, staged, n_staged * sizeof(double), cudaMemcpyHostToDevice, wp->sM));
-            wp->tev_used = 0;
+            wp->tev_used[par] = 0;
         }
-        std::vector<cudaEvent_t> t0(W.size(), nullptr), t1(W.size(), nullptr), done(W.size(), nullptr);
-        for (size_t w = 0; w < W.size(); ++w)
-            if (W[w]) t0[w] = W[w]->evRun0, t1[w] = W[w]->evRun1, done[w] = W[w]->evDone;
         const auto h0 = std::chrono::steady_clock::now();
-        for (size_t w = 0; w < W.size(); ++w)
-            if (W[w]) {
-                CK(cudaSetDevice(W[w]->dev));
-                CK(cudaEventRecord(t0[w], W[w]->sM));
-                CK(cudaStreamWaitEvent(W[w]->sE, t0[w], 0));
+        for (auto& wp : W)
+            if (wp) {
+                CK(cudaSetDevice(wp->dev));
+                CK(cudaEventRecord(wp->evRun0[par], wp->sM));
+                CK(cudaStreamWaitEvent(wp->sE, wp->evRun0[par], 0));
             }
         last_progress = std::chrono::steady_clock::now();
         try {
@@ -1838,43 +1862,68 @@ class Engine {
             if (e.kind == ErrKind::Comm) throw Error(ErrKind::Comm, "worker " + std::to_string(rank) + ": " + e.what());
             throw;
         }
-        for (size_t w = 0; w < W.size(); ++w)
-            if (W[w]) {
-                CK(cudaSetDevice(W[w]->dev));
-                CK(cudaEventRecord(t1[w], W[w]->sM));
-                // this run's observation rows, behind the loop: one device
-                // all-gather (dist mode) and one async copy into pinned memory
-                WorkerDev& wk = *W[w];
-                if (prm.observe_iolets && dist) {
-                    const uint64_t per = obs_gather_per(wk);
-                    CK(cudaStreamWaitEvent(wk.sE, t1[w], 0));
-                    double* dr = obs_gather.reserve<double>(per * uint64_t(nranks));
-                    NK(nccl().AllGather(wk.obs_buf.get<double>(), dr, per, ncclDouble, comm, wk.sE));
-                    if (dev_series) {
-                        reduce_series_async(wk, wk.sE, dr, per, ser_next);
-                    } else {
-                        double* h = h_gather.reserve<double>(per * uint64_t(nranks));
-                        CK(cudaMemcpyAsync(h, dr, per * uint64_t(nranks) * 8, cudaMemcpyDeviceToHost, wk.sE));
-                    }
-                    CK(cudaEventRecord(done[w], wk.sE));
-                    continue;
+        const bool series = prm.observe_iolets && dev_series;
+        for (auto& wp : W) {
+            if (!wp) continue;
+            WorkerDev& wk = *wp;
+            CK(cudaSetDevice(wk.dev));
+            CK(cudaEventRecord(wk.evRun1[par], wk.sM));
+            // this run's observation rows, behind the loop: one device
+            // all-gather (dist mode) and one async copy into pinned memory
+            if (prm.observe_iolets && dist) {
+                const uint64_t per = obs_gather_per(wk);
+                CK(cudaStreamWaitEvent(wk.sE, wk.evRun1[par], 0));
+                double* dr = obs_gather.reserve<double>(per * uint64_t(nranks));
+                NK(nccl().AllGather(wk.obs_buf.get<double>(), dr, per, ncclDouble, comm, wk.sE));
+                if (dev_series) {
+                    reduce_series_async(wk, wk.sE, dr, per, ser_next);
+                } else {
+                    double* h = h_gather.reserve<double>(per * uint64_t(nranks));
+                    CK(cudaMemcpyAsync(h, dr, per * uint64_t(nranks) * 8, cudaMemcpyDeviceToHost, wk.sE));
                 }
-                if (prm.observe_iolets && dev_series) {
-                    reduce_series_async(wk, wk.sM, wk.obs_buf.get<double>(), 0, ser_next);
-                    CK(cudaEventRecord(done[w], wk.sM));
-                    continue;
-                }
-                const size_t nb = prm.observe_iolets ? 3 * wk.obs_rows * wk.n_obs : 0;
-                if (nb) {
-                    double* h = wk.h_obs.reserve<double>(nb);
-                    CK(cudaMemcpyAsync(h, wk.obs_buf.get<double>(), nb * 8, cudaMemcpyDeviceToHost, wk.sM));
-                }
-                CK(cudaEventRecord(done[w], wk.sM));
+                CK(cudaEventRecord(wk.evDone[par], wk.sE));
+                continue;
             }
-        // the previous run's long iolets, on the host while these steps run
-        flush_series();
+            if (series) {
+                reduce_series_async(wk, wk.sM, wk.obs_buf.get<double>(), 0, ser_next);
+                CK(cudaEventRecord(wk.evDone[par], wk.sM));
+                continue;
+            }
+            const size_t nb = prm.observe_iolets ? 3 * wk.obs_rows * wk.n_obs : 0;
+            if (nb) {
+                double* h = wk.h_obs.reserve<double>(nb);
+                CK(cudaMemcpyAsync(h, wk.obs_buf.get<double>(), nb * 8, cudaMemcpyDeviceToHost, wk.sM));
+            }
+            CK(cudaEventRecord(wk.evDone[par], wk.sM));
+        }
+        // the previous run completes while these steps execute
+        complete();
+        steps_run += n;
+        pend.active = true;
+        pend.par = par;
+        pend.timing = kernel_timing;
+        pend.series = series;
+        pend.ser_buf = ser_next;
+        pend.ser_rows = steps_run + 1;
+        pend.caps_before = caps_before;
+        pend.first_run = first_run;
+        pend.h0 = h0;
+        if (series) ser_next ^= 1;
+        run_par ^= 1;
+        if (sync_run) complete();
+    }
+
+    // Completes the run in flight (if any): waits under the watchdog, adds its
+    // device / host loop time and bulk-kernel times, reduces its series rows
+    // and (dist mode) assembles its captures across ranks.
+    void complete() {
+        if (!pend.active) return;
+        pend.active = false;
+        const int par = pend.par;
+        std::vector<cudaEvent_t> done(W.size(), nullptr);
+        for (size_t w = 0; w < W.size(); ++w)
+            if (W[w]) done[w] = W[w]->evDone[par];
         try {
-            for (uint64_t k = n > kDepth ? n - kDepth : 0; k < n; ++k) wait_step(k);
             wait_all(done);
         } catch (const Error& e) {
             if (e.kind == ErrKind::Comm) throw Error(ErrKind::Comm, "worker " + std::to_string(rank) + ": " + e.what());
@@ -1882,33 +1931,35 @@ class Engine {
         }
         const auto h1 = std::chrono::steady_clock::now();
         double dmax = 0.0;
-        for (size_t w = 0; w < W.size(); ++w)
-            if (W[w]) {
+        for (auto& wp : W)
+            if (wp) {
                 float ms = 0.f;
-                CK(cudaEventElapsedTime(&ms, t0[w], t1[w]));
+                CK(cudaEventElapsedTime(&ms, wp->evRun0[par], wp->evRun1[par]));
                 dmax = std::max(dmax, double(ms) * 1e-3);
-                if (kernel_timing)
-                    for (size_t q = 0; q + 1 < W[w]->tev_used; q += 2) {
+                if (pend.timing)
+                    for (size_t q = 0; q + 1 < wp->tev_used[par]; q += 2) {
                         float kms = 0.f;
-                        CK(cudaEventElapsedTime(&kms, W[w]->tev[q], W[w]->tev[q + 1]));
+                        CK(cudaEventElapsedTime(&kms, wp->tev[par][q], wp->tev[par][q + 1]));
                         plain_s += double(kms) * 1e-3;
                     }
             }
         dev_loop_s += dmax;
-        loop_s += std::chrono::duration<double>(h1 - h0).count();
-        steps_run += n;
-        if (prm.observe_iolets && dev_series) {
+        // host loop time: from this run's enqueue (or the previous completion,
+        // when the runs overlapped) to its completion
+        loop_s += std::chrono::duration<double>(h1 - std::max(pend.h0, last_done)).count();
+        last_done = h1;
+        if (pend.series) {
             ser_pending = true;
-            ser_pend_buf = ser_next;
-            ser_pend_rows = steps_run + 1;
-            ser_next ^= 1;
+            ser_pend_buf = pend.ser_buf;
+            ser_pend_rows = pend.ser_rows;
+            flush_series();  // the long iolets, on the host while the next run executes
         } else {
             assemble_series();
         }
         if (dist) {
             // captures of this run hold this rank's sites only: assemble them
             for (size_t c = 0; c < caps.size(); ++c)
-                if (c >= caps_before || (first_run && caps[c].step == 0))
+                if (c >= pend.caps_before || (pend.first_run && caps[c].step == 0))
                     allreduce_host_sum(caps[c].fields.data(), caps[c].fields.size());
         }
     }
@@ -2051,18 +2102,7 @@ class Engine {
         IoletArgs ia{wk.io_geo.get<IoletDev>(), staged, coords};
         const bool remote = edge && p2p_mode && wk.shared > 0;
         const HaloArgs h = remote ? halo_args(wk) : HaloArgs{};
-        cudaEvent_t e0 = nullptr, e1 = nullptr;
-        if (timed && kernel_timing) {
-            if (wk.tev_used + 2 > wk.tev.size())
-                for (int k = 0; k < 2; ++k) {
-                    cudaEvent_t ev;
-                    CK(cudaEventCreate(&ev));
-                    wk.tev.push_back(ev);
-                }
-            e0 = wk.tev[wk.tev_used++];
-            e1 = wk.tev[wk.tev_used++];
-            CK(cudaEventRecord(e0, s));
-        }
+        cudaEvent_t e1 = timed && kernel_timing ? timing_begin(wk, s) : nullptr;
         double* F = wk.f_old();
         const uint32_t* tab = wk.tab.get<uint32_t>();
         const unsigned nb = blocks_for(e - b, 128);
@@ -2098,7 +2138,7 @@ class Engine {
             } else lbm_aa_odd<false, false, 128, 4><<<nb, 128, 0, s>>>(F, tab, wk.P, b, e, omega, ia, h);
         }
         if (timed) {
-            if (kernel_timing) CK(cudaEventRecord(e1, s));
+            if (e1) CK(cudaEventRecord(e1, s));
             plain_launches++;
             plain_sites += e - b;
         }
@@ -2559,15 +2599,27 @@ uint64_t Simulation::n_sites() const { return e_->n_global; }
 uint64_t Simulation::series_d2h_bytes() const { return e_->series_d2h_bytes(); }
 void Simulation::run(uint64_t n) { e_->run(n); }
 uint64_t Simulation::steps_run() const { return e_->steps_run; }
-double Simulation::step_loop_seconds() const { return e_->loop_s; }
-double Simulation::device_loop_seconds() const { return e_->dev_loop_s; }
-double Simulation::plain_kernel_seconds() const { return e_->plain_s; }
+double Simulation::step_loop_seconds() const {
+    e_->complete();
+    return e_->loop_s;
+}
+double Simulation::device_loop_seconds() const {
+    e_->complete();
+    return e_->dev_loop_s;
+}
+double Simulation::plain_kernel_seconds() const {
+    e_->complete();
+    return e_->plain_s;
+}
 uint64_t Simulation::plain_kernel_launches() const { return e_->plain_launches; }
 uint64_t Simulation::plain_kernel_sites() const { return e_->plain_sites; }
 void Simulation::set_kernel_timing(bool on) { e_->kernel_timing = on; }
 uint64_t Simulation::launch_count() const { return e_->launches; }
 int Simulation::bulk_kernel() const { return e_->bulk_kernel(); }
-void Simulation::snapshot(double* out) { e_->snapshot(out); }
+void Simulation::snapshot(double* out) {
+    e_->complete();
+    e_->snapshot(out);
+}
 int Simulation::n_workers() const { return e_->prm.workers; }
 bool Simulation::is_local(int w) const {
     return w >= 0 && w < e_->prm.workers && e_->W[size_t(w)] != nullptr;
@@ -2577,12 +2629,25 @@ void Simulation::store_shape(int w, uint32_t* n, uint32_t* shared) const {
     if (n) *n = wk.n;
     if (shared) *shared = wk.shared;
 }
-void Simulation::get_f(int w, int which, double* host) { e_->get_f(w, which, host); }
-void Simulation::set_f(int w, int which, const double* host) { e_->set_f(w, which, host); }
-ExportedMap Simulation::export_map(int w) { return e_->export_map(w); }
+void Simulation::get_f(int w, int which, double* host) {
+    e_->complete();
+    e_->get_f(w, which, host);
+}
+void Simulation::set_f(int w, int which, const double* host) {
+    e_->complete();
+    e_->set_f(w, which, host);
+}
+ExportedMap Simulation::export_map(int w) {
+    e_->complete();
+    return e_->export_map(w);
+}
 const Partition& Simulation::partition() const { return e_->part; }
-const std::vector<Capture>& Simulation::captures() const { return e_->caps; }
+const std::vector<Capture>& Simulation::captures() const {
+    e_->complete();
+    return e_->caps;
+}
 const Series& Simulation::series() const {
+    e_->complete();
     e_->flush_series();
     return e_->series;
 }
