@@ -1971,7 +1971,10 @@ class Engine {
     // dist mode, fails the run when no step has completed for
     // exchange_timeout_s (a dead or stuck neighbour), checking NCCL's
     // asynchronous errors while it waits.
-    static constexpr uint64_t kDepth = 64;
+    // 16 steps keep the GPU fed (>= 16 x the shortest step) while a stuck
+    // neighbour can never fill the streams' command queues: the host always
+    // reaches the watchdog instead of blocking inside a launch
+    static constexpr uint64_t kDepth = 16;
     bool failed = false;  // an exchange failure left the streams unusable
     std::chrono::steady_clock::time_point last_progress;
 
