@@ -357,6 +357,9 @@ struct WorkerDev {
     // compressed table of the mid-group plain range (kernels.cuh: compress_table)
     DevMem dtab, gbase;
     DevMem ctile;  // tile-major copy of dtab/gbase (T = 256), see build_table_tiles
+    DevMem rtab;   // run-length table of the mid-group plain range (T = 256), see build_run_table
+    bool rtab_ok = false;
+    uint32_t rtab_escaped = 0;  // (direction, group)s read from the u32 table
     uint64_t PG = 0;
     bool ctab_ok = false;
     // fused P2P halo: per shared slot the neighbour index and final flat
@@ -1089,6 +1092,25 @@ class Engine {
                 wk.dtab.release();
                 wk.gbase.release();
             }
+            // run-length table (kernels.cuh: build_run_table), tiles of 256
+            constexpr uint32_t T = 256;
+            const uint32_t t0 = b0 / T, t1 = (b1 + T - 1) / T;
+            unsigned char* rt = wk.rtab.alloc<unsigned char>(uint64_t(t1) * RunTab<T>::kBytes);
+            unsigned* rc = cerr.alloc<unsigned>(2);
+            CK(cudaMemsetAsync(rc, 0, 2 * sizeof(unsigned), s));
+            const uint64_t warps = uint64_t(t1 - t0) * (kQ - 1) * RunTab<T>::kG;
+            build_run_table<T><<<unsigned((warps * 32 + 255) / 256), 256, 0, s>>>(wk.tab.get<uint32_t>(), wk.P, b0, b1,
+                                                                                  t0, t1, rt, rc, rc + 1);
+            CK(cudaGetLastError());
+            unsigned hr[2] = {0, 0};
+            CK(cudaMemcpyAsync(hr, rc, sizeof(hr), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            wk.rtab_ok = hr[0] == 0;
+            wk.rtab_escaped = hr[1];
+            if (std::getenv("SPLBCU_VERBOSE"))
+                std::fprintf(stderr, "[splbcu] worker %d: run table %s, %u of %llu (direction, group)s escaped\n", wk.w,
+                             wk.rtab_ok ? "on" : "off", hr[1], (unsigned long long)(warps));
+            if (!wk.rtab_ok) wk.rtab.release();
         }
         CK(cudaStreamSynchronize(s));
     }
@@ -1319,6 +1341,21 @@ class Engine {
                                                               wk.PG, b, e, omega, pl);
     }
 
+    // Persistent TMA kernel over the run-length table (mid-group range only).
+    template <int T, int S, int B>
+    void launch_run(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e) {
+        constexpr uint32_t kBytes = S * (uint32_t(kQ) * T * 8 + RunTab<T>::kBytes) + S * 8;
+        const int resident = resident_ctas(lbm_push_run<T, S, B>, wk.dev, T, kBytes);
+        const uint32_t base = b & ~uint32_t(T - 1);
+        const uint32_t ntiles = (e - base + T - 1) / T;
+        const unsigned grid = unsigned(std::min<uint32_t>(ntiles, uint32_t(resident)));
+        check_tiles(wk, base, ntiles, T);
+        Planes19 pl;
+        for (int i = 0; i < kQ; ++i) pl.p[i] = wk.f_new() + uint64_t(i) * wk.P;
+        lbm_push_run<T, S, B><<<grid, T, kBytes, s>>>(wk.f_old(), wk.f_new(), wk.rtab.get<unsigned char>(),
+                                                      wk.tab.get<uint32_t>(), wk.P, b, e, omega, pl);
+    }
+
     // Which kernel the bulk (mid) plain range launches now on this process's
     // first worker: 0 just-in-time table loads (<256,2,2,6>), 1 the prefetch
     // kernel (<256,2,2,4102>), -1 any other (forced variant, u32 table).
@@ -1427,7 +1464,7 @@ class Engine {
         (void)v;
         return true;
 #else
-        return v == 0 || v == 24 || v == 43 || v == 59 || v == 60;
+        return v == 0 || v == 24 || v == 43 || v == 59 || v == 60 || v == 71;
 #endif
     }
     void launch_plain(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia, bool mid) {
@@ -1435,6 +1472,7 @@ class Engine {
         if (launch_tuning_variant(wk, s, b, e, ia, mid)) return;
 #endif
         if (plain_variant == 24) return launch_tma<256, 2, 2, false, 2>(wk, s, b, e);
+        if (plain_variant == 71 && mid && wk.rtab_ok) return launch_run<256, 2, 2>(wk, s, b, e);
         if (mid && wk.ctab_ok) {
             const bool pf = plain_variant == 59 || (plain_variant == 0 && wk.mid_pick == 1);
             if (pf) launch_tmc<256, 2, 2, 4102>(wk, s, b, e);
@@ -1449,7 +1487,7 @@ class Engine {
     // defaults, profiles/r01_sweep_*.log).  Returns false for the built-in ones.
     bool launch_tuning_variant(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia, bool mid) {
         if (plain_variant == 0 || plain_variant == 24 || plain_variant == 43 || plain_variant == 59 ||
-            plain_variant == 60)
+            plain_variant == 60 || plain_variant == 71)
             return false;
         if (plain_variant == 69 || plain_variant == 70) {  // tile-major table, one bulk copy per tile
             if (!(mid && wk.ctab_ok)) launch_tma<256, 2, 2, false, 6>(wk, s, b, e);

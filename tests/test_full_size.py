@@ -57,7 +57,7 @@ def test_c2_full_size_kernels_and_workers_agree(product):
     noise = cases.noise_for(d.n_sites(), 20240808, 0.01)
     runs = {}
     for name, variant, workers in (("default", None, 1), ("prefetch", "59", 1), ("u32", "24", 1),
-                                   ("w3", None, 3)):
+                                   ("runs", "71", 1), ("w3", None, 3)):
         prm = P.EngineParams(tau=0.8, dt_s=5e-4, workers=workers, devices=[0], observe_iolets=True)
         runs[name] = _run(P, d, bcs, prm, 200, variant, noise)
     want = runs["default"][0]
@@ -80,7 +80,7 @@ def test_c3_full_size_kernels_and_workers_agree(product):
     bcs = P.BCSet(ents)
     runs = {}
     for name, variant, workers in (("default", None, 1), ("jit", "43", 1), ("prefetch", "59", 1), ("u32", "24", 1),
-                                   ("w2", None, 2)):
+                                   ("runs", "71", 1), ("w2", None, 2)):
         prm = P.EngineParams(tau=0.8, dt_s=1.0, workers=workers, devices=[0])
         runs[name] = _run(P, d, bcs, prm, 40, variant)
     want = runs["default"][0]
