@@ -1836,6 +1836,7 @@ class Engine {
         std::chrono::steady_clock::time_point h0;
     };
     PendingRun pend;
+    const bool sync_runs = std::getenv("SPLBCU_SYNC_RUN") != nullptr;  // A/B knob: every run completes before returning
     int run_par = 0;                                     // event / staging set of the run being enqueued
     PinnedMem h_staged2[2];                              // per-run iolet values, one per run in flight
     std::chrono::steady_clock::time_point last_done{};  // host clock at the last completion
@@ -1847,7 +1848,7 @@ class Engine {
         if (prm.capture_period > 0)
             for (uint64_t st = steps_run == 0 ? 0 : steps_run + 1; st <= steps_run + n && !has_caps; ++st)
                 has_caps = st % prm.capture_period == 0;
-        const bool sync_run = has_caps || (prm.observe_iolets && !dev_series);
+        const bool sync_run = has_caps || (prm.observe_iolets && !dev_series) || sync_runs;
         if (sync_run) complete();
         const int par = run_par;
         const size_t caps_before = caps.size();
