@@ -375,6 +375,20 @@ struct Planes19 {
     double* p[kQ];
 };
 
+// The rare escape of a compressed table (a target the compressed form cannot
+// express) reads the u32 table.  Only a warp with an escaping lane issues the
+// load: a predicated-off load still holds its destination register on the
+// scoreboard until the load/store pipe hands it back, and in the store loop
+// that put every direction behind the queue of scattered stores (ncu, C3 in a
+// developed flow: a third of all stall samples on the first use of the
+// target; escapes are 0.01 % of the links).
+__device__ __forceinline__ uint32_t escape_load(uint32_t t, bool esc, const uint32_t* p) {
+    if (__any_sync(__activemask(), esc)) {
+        if (esc) t = __ldg(p);
+    }
+    return t;
+}
+
 // ---- compressed neighbour table (mid-group plain sites) --------------------
 // The mid-group plain range has only ToLocal and bounce-back links (shared
 // slots occur only at edge sites, iolet links only at iolet sites).  Inside a
@@ -598,14 +612,12 @@ lbm_push_tmc(const double* __restrict__ fo, double* __restrict__ fn, const int16
             const double fpost = relax(f[i], feq[i], omega);
             const uint32_t b = __shfl_sync(0xffffffffu, breg, i - 1);
             const int d = dl[i - 1];
-            // branch-free: the rare escape is a predicated load (inline PTX so
-            // no divergent block is formed), the bounce case a select; plane
-            // base addresses come from the constant bank (kernel params)
+            // the rare escape is a warp-uniform branch around the load, the
+            // bounce case a select; plane base addresses come from the
+            // constant bank (kernel params)
             uint32_t t = b + uint32_t(lane) + uint32_t(d);
             const uint32_t esc = (d == kDeltaEscape) && live;
-            asm("{\n .reg .pred p;\n setp.ne.u32 p, %1, 0;\n @p ld.global.nc.u32 %0, [%2];\n}"
-                : "+r"(t)
-                : "r"(esc), "l"(tab + uint64_t(i - 1) * P + s));
+            t = escape_load(t, esc != 0u, tab + uint64_t(i - 1) * P + s);
             const bool bb = d == kDeltaBounce;
             double* dst;
             if constexpr ((kHints & 8192) != 0) {
@@ -763,9 +775,7 @@ lbm_push_run(const double* __restrict__ fo, double* __restrict__ fn, const unsig
             const int r = __popc((Rm | 1u) & le) - 1;
             uint32_t t = rds[(i - 1) * RT::kG * kRunK + r] + lane;
             const uint32_t esc = Rm == 0u && live;
-            asm("{\n .reg .pred p;\n setp.ne.u32 p, %1, 0;\n @p ld.global.nc.u32 %0, [%2];\n}"
-                : "+r"(t)
-                : "r"(esc), "l"(tab + uint64_t(i - 1) * P + s));
+            t = escape_load(t, esc != 0u, tab + uint64_t(i - 1) * P + s);
             const bool bb = Rm == 0u ? t >= kSpecial : ((Bm >> lane) & 1u) != 0u;
             const int32_t off = (i & 1) ? int32_t(P) : -int32_t(P);
             double* dst = planes.p[i] + (bb ? int32_t(s) + off : int32_t(t));
@@ -1170,9 +1180,7 @@ lbm_aa_odd_c(double* __restrict__ F, const int16_t* __restrict__ dtab, const uin
         const int dj = d[j - 1];
         uint32_t t = b + uint32_t(lane) + uint32_t(dj);
         const uint32_t esc = (dj == kDeltaEscape) && live;
-        asm("{\n .reg .pred p;\n setp.ne.u32 p, %1, 0;\n @p ld.global.nc.u32 %0, [%2];\n}"
-            : "+r"(t)
-            : "r"(esc), "l"(tab + uint64_t(j - 1) * P + s));
+        t = escape_load(t, esc != 0u, tab + uint64_t(j - 1) * P + s);
         bb = dj == kDeltaBounce;
         return bb ? s : t;
     };
@@ -1276,9 +1284,7 @@ lbm_aa_odd_async(double* __restrict__ F, const int16_t* __restrict__ dtab, const
         const int d = ds[(j - 1) * T + tid];
         uint32_t t = bs[(j - 1) * (T / 32) + warp] + uint32_t(lane) + uint32_t(d);
         const uint32_t esc = d == kDeltaEscape;
-        asm("{\n .reg .pred p;\n setp.ne.u32 p, %1, 0;\n @p ld.global.nc.u32 %0, [%2];\n}"
-            : "+r"(t)
-            : "r"(esc), "l"(tab + uint64_t(j - 1) * P + s));
+        t = escape_load(t, esc != 0u, tab + uint64_t(j - 1) * P + s);
         const bool bb = d == kDeltaBounce;
         const uintptr_t pb = reinterpret_cast<uintptr_t>(bb ? planes.p[inv(j)] : planes.p[j]);
         return reinterpret_cast<double*>(pb) + (bb ? s : t);
