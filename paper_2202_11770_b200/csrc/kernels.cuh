@@ -375,13 +375,10 @@ struct Planes19 {
     double* p[kQ];
 };
 
-// The rare escape of a compressed table (a target the compressed form cannot
-// express) reads the u32 table.  Only a warp with an escaping lane issues the
-// load: a predicated-off load still holds its destination register on the
-// scoreboard until the load/store pipe hands it back, and in the store loop
-// that put every direction behind the queue of scattered stores (ncu, C3 in a
-// developed flow: a third of all stall samples on the first use of the
-// target; escapes are 0.01 % of the links).
+// The escape of a run-length table entry (a group with more runs than the
+// record holds) reads the u32 table; the condition is warp-uniform there, so
+// a branch around the load is free (for the per-lane escapes of the delta
+// table a predicated load measured faster: `lbm_push_tmc`).
 __device__ __forceinline__ uint32_t escape_load(uint32_t t, bool esc, const uint32_t* p) {
     if (__any_sync(__activemask(), esc)) {
         if (esc) t = __ldg(p);
@@ -612,12 +609,15 @@ lbm_push_tmc(const double* __restrict__ fo, double* __restrict__ fn, const int16
             const double fpost = relax(f[i], feq[i], omega);
             const uint32_t b = __shfl_sync(0xffffffffu, breg, i - 1);
             const int d = dl[i - 1];
-            // the rare escape is a warp-uniform branch around the load, the
-            // bounce case a select; plane base addresses come from the
-            // constant bank (kernel params)
+            // branch-free: the rare escape is a predicated load (inline PTX so
+            // no divergent block is formed; a warp-uniform branch around it
+            // measured 8 % slower from rest), the bounce case a select; plane
+            // base addresses come from the constant bank (kernel params)
             uint32_t t = b + uint32_t(lane) + uint32_t(d);
             const uint32_t esc = (d == kDeltaEscape) && live;
-            t = escape_load(t, esc != 0u, tab + uint64_t(i - 1) * P + s);
+            asm("{\n .reg .pred p;\n setp.ne.u32 p, %1, 0;\n @p ld.global.nc.u32 %0, [%2];\n}"
+                : "+r"(t)
+                : "r"(esc), "l"(tab + uint64_t(i - 1) * P + s));
             const bool bb = d == kDeltaBounce;
             double* dst;
             if constexpr ((kHints & 8192) != 0) {
@@ -1180,7 +1180,9 @@ lbm_aa_odd_c(double* __restrict__ F, const int16_t* __restrict__ dtab, const uin
         const int dj = d[j - 1];
         uint32_t t = b + uint32_t(lane) + uint32_t(dj);
         const uint32_t esc = (dj == kDeltaEscape) && live;
-        t = escape_load(t, esc != 0u, tab + uint64_t(j - 1) * P + s);
+        asm("{\n .reg .pred p;\n setp.ne.u32 p, %1, 0;\n @p ld.global.nc.u32 %0, [%2];\n}"
+            : "+r"(t)
+            : "r"(esc), "l"(tab + uint64_t(j - 1) * P + s));
         bb = dj == kDeltaBounce;
         return bb ? s : t;
     };
