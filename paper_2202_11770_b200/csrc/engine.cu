@@ -339,17 +339,20 @@ struct WorkerDev {
     // watchdog's progress marks
     std::vector<cudaEvent_t> prog;
     // Online choice of the bulk (mid) plain kernel: just-in-time table loads
-    // (mid_pick 0) or the prefetch kernel (1).  Both give the same bits; which
+    // (mid_pick 0), the prefetch kernel (1) or the run-length table (2).  All
+    // give the same bits; which
     // is faster depends on the geometry and on the flow (from rest vs developed,
     // DESIGN §3), so every kTuneEvery mid launches the next 2 x kTuneReps
     // launches alternate the two under CUDA events and the faster is kept.
     static constexpr int kTuneReps = 3;
+    static constexpr int kCand = 3;  // bulk-kernel candidates: 0 just-in-time, 1 prefetch, 2 run table
     static constexpr uint64_t kTuneEvery = 500;
     int mid_pick = 0;
     int tune_phase = 0;         // 0: exploit; k > 0: measuring launch k-1
     bool tune_pending = false;  // measured, events not read yet
     uint64_t mid_launches = 0;
-    cudaEvent_t tune_ev[2 * kTuneReps][2] = {};
+    cudaEvent_t tune_ev[kCand * kTuneReps][2] = {};
+    int n_cand = 2;  // candidates available on this worker (3 with a run table)
     // 2-D tensor maps over the direction-major planes (per f buffer, table)
     CUtensorMap tm_f[2][2];  // [buffer][box T variant: 0 -> 128 sites, 1 -> 256 sites]
     CUtensorMap tm_t[2];
@@ -1106,6 +1109,7 @@ class Engine {
             CK(cudaMemcpyAsync(hr, rc, sizeof(hr), cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
             wk.rtab_ok = hr[0] == 0;
+            wk.n_cand = wk.rtab_ok && wk.ctab_ok ? 3 : 2;
             wk.rtab_escaped = hr[1];
             if (std::getenv("SPLBCU_VERBOSE"))
                 std::fprintf(stderr, "[splbcu] worker %d: run table %s, %u of %llu (direction, group)s escaped\n", wk.w,
@@ -1365,6 +1369,7 @@ class Engine {
             if (!wp->ctab_ok) return -1;
             if (plain_variant == 43) return 0;
             if (plain_variant == 59) return 1;
+            if (plain_variant == 71) return wp->rtab_ok ? 2 : -1;
             return plain_variant == 0 ? wp->mid_pick : -1;
         }
         return -1;
@@ -1400,7 +1405,7 @@ class Engine {
 
     // The bulk plain launch through the online kernel choice (WorkerDev::mid_pick).
     // Measurement windows start at every multiple of kTuneEvery bulk launches
-    // (0, 500, 1000, ...): 2 x kTuneReps launches alternate the two kernels
+    // (0, 500, 1000, ...): n_cand x kTuneReps launches cycle through the candidates
     // under CUDA events, each kernel's fastest launch counts (the first launch
     // of a template also carries its one-time setup), and the faster kernel
     // is kept from the moment the events have completed.
@@ -1412,17 +1417,21 @@ class Engine {
             ++wk.mid_launches;
             return;
         }
+        const int nc = wk.n_cand, nlaunch = nc * WorkerDev::kTuneReps;
         if (wk.tune_pending) {
             // read the measurement once its last launch has finished (no sync)
-            const cudaError_t q = cudaEventQuery(wk.tune_ev[2 * WorkerDev::kTuneReps - 1][1]);
+            const cudaError_t q = cudaEventQuery(wk.tune_ev[nlaunch - 1][1]);
             if (q == cudaSuccess) {
-                float t[2] = {3.4e38f, 3.4e38f};
-                for (int k = 0; k < 2 * WorkerDev::kTuneReps; ++k) {
+                float t[WorkerDev::kCand] = {3.4e38f, 3.4e38f, 3.4e38f};
+                for (int k = 0; k < nlaunch; ++k) {
                     float ms = 0.f;
                     CK(cudaEventElapsedTime(&ms, wk.tune_ev[k][0], wk.tune_ev[k][1]));
-                    t[k & 1] = std::min(t[k & 1], ms);
+                    t[k % nc] = std::min(t[k % nc], ms);
                 }
-                wk.mid_pick = t[1] < t[0] ? 1 : 0;
+                int best = 0;
+                for (int c = 1; c < nc; ++c)
+                    if (t[c] < t[best]) best = c;
+                wk.mid_pick = best;
                 wk.tune_pending = false;
             } else if (q != cudaErrorNotReady) {
                 CK(q);
@@ -1435,12 +1444,12 @@ class Engine {
             for (auto& ev : wk.tune_ev[k])
                 if (!ev) CK(cudaEventCreate(&ev));
             const int keep = wk.mid_pick;
-            wk.mid_pick = k & 1;
+            wk.mid_pick = k % nc;
             CK(cudaEventRecord(wk.tune_ev[k][0], s));
             launch_bulk(wk, s, b, e, ia);
             CK(cudaEventRecord(wk.tune_ev[k][1], s));
             wk.mid_pick = keep;
-            if (++wk.tune_phase > 2 * WorkerDev::kTuneReps) {
+            if (++wk.tune_phase > nlaunch) {
                 wk.tune_phase = 0;
                 wk.tune_pending = true;
             }
@@ -1473,6 +1482,7 @@ class Engine {
 #endif
         if (plain_variant == 24) return launch_tma<256, 2, 2, false, 2>(wk, s, b, e);
         if (plain_variant == 71 && mid && wk.rtab_ok) return launch_run<256, 2, 2>(wk, s, b, e);
+        if (mid && wk.rtab_ok && plain_variant == 0 && wk.mid_pick == 2) return launch_run<256, 2, 2>(wk, s, b, e);
         if (mid && wk.ctab_ok) {
             const bool pf = plain_variant == 59 || (plain_variant == 0 && wk.mid_pick == 1);
             if (pf) launch_tmc<256, 2, 2, 4102>(wk, s, b, e);
