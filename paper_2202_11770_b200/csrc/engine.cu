@@ -719,7 +719,7 @@ class Engine {
         DevMem dsend, drecv;
         char* ds = dsend.alloc<char>(3 * H);
         char* dr = drecv.alloc<char>(3 * H * size_t(nranks));
-        CK(cudaMemcpy(ds, mine.data(), 3 * H, cudaMemcpyHostToDevice));
+        CK(cudaMemcpyAsync(ds, mine.data(), 3 * H, cudaMemcpyHostToDevice, wk.sE));  // ordered before the all-gather
         NK(nccl().AllGather(ds, dr, 3 * H, ncclChar, comm, wk.sE));
         std::vector<cudaIpcMemHandle_t> all(3 * size_t(nranks));
         CK(cudaMemcpyAsync(all.data(), dr, 3 * H * size_t(nranks), cudaMemcpyDeviceToHost, wk.sE));
@@ -2541,7 +2541,9 @@ class Engine {
             }
             DevMem tmp;
             double* d = tmp.alloc<double>(h.size());
-            CK(cudaMemcpy(d, h.data(), h.size() * 8, cudaMemcpyHostToDevice));
+            // stream-ordered: a legacy cudaMemcpy from pageable memory may
+            // return before its DMA lands, and wk.sM does not wait for it
+            CK(cudaMemcpyAsync(d, h.data(), h.size() * 8, cudaMemcpyHostToDevice, wk.sM));
             if (wk.n)
                 lbm_aa_import<<<blocks_for(wk.n), 256, 0, wk.sM>>>(wk.f_old(), wk.tab.get<uint32_t>(), wk.P, wk.n,
                                                                    int(steps_run & 1), d);
@@ -2556,7 +2558,8 @@ class Engine {
         }
         for (uint32_t k = 0; k < wk.shared; ++k) h[uint64_t(kQ) * wk.P + k] = host[uint64_t(kQ) * wk.n + k];
         double* dst = which == 0 ? wk.f_old() : wk.f_new();
-        CK(cudaMemcpy(dst, h.data(), h.size() * 8, cudaMemcpyHostToDevice));
+        CK(cudaMemcpyAsync(dst, h.data(), h.size() * 8, cudaMemcpyHostToDevice, wk.sM));
+        CK(cudaStreamSynchronize(wk.sM));  // the steps' streams are non-blocking: land the data first
     }
 
     // StreamingMap in the reference encoding (layout.hpp:181-286) from the

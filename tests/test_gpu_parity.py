@@ -288,6 +288,34 @@ def test_store_roundtrip_layouts(product):
             assert np.array_equal(st.f_old(), x)
 
 
+@pytest.mark.parametrize("storage", [0, 1])
+def test_store_set_then_step_large(product, storage):
+    """set_f of large stores is ordered before the next kernels (a legacy
+    pageable cudaMemcpy can return before its DMA lands, and the engine's
+    streams do not wait for it): 3 workers, 2.3e5 sites, a perturbed store
+    written and read back, then stepped — equal to one worker, every time."""
+    d = product.build_channel(48, 40, 120)
+    bcs = product.BCSet([product.BCEntry(product.PRESSURE, product.TimeTable.constant(cases.CS2 * 1.001)),
+                         product.BCEntry(product.PRESSURE, product.TimeTable.constant(cases.CS2 * 0.999))])
+    noise = cases.noise_for(d.n_sites(), 20240808, 0.01)
+    ref = product.Simulation(d, bcs, product.EngineParams(tau=0.8))
+    cases.apply_noise(product, ref, noise)
+    ref.run(1)
+    want = ref.snapshot_fields()
+    for rep in range(3):
+        s = product.Simulation(d, bcs, product.EngineParams(tau=0.8, workers=3, storage=storage))
+        cases.apply_noise(product, s, noise)
+        pa = s.assignment()
+        fr = ref.store(0)
+        for w in range(3):
+            got = s.store(w).f_old()
+            n = len(pa.parts[w].sites)
+            assert np.all(got[:19 * n].reshape(n, 19) >= 0.0)
+        s.run(1)
+        assert np.array_equal(s.snapshot_fields(), want), (storage, rep)
+        s.close()
+
+
 def test_multi_device_placement_single_gpu(product):
     """Workers placed round-robin on the device list; with one device all
     share it and exchange by device-to-device copies."""
