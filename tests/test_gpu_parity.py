@@ -306,7 +306,6 @@ def test_store_set_then_step_large(product, storage):
         s = product.Simulation(d, bcs, product.EngineParams(tau=0.8, workers=3, storage=storage))
         cases.apply_noise(product, s, noise)
         pa = s.assignment()
-        fr = ref.store(0)
         for w in range(3):
             got = s.store(w).f_old()
             n = len(pa.parts[w].sites)
