@@ -134,6 +134,12 @@ static void encode_planes(CUtensorMap* m, void* base, bool f64, int planes, uint
 
 namespace {
 
+// Set once an exchange failure has left streams blocked on a dead
+// neighbour's flags: freeing device or pinned memory would then wait on those
+// streams forever (cudaFree synchronises the device), so the buffers of the
+// failed engine are leaked instead and the caller can report and exit.
+static std::atomic<bool> g_leak_on_free{false};
+
 struct DevMem {
     void* p = nullptr;
     size_t bytes = 0;
@@ -142,7 +148,7 @@ struct DevMem {
     DevMem& operator=(const DevMem&) = delete;
     ~DevMem() { release(); }
     void release() {
-        if (p) cudaFree(p);
+        if (p && !g_leak_on_free.load()) cudaFree(p);
         p = nullptr;
         bytes = 0;
     }
@@ -173,7 +179,7 @@ struct PinnedMem {
     PinnedMem(const PinnedMem&) = delete;
     PinnedMem& operator=(const PinnedMem&) = delete;
     ~PinnedMem() {
-        if (p) cudaFreeHost(p);
+        if (p && !g_leak_on_free.load()) cudaFreeHost(p);
     }
     template <class T>
     T* reserve(size_t n) {
@@ -774,9 +780,10 @@ class Engine {
             } catch (...) {
             }
         }
-        for (auto& wp : W)
-            if (wp)
-                for (void* p : wp->ipc_opened) cudaIpcCloseMemHandle(p);
+        if (!failed)
+            for (auto& wp : W)
+                if (wp)
+                    for (void* p : wp->ipc_opened) cudaIpcCloseMemHandle(p);
         if (comm) nccl().CommDestroy(comm);
         for (auto& wp : W) {
             if (!wp) continue;
@@ -2070,31 +2077,17 @@ class Engine {
         }
     }
 
-    // No progress for exchange_timeout_s: abort the communicator, release the
-    // streams blocked on flag words (so teardown does not wait on them), and
-    // report the neighbour whose halo is missing (the lowest halo_in flag).
+    // No progress for exchange_timeout_s: abort the communicator and fail.  No
+    // CUDA call follows: a stream operation queued now could sit behind the
+    // streams blocked on the dead neighbour's flags (they share hardware
+    // queues), so the failed engine's memory is leaked at teardown instead.
     [[noreturn]] void exchange_timeout(int w) {
         failed = true;
-        WorkerDev& wk = *W[size_t(w)];
-        int nb = wk.segs.empty() ? -1 : wk.segs.front().nb;
+        g_leak_on_free.store(true);
+        const WorkerDev& wk = *W[size_t(w)];
+        const int nb = wk.segs.empty() ? -1 : wk.segs.front().nb;
         if (comm) nccl().CommAbort(comm);
         comm = nullptr;
-        if (wk.flags.p) {
-            cudaStream_t t = nullptr;
-            if (cudaStreamCreateWithFlags(&t, cudaStreamNonBlocking) == cudaSuccess) {
-                const size_t nf = 2 * size_t(prm.workers);
-                std::vector<uint32_t> h(nf, 0);
-                if (cudaMemcpyAsync(h.data(), wk.flags.p, nf * 4, cudaMemcpyDeviceToHost, t) == cudaSuccess &&
-                    cudaStreamSynchronize(t) == cudaSuccess) {
-                    uint32_t lo = UINT32_MAX;
-                    for (const Seg& sg : wk.segs)
-                        if (h[size_t(sg.nb)] < lo) lo = h[size_t(sg.nb)], nb = sg.nb;
-                }
-                cudaMemsetAsync(wk.flags.p, 0xFF, nf * 4, t);
-                cudaStreamSynchronize(t);
-                cudaStreamDestroy(t);
-            }
-        }
         fail(ErrKind::Comm, "exchange failure: worker " + std::to_string(w) + " timed out waiting for neighbor " +
                                 std::to_string(nb));
     }
