@@ -1480,7 +1480,7 @@ class Engine {
         (void)v;
         return true;
 #else
-        return v == 0 || v == 24 || v == 43 || v == 59 || v == 60 || v == 71;
+        return v == 0 || v == 24 || v == 43 || v == 59 || v == 60 || v == 71 || v == 72 || v == 73;
 #endif
     }
     void launch_plain(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia, bool mid) {
@@ -1504,7 +1504,7 @@ class Engine {
     // defaults, profiles/r01_sweep_*.log).  Returns false for the built-in ones.
     bool launch_tuning_variant(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia, bool mid) {
         if (plain_variant == 0 || plain_variant == 24 || plain_variant == 43 || plain_variant == 59 ||
-            plain_variant == 60 || plain_variant == 71)
+            plain_variant == 60 || plain_variant == 71 || plain_variant == 72 || plain_variant == 73)
             return false;
         if (plain_variant == 69 || plain_variant == 70) {  // tile-major table, one bulk copy per tile
             if (!(mid && wk.ctab_ok)) launch_tma<256, 2, 2, false, 6>(wk, s, b, e);
@@ -2141,6 +2141,19 @@ class Engine {
     }
 #endif
 
+    // Warp-autonomous AA odd kernel (persistent; cp.async gathers one tile ahead).
+    template <int NW, int B>
+    void launch_aa_odd_w(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e) {
+        using Lm = AaOddW<NW, B>;
+        const int resident = resident_ctas(lbm_aa_odd_w<NW, B>, wk.dev, NW * 32, Lm::kBytes);
+        const uint32_t ntiles = (e - (b & ~31u) + 31) / 32;
+        const unsigned grid = unsigned(std::min<uint32_t>((ntiles + NW - 1) / NW, uint32_t(resident)));
+        Planes19 pl;
+        for (int i = 0; i < kQ; ++i) pl.p[i] = wk.f_old() + uint64_t(i) * wk.P;
+        lbm_aa_odd_w<NW, B><<<grid, NW * 32, Lm::kBytes, s>>>(wk.f_old(), wk.dtab.get<int16_t>(), wk.gbase.get<uint32_t>(),
+                                                           wk.tab.get<uint32_t>(), wk.P, wk.PG, b, e, omega, pl);
+    }
+
     void launch_aa_range(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, bool iolet, const double* staged,
                          const int32_t* coords, bool timed, bool edge, bool odd) {
         if (e <= b) return;
@@ -2173,7 +2186,11 @@ class Engine {
                         F, wk.dtab.get<int16_t>(), wk.gbase.get<uint32_t>(), tab, wk.P, wk.PG, b, e, omega);
             }
 #endif
-            else if (timed && wk.ctab_ok && v != 60) {
+            else if (timed && wk.ctab_ok && v == 72) {
+                launch_aa_odd_w<4, 4>(wk, s, b, e);
+            } else if (timed && wk.ctab_ok && v == 73) {
+                launch_aa_odd_w<4, 3>(wk, s, b, e);
+            } else if (timed && wk.ctab_ok && v != 60) {
                 // default: compressed table, one thread per site, branch-free
                 // address selects, register gather (C3 developed: 13.6k MSUPS;
                 // the software-pipelined cp.async variant 66 measured 13.1k)

@@ -1336,6 +1336,118 @@ lbm_aa_odd_async(double* __restrict__ F, const int16_t* __restrict__ dtab, const
     cp_async_wait<0>();
 }
 
+// Odd step, mid-group plain range: warp-autonomous software pipeline.  Each
+// warp walks its own 32-site tiles (persistent, no CTA barrier): the
+// compressed table of tile k+2 is loaded into registers, the 19 gathers of
+// tile k+1 are issued as cp.async straight into the warp's shared-memory
+// stage (in flight without holding registers), and tile k collides from its
+// stage and scatters to the 19 locations computed one iteration earlier
+// (kept as signed offsets from each direction's plane).  Every location is
+// owned by one (site, direction): the in-place update needs no ordering.
+template <int kWarps, int kMinBlocks>
+struct AaOddW {
+    static constexpr uint32_t kStage = uint32_t(kQ) * 32 * 8;  // one warp's gathered f
+    static constexpr uint32_t kBytes = 2 * kWarps * kStage;
+};
+
+template <int kWarps, int kMinBlocks>
+__global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
+lbm_aa_odd_w(double* __restrict__ F, const int16_t* __restrict__ dtab, const uint32_t* __restrict__ gbase,
+             const uint32_t* __restrict__ tab, uint64_t P, uint64_t PG, uint32_t begin, uint32_t end, double omega,
+             const __grid_constant__ Planes19 planes) {
+    using L = AaOddW<kWarps, kMinBlocks>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    double* stage[2] = {reinterpret_cast<double*>(smem + (2 * wib) * L::kStage),
+                        reinterpret_cast<double*>(smem + (2 * wib + 1) * L::kStage)};
+    const uint32_t base = begin & ~31u;
+    const uint32_t ntiles = (end - base + 31) / 32;
+    const uint32_t nw = gridDim.x * kWarps;
+    const uint32_t w0 = blockIdx.x * kWarps + wib;
+    // compressed table of warp-tile k into registers: the 18 int16 deltas
+    // packed two per register, and this lane's group base
+    constexpr int kD2 = (kQ - 1) / 2;
+    uint32_t dA[kD2], dB[kD2];
+    uint32_t bA = 0, bB = 0;
+    auto load_table = [&](uint32_t k, uint32_t* d, uint32_t& b) {
+        const uint32_t tile = w0 + k * nw;
+        const uint32_t s = base + tile * 32 + lane;
+        const bool live = tile < ntiles && s >= begin && s < end;
+#pragma unroll
+        for (int i = 0; i < kD2; ++i) {
+            const uint32_t lo = live ? uint16_t(__ldg(dtab + uint64_t(2 * i) * P + s)) : uint16_t(kDeltaBounce);
+            const uint32_t hi = live ? uint16_t(__ldg(dtab + uint64_t(2 * i + 1) * P + s)) : uint16_t(kDeltaBounce);
+            d[i] = lo | (hi << 16);
+        }
+        b = (lane < kQ - 1 && tile < ntiles) ? __ldg(gbase + uint64_t(lane) * PG + (s >> 5)) : 0u;
+    };
+    // location of direction j of site s: signed offset from plane j's base
+    // (a bounce-back lives in the inverse plane at s: s +- P)
+    auto loc = [&](const uint32_t* d, uint32_t b, int j, uint32_t s, bool live) -> int32_t {
+        const uint32_t bj = __shfl_sync(0xffffffffu, b, j - 1);
+        const int dj = (j & 1) ? int(int16_t(d[(j - 1) / 2] & 0xffffu)) : int(int16_t(d[(j - 1) / 2] >> 16));
+        uint32_t t = bj + lane + uint32_t(dj);
+        const uint32_t esc = (dj == kDeltaEscape) && live;
+        asm("{\n .reg .pred p;\n setp.ne.u32 p, %1, 0;\n @p ld.global.nc.u32 %0, [%2];\n}"
+            : "+r"(t)
+            : "r"(esc), "l"(tab + uint64_t(j - 1) * P + s));
+        const int32_t off = (j & 1) ? int32_t(P) : -int32_t(P);
+        return dj == kDeltaBounce ? int32_t(s) + off : int32_t(t);
+    };
+    int32_t oA[kQ - 1], oB[kQ - 1];  // locations of the tile being stored / being gathered
+    // issue the gathers of tile k (table d, b) into stage k & 1; offsets into o
+    auto issue = [&](uint32_t k, const uint32_t* d, uint32_t b, int32_t* o) {
+        const uint32_t tile = w0 + k * nw;
+        const uint32_t s = base + tile * 32 + lane;
+        const bool live = tile < ntiles && s >= begin && s < end;
+        double* st = stage[k & 1];
+#pragma unroll
+        for (int i = 1; i < kQ; ++i) o[i - 1] = loc(d, b, i, s, live);
+        if (live) {
+            cp_async8(st + lane, F + s);
+#pragma unroll
+            for (int i = 1; i < kQ; ++i) cp_async8(st + inv(i) * 32 + lane, planes.p[i] + o[i - 1]);  // f_inv(i)(s)
+        }
+    };
+    // iteration k: gathers of tile k+1 (its table in dN), table of tile k+2
+    // into dNN, then tile k collides from its stage and stores through oK;
+    // two iterations per loop trip swap the register sets without moves
+    auto step = [&](uint32_t k, const uint32_t* dN, uint32_t bN, int32_t* oN, uint32_t* dNN, uint32_t& bNN,
+                    const int32_t* oK) -> bool {
+        const uint32_t tile = w0 + k * nw;
+        if (tile >= ntiles) return false;
+        issue(k + 1, dN, bN, oN);
+        cp_async_commit();
+        load_table(k + 2, dNN, bNN);
+        cp_async_wait<1>();  // this lane's gathers of tile k have landed
+        const uint32_t s = base + tile * 32 + lane;
+        const double* st = stage[k & 1];
+        double f[kQ];
+#pragma unroll
+        for (int i = 0; i < kQ; ++i) f[i] = st[i * 32 + lane];
+        const Macro m = macro_of(f);
+        double feq[kQ];
+        feq_all(m.rho, m.ux, m.uy, m.uz, feq);
+        if (s >= begin && s < end) {
+            F[s] = relax(f[0], feq[0], omega);
+#pragma unroll
+            for (int i = 1; i < kQ; ++i) planes.p[i][oK[i - 1]] = relax(f[i], feq[i], omega);
+        }
+        __syncwarp();  // the stage of tile k is refilled by tile k+2's gathers
+        return true;
+    };
+    load_table(0, dA, bA);
+    if (w0 >= ntiles) return;  // whole warp
+    issue(0, dA, bA, oA);
+    cp_async_commit();
+    load_table(1, dB, bB);
+    for (uint32_t k = 0;; k += 2) {
+        if (!step(k, dB, bB, oB, dA, bA, oA)) break;
+        if (!step(k + 1, dA, bA, oA, dB, bB, oB)) break;
+    }
+    cp_async_wait<0>();
+}
+
 // Gather the 19 populations of site s in the current AA state (state N:
 // plain reads; state S: the rule above).
 template <bool kP2P>

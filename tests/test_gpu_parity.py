@@ -129,7 +129,7 @@ def test_aa_single_buffer_bit_exact(product, golden, key):
     assert cases.run_digest(res) == golden["runs"][key]
 
 
-@pytest.mark.parametrize("variant", ["0", "60", "61", "62", "63", "65", "66"])
+@pytest.mark.parametrize("variant", ["0", "60", "61", "62", "63", "65", "66", "72", "73"])
 def test_aa_odd_kernel_variants(product, golden, variant, monkeypatch):
     """Odd-step kernels: the default register gather over the compressed
     table, the u32-table gather (60), and the tuning shapes (61-63, 65, and
