@@ -1480,7 +1480,7 @@ class Engine {
         (void)v;
         return true;
 #else
-        return v == 0 || v == 24 || v == 43 || v == 59 || v == 60 || v == 71 || v == 72 || v == 73;
+        return v == 0 || v == 24 || v == 43 || v == 59 || v == 60 || v == 64 || v == 71 || v == 72;
 #endif
     }
     void launch_plain(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia, bool mid) {
@@ -1504,7 +1504,7 @@ class Engine {
     // defaults, profiles/r01_sweep_*.log).  Returns false for the built-in ones.
     bool launch_tuning_variant(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia, bool mid) {
         if (plain_variant == 0 || plain_variant == 24 || plain_variant == 43 || plain_variant == 59 ||
-            plain_variant == 60 || plain_variant == 71 || plain_variant == 72 || plain_variant == 73)
+            plain_variant == 60 || plain_variant == 64 || plain_variant == 71 || plain_variant == 72)
             return false;
         if (plain_variant == 69 || plain_variant == 70) {  // tile-major table, one bulk copy per tile
             if (!(mid && wk.ctab_ok)) launch_tma<256, 2, 2, false, 6>(wk, s, b, e);
@@ -2175,7 +2175,7 @@ class Engine {
             const int v = plain_variant;
             if (iolet) lbm_aa_odd<true, false, 128, 4><<<nb, 128, 0, s>>>(F, tab, wk.P, b, e, omega, ia, h);
 #ifdef SPLBCU_TUNING
-            else if (timed && wk.ctab_ok && v >= 61 && v <= 66) {
+            else if (timed && wk.ctab_ok && v >= 61 && v <= 66 && v != 64) {
                 if (v == 61) launch_aa_odd_tmc<128, 2, 4>(wk, s, b, e);
                 else if (v == 62) launch_aa_odd_tmc<256, 3, 2>(wk, s, b, e);
                 else if (v == 63) launch_aa_odd_tmc<256, 2, 2>(wk, s, b, e);
@@ -2187,16 +2187,17 @@ class Engine {
             }
 #endif
             else if (timed && wk.ctab_ok && v == 72) {
-                launch_aa_odd_w<4, 4>(wk, s, b, e);
-            } else if (timed && wk.ctab_ok && v == 73) {
-                launch_aa_odd_w<4, 3>(wk, s, b, e);
-            } else if (timed && wk.ctab_ok && v != 60) {
-                // default: compressed table, one thread per site, branch-free
-                // address selects, register gather (C3 developed: 13.6k MSUPS;
-                // the software-pipelined cp.async variant 66 measured 13.1k)
+                launch_aa_odd_w<4, 4>(wk, s, b, e);  // 128 registers: spills (C3 odd 9.6k)
+            } else if (timed && wk.ctab_ok && v == 64) {
+                // round-1 default: one thread per site, register gather over the
+                // compressed table (C3 developed, odd step: 13.7k MSUPS)
                 const uint32_t b0 = b & ~31u;
                 lbm_aa_odd_c<128, 4><<<unsigned((e - b0 + 127) / 128), 128, 0, s>>>(
                     F, wk.dtab.get<int16_t>(), wk.gbase.get<uint32_t>(), tab, wk.P, wk.PG, b, e, omega);
+            } else if (timed && wk.ctab_ok && v != 60) {
+                // default: warp-autonomous pipeline, cp.async gathers one tile
+                // ahead (C3 developed, odd step: 14.2k MSUPS; C2 14.9k vs 13.6k)
+                launch_aa_odd_w<4, 3>(wk, s, b, e);
             } else lbm_aa_odd<false, false, 128, 4><<<nb, 128, 0, s>>>(F, tab, wk.P, b, e, omega, ia, h);
         }
         if (timed) {

@@ -129,12 +129,13 @@ def test_aa_single_buffer_bit_exact(product, golden, key):
     assert cases.run_digest(res) == golden["runs"][key]
 
 
-@pytest.mark.parametrize("variant", ["0", "60", "61", "62", "63", "65", "66", "72", "73"])
+@pytest.mark.parametrize("variant", ["0", "60", "61", "62", "63", "64", "65", "66", "72"])
 def test_aa_odd_kernel_variants(product, golden, variant, monkeypatch):
-    """Odd-step kernels: the default register gather over the compressed
-    table, the u32-table gather (60), and the tuning shapes (61-63, 65, and
-    66 = cp.async gathers into shared memory; built with TUNING=1) give the
-    reference's bits."""
+    """Odd-step kernels: the default warp-autonomous cp.async pipeline, its
+    128-register shape (72), the round-1 register gather over the compressed
+    table (64) and over the u32 table (60), and the tuning shapes (61-63, 65,
+    66 = CTA-wide cp.async pipeline; built with TUNING=1) give the reference's
+    bits."""
     monkeypatch.setenv("SPLBCU_PLAIN_VARIANT", variant)
     _skip_unbuilt(product)
     for key in ("bif_W3_soa_reordered", "pipe_beat_6_30", "C1_pipe_16_128"):
