@@ -1853,6 +1853,7 @@ class Engine {
         std::chrono::steady_clock::time_point h0;
     };
     PendingRun pend;
+    uint64_t max_run_n = 0;  // the longest run so far (buffer sizes follow it)
     const bool sync_runs = std::getenv("SPLBCU_SYNC_RUN") != nullptr;  // A/B knob: every run completes before returning
     int run_par = 0;                                     // event / staging set of the run being enqueued
     PinnedMem h_staged2[2];                              // per-run iolet values, one per run in flight
@@ -1866,7 +1867,13 @@ class Engine {
             for (uint64_t st = steps_run == 0 ? 0 : steps_run + 1; st <= steps_run + n && !has_caps; ++st)
                 has_caps = st % prm.capture_period == 0;
         const bool sync_run = has_caps || (prm.observe_iolets && !dev_series) || sync_runs;
-        if (sync_run) complete();
+        // A longer run than any before may grow the staging / observation
+        // buffers, and cudaFree waits for every stream: complete the run in
+        // flight first, under the watchdog (a dead neighbour must surface as an
+        // exchange failure, not as a hang inside cudaFree).
+        const bool grows = n > max_run_n;
+        max_run_n = std::max(max_run_n, n);
+        if (sync_run || grows) complete();
         const int par = run_par;
         const size_t caps_before = caps.size();
         const bool first_run = steps_run == 0;
@@ -1975,6 +1982,7 @@ class Engine {
     void complete() {
         if (!pend.active) return;
         pend.active = false;
+        last_progress = std::chrono::steady_clock::now();
         const int par = pend.par;
         std::vector<cudaEvent_t> done(W.size(), nullptr);
         for (size_t w = 0; w < W.size(); ++w)

@@ -186,6 +186,7 @@ DEAD_RANK_SCRIPT = textwrap.dedent("""
     if rank == world - 1:
         os._exit(0)  # this worker dies between steps
     t0 = time.time()
+    print("running", flush=True)
     try:
         sim.run(500)
         print("NO ERROR")
