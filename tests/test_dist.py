@@ -184,7 +184,13 @@ DEAD_RANK_SCRIPT = textwrap.dedent("""
     sim.run(3)
     td.barrier()
     if rank == world - 1:
-        os._exit(0)  # this worker dies between steps
+        # this worker stops stepping: over NCCL it dies; over the fused P2P
+        # halo it stays alive but stuck (a dead exporter's IPC memory must not
+        # be written by the survivor's already-queued step), then exits
+        if os.environ["HALO"] == "0":
+            os._exit(0)
+        time.sleep(40)
+        os._exit(0)
     t0 = time.time()
     print("running", flush=True)
     try:
@@ -201,10 +207,10 @@ DEAD_RANK_SCRIPT = textwrap.dedent("""
 @pytest.mark.gpu
 @pytest.mark.parametrize("halo", ["0", "1"])
 def test_dead_rank_fails_within_timeout(halo):
-    """A worker that dies is reported by its neighbour within
-    exchange_timeout_s of the last completed step, with the reference's
-    message (Mailbox::take, engine.hpp:92-101), and the survivor's teardown
-    completes."""
+    """A worker that dies (NCCL) or stops stepping (fused P2P) is reported by
+    its neighbour within exchange_timeout_s of the last completed step, with
+    the reference's message (Mailbox::take, engine.hpp:92-101), and the
+    survivor's teardown completes."""
     import re
     import torch
     if torch.cuda.device_count() < 2:
