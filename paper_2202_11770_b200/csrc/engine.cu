@@ -134,6 +134,16 @@ static void encode_planes(CUtensorMap* m, void* base, bool f64, int planes, uint
 
 namespace {
 
+// SPLBCU_TRACE: host-side progress lines on stderr (run enqueue, watchdog).
+static const bool g_trace = std::getenv("SPLBCU_TRACE") != nullptr;
+#define TRACE(...)                                        \
+    do {                                                  \
+        if (g_trace) {                                    \
+            std::fprintf(stderr, "[splbcu] " __VA_ARGS__); \
+            std::fflush(stderr);                          \
+        }                                                 \
+    } while (0)
+
 // Set once an exchange failure has left streams blocked on a dead
 // neighbour's flags: freeing device or pinned memory would then wait on those
 // streams forever (cudaFree synchronises the device), so the buffers of the
@@ -1873,6 +1883,8 @@ class Engine {
         // exchange failure, not as a hang inside cudaFree).
         const bool grows = n > max_run_n;
         max_run_n = std::max(max_run_n, n);
+        TRACE("run(%llu): rank %d, completing the run in flight: %d\n", (unsigned long long)n, rank,
+              int(sync_run || grows));
         if (sync_run || grows) complete();
         const int par = run_par;
         const size_t caps_before = caps.size();
@@ -1918,6 +1930,7 @@ class Engine {
                 // at most kDepth steps in flight: the host waits for step
                 // k - kDepth first, under the exchange watchdog
                 if (k >= kDepth) wait_step(k - kDepth);
+                if (k < 2 || k == kDepth) TRACE("run: enqueue step %llu\n", (unsigned long long)k);
                 step_once(k, k * n_io);
                 mark_step(k);
             }
@@ -2079,6 +2092,7 @@ class Engine {
                 fail(ErrKind::Comm, std::string("exchange failure: NCCL async error: ") + nccl().GetErrorString(ar));
             const double el =
                 std::chrono::duration<double>(std::chrono::steady_clock::now() - last_progress).count();
+            if (spins % 20000 == 0) TRACE("watchdog: worker %d waiting %.1f s\n", w, el);
             if (el > prm.exchange_timeout_s) exchange_timeout(w);
             if (spins < 2000) std::this_thread::yield();
             else std::this_thread::sleep_for(std::chrono::microseconds(50));
@@ -2094,8 +2108,10 @@ class Engine {
         g_leak_on_free.store(true);
         const WorkerDev& wk = *W[size_t(w)];
         const int nb = wk.segs.empty() ? -1 : wk.segs.front().nb;
+        TRACE("watchdog: worker %d timed out; aborting the communicator\n", w);
         if (comm) nccl().CommAbort(comm);
         comm = nullptr;
+        TRACE("watchdog: communicator aborted\n");
         fail(ErrKind::Comm, "exchange failure: worker " + std::to_string(w) + " timed out waiting for neighbor " +
                                 std::to_string(nb));
     }
