@@ -2099,19 +2099,22 @@ class Engine {
         }
     }
 
-    // No progress for exchange_timeout_s: abort the communicator and fail.  No
-    // CUDA call follows: a stream operation queued now could sit behind the
-    // streams blocked on the dead neighbour's flags (they share hardware
-    // queues), so the failed engine's memory is leaked at teardown instead.
+    // No progress for exchange_timeout_s: fail.  No CUDA call follows: a stream
+    // operation queued now could sit behind the streams blocked on the dead
+    // neighbour's flags (they share hardware queues), so the failed engine's
+    // memory is leaked at teardown instead.
     [[noreturn]] void exchange_timeout(int w) {
         failed = true;
         g_leak_on_free.store(true);
         const WorkerDev& wk = *W[size_t(w)];
         const int nb = wk.segs.empty() ? -1 : wk.segs.front().nb;
-        TRACE("watchdog: worker %d timed out; aborting the communicator\n", w);
-        if (comm) nccl().CommAbort(comm);
+        // NCCL halo: abort the communicator (its kernels wait for the dead
+        // peer).  Fused P2P halo: the communicator is idle, and aborting it
+        // frees device memory — cudaFree waits for every stream, including the
+        // ones blocked on the peer's flags — so it is left to process exit.
+        TRACE("watchdog: worker %d timed out; %s the communicator\n", w, p2p_mode ? "leaving" : "aborting");
+        if (comm && !p2p_mode) nccl().CommAbort(comm);
         comm = nullptr;
-        TRACE("watchdog: communicator aborted\n");
         fail(ErrKind::Comm, "exchange failure: worker " + std::to_string(w) + " timed out waiting for neighbor " +
                                 std::to_string(nb));
     }
