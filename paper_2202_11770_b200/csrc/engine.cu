@@ -1362,6 +1362,21 @@ class Engine {
                                                               wk.PG, b, e, omega, pl);
     }
 
+    // Warp-autonomous push kernel over the delta table (mid-group range only).
+    template <int NW, int B>
+    void launch_push_w(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e) {
+        using Lm = PushW<NW, B>;
+        const int resident = resident_ctas(lbm_push_w<NW, B>, wk.dev, NW * 32, Lm::kBytes);
+        const uint32_t ntiles = (e - (b & ~31u) + 31) / 32;
+        const unsigned grid = unsigned(std::min<uint32_t>((ntiles + NW - 1) / NW, uint32_t(resident)));
+        check_tiles(wk, b & ~31u, ntiles, 32);
+        Planes19 pl;
+        for (int i = 0; i < kQ; ++i) pl.p[i] = wk.f_new() + uint64_t(i) * wk.P;
+        lbm_push_w<NW, B><<<grid, NW * 32, Lm::kBytes, s>>>(wk.f_old(), wk.f_new(), wk.dtab.get<int16_t>(),
+                                                         wk.gbase.get<uint32_t>(), wk.tab.get<uint32_t>(), wk.P, wk.PG, b,
+                                                         e, omega, pl);
+    }
+
     // Persistent TMA kernel over the run-length table (mid-group range only).
     template <int T, int S, int B>
     void launch_run(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e) {
@@ -1490,7 +1505,7 @@ class Engine {
         (void)v;
         return true;
 #else
-        return v == 0 || v == 24 || v == 43 || v == 59 || v == 60 || v == 64 || v == 71 || v == 72;
+        return v == 0 || v == 24 || v == 43 || v == 59 || v == 60 || v == 64 || v == 71 || v == 72 || v == 74 || v == 75;
 #endif
     }
     void launch_plain(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia, bool mid) {
@@ -1499,6 +1514,10 @@ class Engine {
 #endif
         if (plain_variant == 24) return launch_tma<256, 2, 2, false, 2>(wk, s, b, e);
         if (plain_variant == 71 && mid && wk.rtab_ok) return launch_run<256, 2, 2>(wk, s, b, e);
+        if ((plain_variant == 74 || plain_variant == 75) && mid && wk.ctab_ok) {
+            if (plain_variant == 74) return launch_push_w<4, 4>(wk, s, b, e);
+            return launch_push_w<4, 3>(wk, s, b, e);
+        }
         if (mid && wk.rtab_ok && plain_variant == 0 && wk.mid_pick == 2) return launch_run<256, 2, 2>(wk, s, b, e);
         if (mid && wk.ctab_ok) {
             const bool pf = plain_variant == 59 || (plain_variant == 0 && wk.mid_pick == 1);
@@ -1514,7 +1533,8 @@ class Engine {
     // defaults, profiles/r01_sweep_*.log).  Returns false for the built-in ones.
     bool launch_tuning_variant(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia, bool mid) {
         if (plain_variant == 0 || plain_variant == 24 || plain_variant == 43 || plain_variant == 59 ||
-            plain_variant == 60 || plain_variant == 64 || plain_variant == 71 || plain_variant == 72)
+            plain_variant == 60 || plain_variant == 64 || plain_variant == 71 || plain_variant == 72 ||
+            plain_variant == 74 || plain_variant == 75)
             return false;
         if (plain_variant == 69 || plain_variant == 70) {  // tile-major table, one bulk copy per tile
             if (!(mid && wk.ctab_ok)) launch_tma<256, 2, 2, false, 6>(wk, s, b, e);

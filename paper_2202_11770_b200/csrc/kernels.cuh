@@ -261,6 +261,16 @@ __device__ __forceinline__ uint64_t evict_last_policy(float fraction) {
 __device__ __forceinline__ void st_hint(double* p, double v, uint64_t policy) {
     asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(policy) : "memory");
 }
+// Ampere-style asynchronous copies global -> shared (LDGSTS): register-free
+// loads completing per thread on cp.async groups.
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 __device__ __forceinline__ uint64_t evict_normal_policy() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
@@ -785,6 +795,112 @@ lbm_push_run(const double* __restrict__ fo, double* __restrict__ fn, const unsig
     }
 }
 
+// ---- warp-autonomous push kernel (delta table) ------------------------------
+// Each warp walks its own 32-site tiles (persistent, no CTA barrier): the 19
+// f-plane segments of tile k+1 are copied into the warp's shared-memory stage
+// with 16-byte cp.async (register-free, in flight while tile k computes), the
+// compressed table of tile k+1 is loaded into registers one tile ahead (deltas
+// packed two per register), and tile k collides and scatters its 19 results.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
+template <int kWarps, int kMinBlocks>
+struct PushW {
+    static constexpr uint32_t kStage = uint32_t(kQ) * 32 * 8;  // one warp-tile of f
+    static constexpr uint32_t kBytes = 2 * kWarps * kStage;
+};
+
+template <int kWarps, int kMinBlocks>
+__global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
+lbm_push_w(const double* __restrict__ fo, double* __restrict__ fn, const int16_t* __restrict__ dtab,
+           const uint32_t* __restrict__ gbase, const uint32_t* __restrict__ tab, uint64_t P, uint64_t PG,
+           uint32_t begin, uint32_t end, double omega, const __grid_constant__ Planes19 planes) {
+    using L = PushW<kWarps, kMinBlocks>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    double* stage[2] = {reinterpret_cast<double*>(smem + (2 * wib) * L::kStage),
+                        reinterpret_cast<double*>(smem + (2 * wib + 1) * L::kStage)};
+    const uint32_t base = begin & ~31u;
+    const uint32_t ntiles = (end - base + 31) / 32;
+    const uint32_t nw = gridDim.x * kWarps;
+    const uint32_t w0 = blockIdx.x * kWarps + wib;
+    if (w0 >= ntiles) return;  // whole warp
+    constexpr int kD2 = (kQ - 1) / 2;
+    uint32_t dA[kD2], dB[kD2];
+    uint32_t bA = 0, bB = 0;
+    auto load_table = [&](uint32_t k, uint32_t* d, uint32_t& b) {
+        const uint32_t tile = w0 + k * nw;
+        const uint32_t s = base + tile * 32 + lane;
+        const bool live = tile < ntiles && s >= begin && s < end;
+#pragma unroll
+        for (int i = 0; i < kD2; ++i) {
+            const uint32_t lo = live ? uint16_t(__ldg(dtab + uint64_t(2 * i) * P + s)) : 0u;
+            const uint32_t hi = live ? uint16_t(__ldg(dtab + uint64_t(2 * i + 1) * P + s)) : 0u;
+            d[i] = lo | (hi << 16);
+        }
+        b = (lane < kQ - 1 && tile < ntiles) ? __ldg(gbase + uint64_t(lane) * PG + (s >> 5)) : 0u;
+    };
+    // the 19 plane segments of warp-tile k: 304 chunks of 16 B over 32 lanes
+    auto copy_tile = [&](uint32_t k) {
+        const uint32_t tile = w0 + k * nw;
+        if (tile >= ntiles) return;
+        const uint64_t t0 = uint64_t(base) + uint64_t(tile) * 32;
+        double* st = stage[k & 1];
+#pragma unroll
+        for (int r = 0; r < 10; ++r) {
+            const uint32_t c = uint32_t(r) * 32 + lane;
+            if (c < uint32_t(kQ) * 16) {
+                const uint32_t pl = c >> 4, off = (c & 15u) * 2;
+                cp_async16(st + pl * 32 + off, fo + uint64_t(pl) * P + t0 + off);
+            }
+        }
+    };
+    auto step = [&](uint32_t k, const uint32_t* dK, uint32_t bK, uint32_t* dN, uint32_t& bN) -> bool {
+        const uint32_t tile = w0 + k * nw;
+        if (tile >= ntiles) return false;
+        copy_tile(k + 1);
+        cp_async_commit();
+        load_table(k + 1, dN, bN);
+        cp_async_wait<1>();
+        __syncwarp();  // every lane's chunks of tile k are in
+        const uint32_t s = base + tile * 32 + lane;
+        const bool live = s >= begin && s < end;
+        const double* st = stage[k & 1];
+        double f[kQ];
+#pragma unroll
+        for (int i = 0; i < kQ; ++i) f[i] = st[i * 32 + lane];
+        const Macro m = macro_of(f);
+        double feq[kQ];
+        feq_all(m.rho, m.ux, m.uy, m.uz, feq);
+        if (live) fn[s] = relax(f[0], feq[0], omega);
+#pragma unroll
+        for (int i = 1; i < kQ; ++i) {
+            const double fpost = relax(f[i], feq[i], omega);
+            const uint32_t b = __shfl_sync(0xffffffffu, bK, i - 1);
+            const int d = (i & 1) ? int(int16_t(dK[(i - 1) / 2] & 0xffffu)) : int(int16_t(dK[(i - 1) / 2] >> 16));
+            uint32_t t = b + lane + uint32_t(d);
+            const uint32_t esc = (d == kDeltaEscape) && live;
+            asm("{\n .reg .pred p;\n setp.ne.u32 p, %1, 0;\n @p ld.global.nc.u32 %0, [%2];\n}"
+                : "+r"(t)
+                : "r"(esc), "l"(tab + uint64_t(i - 1) * P + s));
+            const int32_t off = (i & 1) ? int32_t(P) : -int32_t(P);
+            double* dst = planes.p[i] + (d == kDeltaBounce ? int32_t(s) + off : int32_t(t));
+            if (live) *dst = fpost;
+        }
+        __syncwarp();  // stage k & 1 is refilled by tile k+2's copies
+        return true;
+    };
+    load_table(0, dA, bA);
+    copy_tile(0);
+    cp_async_commit();
+    for (uint32_t k = 0;; k += 2) {
+        if (!step(k, dA, bA, dB, bB)) break;
+        if (!step(k + 1, dB, bB, dA, bA)) break;
+    }
+    cp_async_wait<0>();
+}
+
 // ---- warp-specialised 2-D TMA variant --------------------------------------
 // One TMA instruction per tile moves the whole [19 planes x T sites] f box
 // (and, optionally, the [18 x T] table box) described by a CUtensorMap over
@@ -1223,14 +1339,6 @@ lbm_aa_odd_c(double* __restrict__ F, const int16_t* __restrict__ dtab, const uin
 //     same locations (addresses recomputed from the staged table).
 // Every location is owned by one (site, direction), so the in-place update
 // needs no ordering between tiles or CTAs; the arithmetic is the push step's.
-__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
 
 template <int T>
 struct AaAsyncSmem {
