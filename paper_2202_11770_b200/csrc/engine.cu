@@ -1362,6 +1362,7 @@ class Engine {
                                                               wk.PG, b, e, omega, pl);
     }
 
+#ifdef SPLBCU_TUNING
     // Warp-autonomous push kernel over the delta table (mid-group range only).
     template <int NW, int B>
     void launch_push_w(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e) {
@@ -1376,6 +1377,7 @@ class Engine {
                                                          wk.gbase.get<uint32_t>(), wk.tab.get<uint32_t>(), wk.P, wk.PG, b,
                                                          e, omega, pl);
     }
+#endif
 
     // Persistent TMA kernel over the run-length table (mid-group range only).
     template <int T, int S, int B>
@@ -1505,7 +1507,7 @@ class Engine {
         (void)v;
         return true;
 #else
-        return v == 0 || v == 24 || v == 43 || v == 59 || v == 60 || v == 64 || v == 71 || v == 72 || v == 74 || v == 75;
+        return v == 0 || v == 24 || v == 43 || v == 59 || v == 60 || v == 64 || v == 71 || v == 72;
 #endif
     }
     void launch_plain(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia, bool mid) {
@@ -1514,10 +1516,14 @@ class Engine {
 #endif
         if (plain_variant == 24) return launch_tma<256, 2, 2, false, 2>(wk, s, b, e);
         if (plain_variant == 71 && mid && wk.rtab_ok) return launch_run<256, 2, 2>(wk, s, b, e);
+#ifdef SPLBCU_TUNING
+        // warp-autonomous push kernel: measured slower (C3 developed 14.8-15.1k
+        // vs 16.6-16.7k for the CTA-wide TMA pipeline, profiles/r02/sweep_dev_pushw.jsonl)
         if ((plain_variant == 74 || plain_variant == 75) && mid && wk.ctab_ok) {
             if (plain_variant == 74) return launch_push_w<4, 4>(wk, s, b, e);
             return launch_push_w<4, 3>(wk, s, b, e);
         }
+#endif
         if (mid && wk.rtab_ok && plain_variant == 0 && wk.mid_pick == 2) return launch_run<256, 2, 2>(wk, s, b, e);
         if (mid && wk.ctab_ok) {
             const bool pf = plain_variant == 59 || (plain_variant == 0 && wk.mid_pick == 1);
@@ -1533,8 +1539,7 @@ class Engine {
     // defaults, profiles/r01_sweep_*.log).  Returns false for the built-in ones.
     bool launch_tuning_variant(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia, bool mid) {
         if (plain_variant == 0 || plain_variant == 24 || plain_variant == 43 || plain_variant == 59 ||
-            plain_variant == 60 || plain_variant == 64 || plain_variant == 71 || plain_variant == 72 ||
-            plain_variant == 74 || plain_variant == 75)
+            plain_variant == 60 || plain_variant == 64 || plain_variant == 71 || plain_variant == 72)
             return false;
         if (plain_variant == 69 || plain_variant == 70) {  // tile-major table, one bulk copy per tile
             if (!(mid && wk.ctab_ok)) launch_tma<256, 2, 2, false, 6>(wk, s, b, e);
