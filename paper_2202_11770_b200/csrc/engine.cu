@@ -1890,6 +1890,7 @@ class Engine {
     PendingRun pend;
     uint64_t max_run_n = 0;  // the longest run so far (buffer sizes follow it)
     const bool sync_runs = std::getenv("SPLBCU_SYNC_RUN") != nullptr;  // A/B knob: every run completes before returning
+    const bool wait_series_off = std::getenv("SPLBCU_NO_SERIES_FIRST") != nullptr;  // A/B knob for the ordering below
     int run_par = 0;                                     // event / staging set of the run being enqueued
     PinnedMem h_staged2[2];                              // per-run iolet values, one per run in flight
     std::chrono::steady_clock::time_point last_done{};  // host clock at the last completion
@@ -1938,6 +1939,12 @@ class Engine {
         for (auto& wp : W) {
             if (!wp) continue;
             CK(cudaSetDevice(wp->dev));
+            // dist mode with observation: the previous run's all-gather and
+            // series kernels (on sE) go first.  Otherwise this run's persistent
+            // bulk kernel can take every SM before the NCCL kernel, which then
+            // lands after it and delays this run's edge kernels behind it.
+            if (pend.active && dist && prm.observe_iolets && !wait_series_off)
+                CK(cudaStreamWaitEvent(wp->sM, wp->evDone[pend.par], 0));
             double* d = wp->staged.reserve<double>(n_staged);
             CK(cudaMemcpyAsync(d, staged, n_staged * sizeof(double), cudaMemcpyHostToDevice, wp->sM));
             wp->tev_used[par] = 0;
