@@ -56,3 +56,21 @@ def test_bench_contract():
     assert e2e["value"] > 0 and e2e["h2d_bytes_per_step"] > 0 and e2e["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] >= 5  # at least the plain kernel every step
     assert set(d["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
+
+
+def test_reference_arm_never_maps_the_product():
+    """The reference arm times the reference engine alone: its process maps
+    oracle/_ref/libsplbref.so and never libsplbcu.so (the C3 sample is
+    voxelised by oracle/geometry_gen.py and classified by the reference)."""
+    ref = os.path.join(ROOT, "oracle", "_ref", "libsplbref.so")
+    if not os.path.exists(ref):
+        pytest.skip("oracle/_ref not built")
+    code = ("import sys; sys.argv=['bench.py']; import bench; "
+            "v = bench.cpu_reference_run('c3', 1, 1.0, 1.0, 1, 'baseline'); "
+            "maps = open('/proc/self/maps').read(); "
+            "print('REF', 'libsplbref' in maps, 'PRODUCT', 'libsplbcu' in maps, v[3])")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = [x for x in r.stdout.splitlines() if x.startswith("REF")][0].split()
+    assert line[1] == "True" and line[3] == "False", line
+    assert int(line[4]) == 3478268  # the C3-shaped sample R0=32 L0=160
