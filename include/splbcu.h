@@ -80,14 +80,17 @@ typedef struct splbcu_params {
     double rho0;
     double dt_s;
     int32_t layout;             /* layout of host-visible stores/maps (AoS/SoA) */
-    int32_t scheme;             /* push/pull: both run the push kernels (bitwise
-                                   identical by the reference's own contract,
-                                   engine.hpp:20-22) */
+    int32_t scheme;             /* 0 push (update_push), 1 pull (update_pull +
+                                   fill_send_slots, engine.hpp:435-502; bitwise
+                                   identical to push, engine.hpp:20-22).  With
+                                   storage = 1 the AA scheme runs either way. */
     int32_t sequence;           /* classic/reordered exchange order */
     int32_t workers;            /* logical workers (slabs) */
     uint64_t capture_period;    /* 0 disables field captures */
     int32_t observe_iolets;     /* per-step iolet time series */
-    double exchange_timeout_s;
+    double exchange_timeout_s;  /* engine.hpp:92-101: a run fails when no step
+                                   completes for this long (dead or stuck
+                                   neighbour, one process per GPU) */
     /* B200 extension: devices the workers are placed on, round robin.
      * n_devices == 0 means {current device}. */
     int32_t n_devices;
@@ -241,7 +244,12 @@ int splbcu_sim_create_dist_source(const splbcu_source* src, const splbcu_bc* bcs
  * splbcu_sim_partition returns NULL); sites of the whole domain. */
 int32_t splbcu_sim_slab_local(const splbcu_sim* s);
 uint64_t splbcu_sim_n_sites(const splbcu_sim* s);
-/* run(nSteps) (engine.hpp:155-197). */
+/* run(nSteps) (engine.hpp:155-197).  The steps are enqueued and the
+ * PREVIOUS run is completed before returning (so consecutive calls keep the
+ * GPU busy); every accessor below completes the run in flight first, so the
+ * results are those of a synchronous engine.  A run with captures, and every
+ * run under SPLBCU_SYNC_RUN=1, completes before returning.  An exchange
+ * failure is reported by this call or, at the latest, by the next one. */
 int splbcu_sim_run(splbcu_sim* s, uint64_t n_steps);
 uint64_t splbcu_sim_steps_run(const splbcu_sim* s);
 double splbcu_sim_step_loop_seconds(const splbcu_sim* s);
