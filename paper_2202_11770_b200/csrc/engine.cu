@@ -377,6 +377,8 @@ struct WorkerDev {
     DevMem dtab, gbase;
     DevMem ctile;  // tile-major copy of dtab/gbase (T = 256), see build_table_tiles
     DevMem rtab;   // run-length table of the mid-group plain range (T = 256), see build_run_table
+    DevMem tile_ctr;  // dynamic tile counters of the bulk launches of one step (lbm_push_dyn)
+    uint32_t ctr_used = 0;
     bool rtab_ok = false;
     uint32_t rtab_escaped = 0;  // (direction, group)s read from the u32 table
     uint64_t PG = 0;
@@ -1379,6 +1381,28 @@ class Engine {
     }
 #endif
 
+    // Persistent TMA kernel with a dynamic tile order (mid-group range only).
+    template <int T, int S, int B>
+    void launch_dyn(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e) {
+        using L0 = PushTmaSmem<T, S, false>;
+        constexpr uint32_t kBytes = S * L0::kF + S * 8 + S * 4;
+        const int resident = resident_ctas(lbm_push_dyn<T, S, B>, wk.dev, T, kBytes);
+        const uint32_t base = b & ~31u;
+        const uint32_t ntiles = (e - base + T - 1) / T;
+        const unsigned grid = unsigned(std::min<uint32_t>(ntiles, uint32_t(resident)));
+        check_tiles(wk, base, ntiles, T);
+        constexpr uint32_t kCtr = 256;
+        if (!wk.tile_ctr.p) wk.tile_ctr.alloc<unsigned>(kCtr);
+        if (wk.ctr_used + 1 > kCtr) wk.ctr_used = 0;
+        unsigned* ctr = wk.tile_ctr.get<unsigned>() + wk.ctr_used++;
+        CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned), s));
+        Planes19 pl;
+        for (int i = 0; i < kQ; ++i) pl.p[i] = wk.f_new() + uint64_t(i) * wk.P;
+        lbm_push_dyn<T, S, B><<<grid, T, kBytes, s>>>(wk.f_old(), wk.f_new(), wk.dtab.get<int16_t>(),
+                                                      wk.gbase.get<uint32_t>(), wk.tab.get<uint32_t>(), wk.P, wk.PG, b,
+                                                      e, omega, ctr, pl);
+    }
+
     // Persistent TMA kernel over the run-length table (mid-group range only).
     template <int T, int S, int B>
     void launch_run(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e) {
@@ -1507,7 +1531,7 @@ class Engine {
         (void)v;
         return true;
 #else
-        return v == 0 || v == 24 || v == 43 || v == 59 || v == 60 || v == 64 || v == 71 || v == 72;
+        return v == 0 || v == 24 || v == 43 || v == 59 || v == 60 || v == 64 || v == 71 || v == 72 || v == 76;
 #endif
     }
     void launch_plain(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia, bool mid) {
@@ -1516,6 +1540,7 @@ class Engine {
 #endif
         if (plain_variant == 24) return launch_tma<256, 2, 2, false, 2>(wk, s, b, e);
         if (plain_variant == 71 && mid && wk.rtab_ok) return launch_run<256, 2, 2>(wk, s, b, e);
+        if (plain_variant == 76 && mid && wk.ctab_ok) return launch_dyn<256, 2, 2>(wk, s, b, e);
 #ifdef SPLBCU_TUNING
         // warp-autonomous push kernel: measured slower (C3 developed 14.8-15.1k
         // vs 16.6-16.7k for the CTA-wide TMA pipeline, profiles/r02/sweep_dev_pushw.jsonl)
@@ -1539,7 +1564,8 @@ class Engine {
     // defaults, profiles/r01_sweep_*.log).  Returns false for the built-in ones.
     bool launch_tuning_variant(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia, bool mid) {
         if (plain_variant == 0 || plain_variant == 24 || plain_variant == 43 || plain_variant == 59 ||
-            plain_variant == 60 || plain_variant == 64 || plain_variant == 71 || plain_variant == 72)
+            plain_variant == 60 || plain_variant == 64 || plain_variant == 71 || plain_variant == 72 ||
+            plain_variant == 76)
             return false;
         if (plain_variant == 69 || plain_variant == 70) {  // tile-major table, one bulk copy per tile
             if (!(mid && wk.ctab_ok)) launch_tma<256, 2, 2, false, 6>(wk, s, b, e);

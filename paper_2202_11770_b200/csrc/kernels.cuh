@@ -901,6 +901,86 @@ lbm_push_w(const double* __restrict__ fo, double* __restrict__ fn, const int16_t
     cp_async_wait<0>();
 }
 
+// ---- dynamic tile order (delta table, just-in-time table loads) ------------
+// lbm_push_tmc<.., 6> with the persistent CTAs taking tiles from a global
+// counter instead of the fixed stride blockIdx.x + k * grid: the tiles in
+// flight stay within ~one grid's width of the frontier however the CTAs drift
+// apart, so the scattered stores of the whole GPU hit a compact window of each
+// direction plane (the effect that cutting the bulk range into parts buys).
+template <int T, int S, int kMinBlocks>
+__global__ void __launch_bounds__(T, kMinBlocks)
+lbm_push_dyn(const double* __restrict__ fo, double* __restrict__ fn, const int16_t* __restrict__ dtab,
+             const uint32_t* __restrict__ gbase, const uint32_t* __restrict__ tab, uint64_t P, uint64_t PG,
+             uint32_t begin, uint32_t end, double omega, unsigned* __restrict__ counter,
+             const __grid_constant__ Planes19 planes) {
+    using L = PushTmaSmem<T, S, false>;
+    constexpr uint32_t kStage = L::kF;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S * kStage);
+    uint32_t* tidx = reinterpret_cast<uint32_t*>(bar + S);  // tile of each stage
+    const uint32_t base = begin & ~31u;
+    const uint32_t ntiles = (end - base + T - 1) / T;
+    const uint32_t tid = threadIdx.x;
+    const int lane = int(tid & 31);
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) mbar_init(&bar[s], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    const uint64_t policy = evict_normal_policy();
+    auto issue = [&](uint32_t k) {  // thread 0: take the next tile for iteration k
+        const int st = int(k % S);
+        const uint32_t tile = atomicAdd(counter, 1u);
+        tidx[st] = tile;
+        if (tile >= ntiles) return;
+        unsigned char* buf = smem + st * kStage;
+        const uint64_t t0 = uint64_t(base) + uint64_t(tile) * T;
+        mbar_expect_tx(&bar[st], kStage);
+#pragma unroll 1
+        for (int i = 0; i < kQ; ++i) bulk_g2s(buf + i * T * 8, fo + uint64_t(i) * P + t0, T * 8, &bar[st], policy);
+    };
+    if (tid == 0)
+        for (uint32_t k = 0; k + 1 < uint32_t(S); ++k) issue(k);
+    __syncthreads();
+    for (uint32_t k = 0;; ++k) {
+        const int st = int(k % S);
+        const uint32_t tile = tidx[st];
+        if (tile >= ntiles) break;
+        if (tid == 0) issue(k + S - 1);
+        const uint32_t s = base + tile * T + tid;
+        const bool live = s >= begin && s < end;
+        int16_t dl[kQ - 1];
+#pragma unroll
+        for (int i = 0; i < kQ - 1; ++i) dl[i] = live ? __ldg(dtab + uint64_t(i) * P + s) : int16_t(0);
+        const uint32_t breg = (lane < kQ - 1) ? __ldg(gbase + uint64_t(lane) * PG + (s >> 5)) : 0u;
+        mbar_wait(&bar[st], (k / S) & 1u);
+        const double* fs = reinterpret_cast<const double*>(smem + st * kStage);
+        double f[kQ];
+#pragma unroll
+        for (int i = 0; i < kQ; ++i) f[i] = fs[i * T + tid];
+        const Macro m = macro_of(f);
+        double feq[kQ];
+        feq_all(m.rho, m.ux, m.uy, m.uz, feq);
+        if (live) fn[s] = relax(f[0], feq[0], omega);
+#pragma unroll
+        for (int i = 1; i < kQ; ++i) {
+            const double fpost = relax(f[i], feq[i], omega);
+            const uint32_t b = __shfl_sync(0xffffffffu, breg, i - 1);
+            const int d = dl[i - 1];
+            uint32_t t = b + uint32_t(lane) + uint32_t(d);
+            const uint32_t esc = (d == kDeltaEscape) && live;
+            asm("{\n .reg .pred p;\n setp.ne.u32 p, %1, 0;\n @p ld.global.nc.u32 %0, [%2];\n}"
+                : "+r"(t)
+                : "r"(esc), "l"(tab + uint64_t(i - 1) * P + s));
+            const bool bb = d == kDeltaBounce;
+            const uintptr_t pb = reinterpret_cast<uintptr_t>(bb ? planes.p[inv(i)] : planes.p[i]);
+            double* dst = reinterpret_cast<double*>(pb) + (bb ? s : t);
+            if (live) *dst = fpost;
+        }
+        __syncthreads();  // stage st is free; the next stage's tile index is visible
+    }
+}
+
 // ---- warp-specialised 2-D TMA variant --------------------------------------
 // One TMA instruction per tile moves the whole [19 planes x T sites] f box
 // (and, optionally, the [18 x T] table box) described by a CUtensorMap over

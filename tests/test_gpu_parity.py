@@ -86,7 +86,7 @@ def test_runs_bit_exact(product, golden, golden_arrays, key):
 @pytest.mark.parametrize("variant", ["1", "3", "5", "10", "11", "12", "13", "14", "15", "16", "17", "18", "19",
                                      "20", "21", "22", "23", "24", "25", "26", "27", "28", "29", "30", "31", "32", "33", "34", "35", "36", "40", "41", "43", "44", "45", "46", "47", "48",
                                      "42", "49", "52", "53", "54", "55", "56", "57", "58", "59", "67", "68", "69",
-                                     "70", "71", "74", "75"])
+                                     "70", "71", "74", "75", "76"])
 def test_kernel_variants_bit_exact(product, golden, variant, monkeypatch):
     """Every launch shape of the plain kernel (register-resident and
     TMA-pipelined persistent) gives the reference's bits."""
@@ -415,7 +415,7 @@ def test_online_bulk_kernel_choice(product, monkeypatch):
     assert np.array_equal(f_auto, f43) and np.array_equal(f43, f59) and np.array_equal(f59, f71)
 
 
-@pytest.mark.parametrize("variant", ["43", "59", "71"])
+@pytest.mark.parametrize("variant", ["43", "59", "71", "76"])
 def test_chunked_bulk_range_bit_exact(product, golden, variant, monkeypatch):
     """SPLBCU_BULK_CHUNK (tuning knob) cuts the bulk range into several
     launches at 256-site boundaries; the bits do not change."""
