@@ -1435,11 +1435,14 @@ class Engine {
 
     // The bulk range as `parts` launches of about equal size (at most
     // ~kBulkChunk sites each), cut at absolute 256-site boundaries.  Measured
-    // on B200, C3 tree 1.07e8 sites from rest: one launch 16,190 MSUPS
-    // (just-in-time kernel) / 16,556 (prefetch); 27e6-site parts 17,663 /
-    // 16,844; 13.5e6-site parts 17,941 / 16,952 (profiles/r01_sweep_chunk.log).
-    // SPLBCU_BULK_CHUNK overrides the part size (0: one launch).
-    static constexpr uint64_t kBulkChunk = 13500000;
+    // on B200, C3 tree 1.07e8 sites, just-in-time kernel: from rest one launch
+    // 16,190 MSUPS, 13.5e6-site parts 17,941 (profiles/r01_sweep_chunk.log);
+    // in a developed flow 13.5e6-site parts 16,684, 9e6 17,192, 6.75e6
+    // 17,028-17,330, 4.5e6 17,396, 3.4e6 17,312, while from rest 6.75e6 and
+    // 13.5e6 tie (17,932 / 17,957) and the 1e7-site pipe gains 5 % with the
+    // run-length table (profiles/r02/sweep4_*).  SPLBCU_BULK_CHUNK overrides
+    // the part size (0: one launch).
+    static constexpr uint64_t kBulkChunk = 6750000;
     uint64_t bulk_chunk = [] {
         const char* v = getenv("SPLBCU_BULK_CHUNK");
         return v ? uint64_t(atoll(v)) : kBulkChunk;
