@@ -197,8 +197,8 @@ def cpu_reference_run(name, steps_cap, seconds, scale, warmup=1, sample="baselin
     return d.n_sites() * steps / T / 1e6, cores, steps, d.n_sites(), desc
 
 
-BULK_KERNELS = {0: "void lbm_push_tmc<256, 2, 2, 6>", 1: "void lbm_push_tmc<256, 2, 2, 4102>",
-                2: "void lbm_push_run<256, 2, 2>"}
+BULK_KERNELS = {0: "void lbm_push_dyn<256, 2, 2>", 1: "void lbm_push_tmc<256, 2, 2, 4102>",
+                2: "void lbm_push_run<256, 2, 2>", 3: "void lbm_push_tmc<256, 2, 2, 6>"}
 RUN_BYTES_PER_SITE = 19 * 8 + 19 * 8 + 3456 / 256  # 317.5: run-length table kernel
 
 
@@ -257,7 +257,7 @@ def timed_loop(sim, n, steps, warmup, bps, barrier, max_over_ranks, gpu, name, d
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
             "frac": achieved / hbm if achieved else None,
             "traffic": (traffic * kn / kl) if (traffic and kl) else None,
-            "peak_source": src, "kernel": "lbm_push_tmc / lbm_push_run (Inner+Wall fused collide+stream, TMA-pipelined)",
+            "peak_source": src, "kernel": "lbm_push_dyn / lbm_push_tmc / lbm_push_run (Inner+Wall fused collide+stream, TMA-pipelined)",
             "kernel_template": kernel, "traffic_source": traffic_key,
             "bytes_per_site": bps, "achieved_376": achieved_376,
             "frac_376": achieved_376 / hbm if achieved_376 else None,

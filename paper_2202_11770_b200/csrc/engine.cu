@@ -355,8 +355,8 @@ struct WorkerDev {
     // watchdog's progress marks
     std::vector<cudaEvent_t> prog;
     // Online choice of the bulk (mid) plain kernel: just-in-time table loads
-    // (mid_pick 0), the prefetch kernel (1) or the run-length table (2).  All
-    // give the same bits; which
+    // with a dynamic tile order (mid_pick 0), the prefetch kernel (1) or the
+    // run-length table (2).  All give the same bits; which
     // is faster depends on the geometry and on the flow (from rest vs developed,
     // DESIGN §3), so every kTuneEvery mid launches the next 2 x kTuneReps
     // launches alternate the two under CUDA events and the faster is kept.
@@ -1288,7 +1288,6 @@ class Engine {
     // ---- stepping -----------------------------------------------------------
     // Launch-shape variants of the plain kernel (SPLBCU_PLAIN_VARIANT picks
     // one for tuning; the default is the measured best).
-    static constexpr uint32_t kPrefetchMinSites = 20000000;
     int plain_variant = [] {
         const char* v = getenv("SPLBCU_PLAIN_VARIANT");
         return v ? atoi(v) : 0;
@@ -1419,17 +1418,20 @@ class Engine {
     }
 
     // Which kernel the bulk (mid) plain range launches now on this process's
-    // first worker: 0 just-in-time table loads (<256,2,2,6>), 1 the prefetch
-    // kernel (<256,2,2,4102>), -1 any other (forced variant, u32 table).
+    // first worker:
+    // 0 dynamic tile order (just-in-time table loads), 1 prefetch kernel,
+    // 2 run-length table, 3 the fixed-order just-in-time kernel; -1 other.
+    int bulk_kernel_of(const WorkerDev& wk) const {
+        if (!wk.ctab_ok) return -1;
+        if (plain_variant == 43) return 3;
+        if (plain_variant == 76) return 0;
+        if (plain_variant == 59) return 1;
+        if (plain_variant == 71) return wk.rtab_ok ? 2 : -1;
+        return plain_variant == 0 ? wk.mid_pick : -1;
+    }
     int bulk_kernel() const {
-        for (const auto& wp : W) {
-            if (!wp) continue;
-            if (!wp->ctab_ok) return -1;
-            if (plain_variant == 43) return 0;
-            if (plain_variant == 59) return 1;
-            if (plain_variant == 71) return wp->rtab_ok ? 2 : -1;
-            return plain_variant == 0 ? wp->mid_pick : -1;
-        }
+        for (const auto& wp : W)
+            if (wp) return bulk_kernel_of(*wp);
         return -1;
     }
 
@@ -1447,6 +1449,7 @@ class Engine {
         const char* v = getenv("SPLBCU_BULK_CHUNK");
         return v ? uint64_t(atoll(v)) : kBulkChunk;
     }();
+    const bool parts_forced = getenv("SPLBCU_BULK_CHUNK") != nullptr;
     template <class Fn>
     void for_parts(uint32_t b, uint32_t e, Fn&& fn) {
         const uint64_t n = uint64_t(e - b);
@@ -1461,6 +1464,9 @@ class Engine {
         }
     }
     void launch_bulk(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia) {
+        // the dynamic tile order keeps the CTAs together by itself: one launch
+        // (C3 developed 17,631 vs 17,186 in 6.75e6-site parts, profiles/r02/dyn_*)
+        if (bulk_kernel_of(wk) == 0 && !parts_forced) return launch_plain(wk, s, b, e, ia, true);
         for_parts(b, e, [&](uint32_t c, uint32_t c1) { launch_plain(wk, s, c, c1, ia, true); });
     }
 
@@ -1471,8 +1477,8 @@ class Engine {
     // of a template also carries its one-time setup), and the faster kernel
     // is kept from the moment the events have completed.
     void launch_mid_tuned(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia) {
-        // prior before the first measurement: the prefetch kernel on large ranges
-        if (wk.mid_launches == 0) wk.mid_pick = (e - b >= kPrefetchMinSites) ? 1 : 0;
+        // prior before the first measurement: the dynamic-order kernel
+        if (wk.mid_launches == 0) wk.mid_pick = 0;
         if (!autotune || !wk.ctab_ok) {
             launch_bulk(wk, s, b, e, ia);
             ++wk.mid_launches;
@@ -1543,7 +1549,6 @@ class Engine {
 #endif
         if (plain_variant == 24) return launch_tma<256, 2, 2, false, 2>(wk, s, b, e);
         if (plain_variant == 71 && mid && wk.rtab_ok) return launch_run<256, 2, 2>(wk, s, b, e);
-        if (plain_variant == 76 && mid && wk.ctab_ok) return launch_dyn<256, 2, 2>(wk, s, b, e);
 #ifdef SPLBCU_TUNING
         // warp-autonomous push kernel: measured slower (C3 developed 14.8-15.1k
         // vs 16.6-16.7k for the CTA-wide TMA pipeline, profiles/r02/sweep_dev_pushw.jsonl)
@@ -1556,7 +1561,8 @@ class Engine {
         if (mid && wk.ctab_ok) {
             const bool pf = plain_variant == 59 || (plain_variant == 0 && wk.mid_pick == 1);
             if (pf) launch_tmc<256, 2, 2, 4102>(wk, s, b, e);
-            else launch_tmc<256, 2, 2, 6>(wk, s, b, e);
+            else if (plain_variant == 43) launch_tmc<256, 2, 2, 6>(wk, s, b, e);
+            else launch_dyn<256, 2, 2>(wk, s, b, e);
         } else {
             launch_tma<256, 2, 2, false, 6>(wk, s, b, e);
         }

@@ -392,7 +392,8 @@ def test_output_files_match_reference(product, reference, tmp_path):
 
 def test_online_bulk_kernel_choice(product, monkeypatch):
     """The engine times the bulk kernels online (every 500 launches: delta
-    table just-in-time / prefetch, run-length table) and keeps the fastest; switching between them mid-run leaves the bits alone,
+    table with a dynamic tile order / prefetch, run-length table) and keeps
+    the fastest; switching between them mid-run leaves the bits alone,
     and splbcu_sim_bulk_kernel reports the choice (forced variants included)."""
     d = product.build_pipe(16, 128)
     bcs = cases.make_bcs(product, ("pressure", cases.CS2 * 1.001, cases.CS2 * 0.999))
@@ -407,12 +408,14 @@ def test_online_bulk_kernel_choice(product, monkeypatch):
         return s.bulk_kernel(), s.snapshot_fields()
 
     k_auto, f_auto = run(None)
+    k76, f76 = run("76")
     k43, f43 = run("43")
     k59, f59 = run("59")
     k71, f71 = run("71")
     k1, _ = run("24", 2)  # the u32-table kernel everywhere
-    assert k_auto in (0, 1, 2) and (k43, k59, k71, k1) == (0, 1, 2, -1)
-    assert np.array_equal(f_auto, f43) and np.array_equal(f43, f59) and np.array_equal(f59, f71)
+    assert k_auto in (0, 1, 2) and (k76, k59, k71, k43, k1) == (0, 1, 2, 3, -1)
+    for f in (f76, f43, f59, f71):
+        assert np.array_equal(f_auto, f)
 
 
 @pytest.mark.parametrize("variant", ["43", "59", "71", "76"])
