@@ -1380,6 +1380,17 @@ class Engine {
     }
 #endif
 
+    // A zeroed tile counter for one dynamic-order launch on stream s (a ring of
+    // slots, each zeroed stream-ordered right before its launch).
+    unsigned* tile_counter(WorkerDev& wk, cudaStream_t s) {
+        constexpr uint32_t kCtr = 256;
+        if (!wk.tile_ctr.p) wk.tile_ctr.alloc<unsigned>(kCtr);
+        if (wk.ctr_used + 1 > kCtr) wk.ctr_used = 0;
+        unsigned* ctr = wk.tile_ctr.get<unsigned>() + wk.ctr_used++;
+        CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned), s));
+        return ctr;
+    }
+
     // Persistent TMA kernel with a dynamic tile order (mid-group range only).
     template <int T, int S, int B>
     void launch_dyn(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e) {
@@ -1390,11 +1401,7 @@ class Engine {
         const uint32_t ntiles = (e - base + T - 1) / T;
         const unsigned grid = unsigned(std::min<uint32_t>(ntiles, uint32_t(resident)));
         check_tiles(wk, base, ntiles, T);
-        constexpr uint32_t kCtr = 256;
-        if (!wk.tile_ctr.p) wk.tile_ctr.alloc<unsigned>(kCtr);
-        if (wk.ctr_used + 1 > kCtr) wk.ctr_used = 0;
-        unsigned* ctr = wk.tile_ctr.get<unsigned>() + wk.ctr_used++;
-        CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned), s));
+        unsigned* ctr = tile_counter(wk, s);
         Planes19 pl;
         for (int i = 0; i < kQ; ++i) pl.p[i] = wk.f_new() + uint64_t(i) * wk.P;
         lbm_push_dyn<T, S, B><<<grid, T, kBytes, s>>>(wk.f_old(), wk.f_new(), wk.dtab.get<int16_t>(),
@@ -1404,8 +1411,8 @@ class Engine {
 
     // Persistent TMA kernel over the run-length table (mid-group range only).
     template <int T, int S, int B>
-    void launch_run(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e) {
-        constexpr uint32_t kBytes = S * (uint32_t(kQ) * T * 8 + RunTab<T>::kBytes) + S * 8;
+    void launch_run(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, bool dyn = false) {
+        constexpr uint32_t kBytes = S * (uint32_t(kQ) * T * 8 + RunTab<T>::kBytes) + S * 8 + S * 4;
         const int resident = resident_ctas(lbm_push_run<T, S, B>, wk.dev, T, kBytes);
         const uint32_t base = b & ~uint32_t(T - 1);
         const uint32_t ntiles = (e - base + T - 1) / T;
@@ -1413,8 +1420,9 @@ class Engine {
         check_tiles(wk, base, ntiles, T);
         Planes19 pl;
         for (int i = 0; i < kQ; ++i) pl.p[i] = wk.f_new() + uint64_t(i) * wk.P;
+        unsigned* ctr = dyn ? tile_counter(wk, s) : nullptr;
         lbm_push_run<T, S, B><<<grid, T, kBytes, s>>>(wk.f_old(), wk.f_new(), wk.rtab.get<unsigned char>(),
-                                                      wk.tab.get<uint32_t>(), wk.P, b, e, omega, pl);
+                                                      wk.tab.get<uint32_t>(), wk.P, b, e, omega, pl, ctr);
     }
 
     // Which kernel the bulk (mid) plain range launches now on this process's
@@ -1426,7 +1434,7 @@ class Engine {
         if (plain_variant == 43) return 3;
         if (plain_variant == 76) return 0;
         if (plain_variant == 59) return 1;
-        if (plain_variant == 71) return wk.rtab_ok ? 2 : -1;
+        if (plain_variant == 71 || plain_variant == 77) return wk.rtab_ok ? 2 : -1;
         return plain_variant == 0 ? wk.mid_pick : -1;
     }
     int bulk_kernel() const {
@@ -1466,7 +1474,7 @@ class Engine {
     void launch_bulk(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia) {
         // the dynamic tile order keeps the CTAs together by itself: one launch
         // (C3 developed 17,631 vs 17,186 in 6.75e6-site parts, profiles/r02/dyn_*)
-        if (bulk_kernel_of(wk) == 0 && !parts_forced) return launch_plain(wk, s, b, e, ia, true);
+        if ((bulk_kernel_of(wk) == 0 || plain_variant == 77) && !parts_forced) return launch_plain(wk, s, b, e, ia, true);
         for_parts(b, e, [&](uint32_t c, uint32_t c1) { launch_plain(wk, s, c, c1, ia, true); });
     }
 
@@ -1540,7 +1548,8 @@ class Engine {
         (void)v;
         return true;
 #else
-        return v == 0 || v == 24 || v == 43 || v == 59 || v == 60 || v == 64 || v == 71 || v == 72 || v == 76;
+        return v == 0 || v == 24 || v == 43 || v == 59 || v == 60 || v == 64 || v == 71 || v == 72 || v == 76 ||
+               v == 77 || v == 78;
 #endif
     }
     void launch_plain(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia, bool mid) {
@@ -1549,6 +1558,7 @@ class Engine {
 #endif
         if (plain_variant == 24) return launch_tma<256, 2, 2, false, 2>(wk, s, b, e);
         if (plain_variant == 71 && mid && wk.rtab_ok) return launch_run<256, 2, 2>(wk, s, b, e);
+        if (plain_variant == 77 && mid && wk.rtab_ok) return launch_run<256, 2, 2>(wk, s, b, e, true);
 #ifdef SPLBCU_TUNING
         // warp-autonomous push kernel: measured slower (C3 developed 14.8-15.1k
         // vs 16.6-16.7k for the CTA-wide TMA pipeline, profiles/r02/sweep_dev_pushw.jsonl)
@@ -1574,7 +1584,7 @@ class Engine {
     bool launch_tuning_variant(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia, bool mid) {
         if (plain_variant == 0 || plain_variant == 24 || plain_variant == 43 || plain_variant == 59 ||
             plain_variant == 60 || plain_variant == 64 || plain_variant == 71 || plain_variant == 72 ||
-            plain_variant == 76)
+            plain_variant == 76 || plain_variant == 77 || plain_variant == 78)
             return false;
         if (plain_variant == 69 || plain_variant == 70) {  // tile-major table, one bulk copy per tile
             if (!(mid && wk.ctab_ok)) launch_tma<256, 2, 2, false, 6>(wk, s, b, e);
@@ -2195,14 +2205,15 @@ class Engine {
     // advance_one (engine.hpp:330-363) for every local worker.
     // ---- AA single-buffer scheme ------------------------------------------------
     template <int T, int S, int B>
-    void launch_aa_even_tma(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e) {
+    void launch_aa_even_tma(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, bool dyn = false) {
         using Lm = PushTmaSmem<T, S, false>;
-        const int resident = resident_ctas(lbm_aa_even_tma<T, S, B>, wk.dev, T, Lm::kBytes);
+        const int resident = resident_ctas(lbm_aa_even_tma<T, S, B>, wk.dev, T, Lm::kBytes + S * 4);
         const uint32_t base = b & ~3u;
         const uint32_t ntiles = (e - base + T - 1) / T;
         const unsigned grid = unsigned(std::min<uint32_t>(ntiles, uint32_t(resident)));
         check_tiles(wk, base, ntiles, T);
-        lbm_aa_even_tma<T, S, B><<<grid, T, Lm::kBytes, s>>>(wk.f_old(), wk.P, b, e, omega);
+        unsigned* ctr = dyn ? tile_counter(wk, s) : nullptr;
+        lbm_aa_even_tma<T, S, B><<<grid, T, Lm::kBytes + S * 4, s>>>(wk.f_old(), wk.P, b, e, omega, ctr);
     }
 
 #ifdef SPLBCU_TUNING
@@ -2260,7 +2271,8 @@ class Engine {
         const unsigned nb = blocks_for(e - b, 128);
         if (!odd) {
             if (iolet) lbm_aa_even<true><<<blocks_for(e - b), 256, 0, s>>>(F, tab, wk.P, b, e, omega, ia);
-            else if (wk.tma_ok) launch_aa_even_tma<256, 2, 2>(wk, s, b, e);  // one launch: parts measured no faster
+            else if (wk.tma_ok)  // one launch: parts measured no faster; 78: dynamic tile order
+                launch_aa_even_tma<256, 2, 2>(wk, s, b, e, plain_variant == 78 && timed);
             else lbm_aa_even<false><<<blocks_for(e - b), 256, 0, s>>>(F, tab, wk.P, b, e, omega, ia);
         } else if (remote) {
             if (iolet) lbm_aa_odd<true, true, 128, 4><<<nb, 128, 0, s>>>(F, tab, wk.P, b, e, omega, ia, h);

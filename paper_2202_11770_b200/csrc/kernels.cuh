@@ -726,12 +726,13 @@ template <int T, int S, int kMinBlocks>
 __global__ void __launch_bounds__(T, kMinBlocks)
 lbm_push_run(const double* __restrict__ fo, double* __restrict__ fn, const unsigned char* __restrict__ rtab,
              const uint32_t* __restrict__ tab, uint64_t P, uint32_t begin, uint32_t end, double omega,
-             const __grid_constant__ Planes19 planes) {
+             const __grid_constant__ Planes19 planes, unsigned* __restrict__ counter = nullptr) {
     using RT = RunTab<T>;
     constexpr uint32_t kF = uint32_t(kQ) * T * 8;
     constexpr uint32_t kStage = kF + RT::kBytes;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S * kStage);
+    uint32_t* tidx = reinterpret_cast<uint32_t*>(bar + S);  // dynamic order: tile of each stage
     const uint32_t base = begin & ~uint32_t(T - 1);  // tiles on the table's absolute grid
     const uint32_t ntiles = (end - base + T - 1) / T;
     const uint32_t G = gridDim.x;
@@ -745,7 +746,8 @@ lbm_push_run(const double* __restrict__ fo, double* __restrict__ fn, const unsig
     __syncthreads();
     const uint64_t policy = evict_normal_policy();
     auto issue = [&](uint32_t k) {
-        const uint32_t tile = blockIdx.x + k * G;
+        uint32_t tile = blockIdx.x + k * G;
+        if (counter) tidx[k % S] = tile = atomicAdd(counter, 1u);
         if (tile >= ntiles) return;
         const int st = int(k % S);
         unsigned char* buf = smem + st * kStage;
@@ -757,8 +759,9 @@ lbm_push_run(const double* __restrict__ fo, double* __restrict__ fn, const unsig
     };
     if (tid == 0)
         for (uint32_t k = 0; k + 1 < uint32_t(S); ++k) issue(k);
+    if (counter) __syncthreads();
     for (uint32_t k = 0;; ++k) {
-        const uint32_t tile = blockIdx.x + k * G;
+        const uint32_t tile = counter ? tidx[k % S] : blockIdx.x + k * G;
         if (tile >= ntiles) break;
         if (tid == 0) issue(k + S - 1);
         const int st = int(k % S);
@@ -1160,10 +1163,12 @@ lbm_aa_even(double* __restrict__ F, const uint32_t* __restrict__ tab, uint64_t P
 // streaming out, 304 B/site.
 template <int T, int S, int kMinBlocks>
 __global__ void __launch_bounds__(T, kMinBlocks)
-lbm_aa_even_tma(double* __restrict__ F, uint64_t P, uint32_t begin, uint32_t end, double omega) {
+lbm_aa_even_tma(double* __restrict__ F, uint64_t P, uint32_t begin, uint32_t end, double omega,
+                unsigned* __restrict__ counter = nullptr) {
     using L = PushTmaSmem<T, S, false>;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S * L::kStage);
+    uint32_t* tidx = reinterpret_cast<uint32_t*>(bar + S);  // dynamic order: tile of each stage
     const uint32_t base = begin & ~3u;
     const uint32_t ntiles = (end - base + T - 1) / T;
     const uint32_t G = gridDim.x;
@@ -1175,7 +1180,8 @@ lbm_aa_even_tma(double* __restrict__ F, uint64_t P, uint32_t begin, uint32_t end
     __syncthreads();
     const uint64_t policy = evict_normal_policy();
     auto issue = [&](uint32_t k) {
-        const uint32_t tile = blockIdx.x + k * G;
+        uint32_t tile = blockIdx.x + k * G;
+        if (counter) tidx[k % S] = tile = atomicAdd(counter, 1u);
         if (tile >= ntiles) return;
         const int st = int(k % S);
         unsigned char* buf = smem + st * L::kStage;
@@ -1186,8 +1192,9 @@ lbm_aa_even_tma(double* __restrict__ F, uint64_t P, uint32_t begin, uint32_t end
     };
     if (tid == 0)
         for (uint32_t k = 0; k + 1 < uint32_t(S); ++k) issue(k);
+    if (counter) __syncthreads();
     for (uint32_t k = 0;; ++k) {
-        const uint32_t tile = blockIdx.x + k * G;
+        const uint32_t tile = counter ? tidx[k % S] : blockIdx.x + k * G;
         if (tile >= ntiles) break;
         if (tid == 0) issue(k + S - 1);
         const int st = int(k % S);

@@ -86,7 +86,7 @@ def test_runs_bit_exact(product, golden, golden_arrays, key):
 @pytest.mark.parametrize("variant", ["1", "3", "5", "10", "11", "12", "13", "14", "15", "16", "17", "18", "19",
                                      "20", "21", "22", "23", "24", "25", "26", "27", "28", "29", "30", "31", "32", "33", "34", "35", "36", "40", "41", "43", "44", "45", "46", "47", "48",
                                      "42", "49", "52", "53", "54", "55", "56", "57", "58", "59", "67", "68", "69",
-                                     "70", "71", "74", "75", "76"])
+                                     "70", "71", "74", "75", "76", "77"])
 def test_kernel_variants_bit_exact(product, golden, variant, monkeypatch):
     """Every launch shape of the plain kernel (register-resident and
     TMA-pipelined persistent) gives the reference's bits."""
@@ -129,7 +129,7 @@ def test_aa_single_buffer_bit_exact(product, golden, key):
     assert cases.run_digest(res) == golden["runs"][key]
 
 
-@pytest.mark.parametrize("variant", ["0", "60", "61", "62", "63", "64", "65", "66", "72"])
+@pytest.mark.parametrize("variant", ["0", "60", "61", "62", "63", "64", "65", "66", "72", "78"])
 def test_aa_odd_kernel_variants(product, golden, variant, monkeypatch):
     """Odd-step kernels: the default warp-autonomous cp.async pipeline, its
     128-register shape (72), the round-1 register gather over the compressed
