@@ -1549,7 +1549,7 @@ class Engine {
         return true;
 #else
         return v == 0 || v == 24 || v == 43 || v == 59 || v == 60 || v == 64 || v == 71 || v == 72 || v == 76 ||
-               v == 77 || v == 78;
+               v == 77 || v == 78 || v == 79;
 #endif
     }
     void launch_plain(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia, bool mid) {
@@ -1584,7 +1584,7 @@ class Engine {
     bool launch_tuning_variant(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia, bool mid) {
         if (plain_variant == 0 || plain_variant == 24 || plain_variant == 43 || plain_variant == 59 ||
             plain_variant == 60 || plain_variant == 64 || plain_variant == 71 || plain_variant == 72 ||
-            plain_variant == 76 || plain_variant == 77 || plain_variant == 78)
+            plain_variant == 76 || plain_variant == 77 || plain_variant == 78 || plain_variant == 79)
             return false;
         if (plain_variant == 69 || plain_variant == 70) {  // tile-major table, one bulk copy per tile
             if (!(mid && wk.ctab_ok)) launch_tma<256, 2, 2, false, 6>(wk, s, b, e);
@@ -2271,8 +2271,9 @@ class Engine {
         const unsigned nb = blocks_for(e - b, 128);
         if (!odd) {
             if (iolet) lbm_aa_even<true><<<blocks_for(e - b), 256, 0, s>>>(F, tab, wk.P, b, e, omega, ia);
-            else if (wk.tma_ok)  // one launch: parts measured no faster; 78: dynamic tile order
-                launch_aa_even_tma<256, 2, 2>(wk, s, b, e, plain_variant == 78 && timed);
+            else if (wk.tma_ok)  // the bulk (mid) range in one launch, dynamic tile order
+                // (C3 developed even step 22,201 vs 19,532 fixed order; 79 forces the fixed order)
+                launch_aa_even_tma<256, 2, 2>(wk, s, b, e, timed && plain_variant != 79);
             else lbm_aa_even<false><<<blocks_for(e - b), 256, 0, s>>>(F, tab, wk.P, b, e, omega, ia);
         } else if (remote) {
             if (iolet) lbm_aa_odd<true, true, 128, 4><<<nb, 128, 0, s>>>(F, tab, wk.P, b, e, omega, ia, h);
