@@ -1549,7 +1549,7 @@ class Engine {
         return true;
 #else
         return v == 0 || v == 24 || v == 43 || v == 59 || v == 60 || v == 64 || v == 71 || v == 72 || v == 76 ||
-               v == 77 || v == 78 || v == 79;
+               v == 77 || v == 78 || v == 79 || v == 80;
 #endif
     }
     void launch_plain(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia, bool mid) {
@@ -1584,7 +1584,8 @@ class Engine {
     bool launch_tuning_variant(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia, bool mid) {
         if (plain_variant == 0 || plain_variant == 24 || plain_variant == 43 || plain_variant == 59 ||
             plain_variant == 60 || plain_variant == 64 || plain_variant == 71 || plain_variant == 72 ||
-            plain_variant == 76 || plain_variant == 77 || plain_variant == 78 || plain_variant == 79)
+            plain_variant == 76 || plain_variant == 77 || plain_variant == 78 || plain_variant == 79 ||
+            plain_variant == 80)
             return false;
         if (plain_variant == 69 || plain_variant == 70) {  // tile-major table, one bulk copy per tile
             if (!(mid && wk.ctab_ok)) launch_tma<256, 2, 2, false, 6>(wk, s, b, e);
@@ -2248,15 +2249,16 @@ class Engine {
 
     // Warp-autonomous AA odd kernel (persistent; cp.async gathers one tile ahead).
     template <int NW, int B>
-    void launch_aa_odd_w(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e) {
+    void launch_aa_odd_w(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, bool dyn = false) {
         using Lm = AaOddW<NW, B>;
         const int resident = resident_ctas(lbm_aa_odd_w<NW, B>, wk.dev, NW * 32, Lm::kBytes);
         const uint32_t ntiles = (e - (b & ~31u) + 31) / 32;
         const unsigned grid = unsigned(std::min<uint32_t>((ntiles + NW - 1) / NW, uint32_t(resident)));
         Planes19 pl;
         for (int i = 0; i < kQ; ++i) pl.p[i] = wk.f_old() + uint64_t(i) * wk.P;
+        unsigned* ctr = dyn ? tile_counter(wk, s) : nullptr;
         lbm_aa_odd_w<NW, B><<<grid, NW * 32, Lm::kBytes, s>>>(wk.f_old(), wk.dtab.get<int16_t>(), wk.gbase.get<uint32_t>(),
-                                                           wk.tab.get<uint32_t>(), wk.P, wk.PG, b, e, omega, pl);
+                                                           wk.tab.get<uint32_t>(), wk.P, wk.PG, b, e, omega, pl, ctr);
     }
 
     void launch_aa_range(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, bool iolet, const double* staged,
@@ -2304,7 +2306,7 @@ class Engine {
             } else if (timed && wk.ctab_ok && v != 60) {
                 // default: warp-autonomous pipeline, cp.async gathers one tile
                 // ahead (C3 developed, odd step: 14.2k MSUPS; C2 14.9k vs 13.6k)
-                launch_aa_odd_w<4, 3>(wk, s, b, e);
+                launch_aa_odd_w<4, 3>(wk, s, b, e, v == 80);
             } else lbm_aa_odd<false, false, 128, 4><<<nb, 128, 0, s>>>(F, tab, wk.P, b, e, omega, ia, h);
         }
         if (timed) {

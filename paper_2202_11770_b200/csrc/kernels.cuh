@@ -1549,7 +1549,7 @@ template <int kWarps, int kMinBlocks>
 __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
 lbm_aa_odd_w(double* __restrict__ F, const int16_t* __restrict__ dtab, const uint32_t* __restrict__ gbase,
              const uint32_t* __restrict__ tab, uint64_t P, uint64_t PG, uint32_t begin, uint32_t end, double omega,
-             const __grid_constant__ Planes19 planes) {
+             const __grid_constant__ Planes19 planes, unsigned* __restrict__ counter = nullptr) {
     using L = AaOddW<kWarps, kMinBlocks>;
     extern __shared__ __align__(128) unsigned char smem[];
     const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -1559,13 +1559,31 @@ lbm_aa_odd_w(double* __restrict__ F, const int16_t* __restrict__ dtab, const uin
     const uint32_t ntiles = (end - base + 31) / 32;
     const uint32_t nw = gridDim.x * kWarps;
     const uint32_t w0 = blockIdx.x * kWarps + wib;
+    // warp-tile sequence: the fixed stride w0 + k * nw, or (counter) batches
+    // of 4 consecutive tiles taken from a global counter (dynamic order: the
+    // tiles in flight stay near the frontier however the warps drift apart)
+    constexpr uint32_t kBatch = 4;
+    uint32_t bb0 = 0, bb1 = 0, bi0 = 0xffffffffu, bi1 = 0xffffffffu;
+    auto tile_at = [&](uint32_t k) -> uint32_t {
+        if (!counter) return w0 + k * nw;
+        const uint32_t bi = k / kBatch;
+        const bool odd = bi & 1u;
+        if ((odd ? bi1 : bi0) != bi) {
+            uint32_t v = 0;
+            if (lane == 0) v = atomicAdd(counter, kBatch);
+            v = __shfl_sync(0xffffffffu, v, 0);
+            if (odd) bb1 = v, bi1 = bi;
+            else bb0 = v, bi0 = bi;
+        }
+        return (odd ? bb1 : bb0) + k % kBatch;
+    };
     // compressed table of warp-tile k into registers: the 18 int16 deltas
     // packed two per register, and this lane's group base
     constexpr int kD2 = (kQ - 1) / 2;
     uint32_t dA[kD2], dB[kD2];
     uint32_t bA = 0, bB = 0;
     auto load_table = [&](uint32_t k, uint32_t* d, uint32_t& b) {
-        const uint32_t tile = w0 + k * nw;
+        const uint32_t tile = tile_at(k);
         const uint32_t s = base + tile * 32 + lane;
         const bool live = tile < ntiles && s >= begin && s < end;
 #pragma unroll
@@ -1592,7 +1610,7 @@ lbm_aa_odd_w(double* __restrict__ F, const int16_t* __restrict__ dtab, const uin
     int32_t oA[kQ - 1], oB[kQ - 1];  // locations of the tile being stored / being gathered
     // issue the gathers of tile k (table d, b) into stage k & 1; offsets into o
     auto issue = [&](uint32_t k, const uint32_t* d, uint32_t b, int32_t* o) {
-        const uint32_t tile = w0 + k * nw;
+        const uint32_t tile = tile_at(k);
         const uint32_t s = base + tile * 32 + lane;
         const bool live = tile < ntiles && s >= begin && s < end;
         double* st = stage[k & 1];
@@ -1609,7 +1627,7 @@ lbm_aa_odd_w(double* __restrict__ F, const int16_t* __restrict__ dtab, const uin
     // two iterations per loop trip swap the register sets without moves
     auto step = [&](uint32_t k, const uint32_t* dN, uint32_t bN, int32_t* oN, uint32_t* dNN, uint32_t& bNN,
                     const int32_t* oK) -> bool {
-        const uint32_t tile = w0 + k * nw;
+        const uint32_t tile = tile_at(k);
         if (tile >= ntiles) return false;
         issue(k + 1, dN, bN, oN);
         cp_async_commit();
@@ -1632,7 +1650,7 @@ lbm_aa_odd_w(double* __restrict__ F, const int16_t* __restrict__ dtab, const uin
         return true;
     };
     load_table(0, dA, bA);
-    if (w0 >= ntiles) return;  // whole warp
+    if (tile_at(0) >= ntiles) return;  // whole warp
     issue(0, dA, bA, oA);
     cp_async_commit();
     load_table(1, dB, bB);
