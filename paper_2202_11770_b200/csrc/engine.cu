@@ -1549,7 +1549,7 @@ class Engine {
         return true;
 #else
         return v == 0 || v == 24 || v == 43 || v == 59 || v == 60 || v == 64 || v == 71 || v == 72 || v == 76 ||
-               v == 77 || v == 78 || v == 79 || v == 80;
+               v == 77 || v == 78 || v == 79 || v == 80 || v == 81;
 #endif
     }
     void launch_plain(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia, bool mid) {
@@ -1585,7 +1585,7 @@ class Engine {
         if (plain_variant == 0 || plain_variant == 24 || plain_variant == 43 || plain_variant == 59 ||
             plain_variant == 60 || plain_variant == 64 || plain_variant == 71 || plain_variant == 72 ||
             plain_variant == 76 || plain_variant == 77 || plain_variant == 78 || plain_variant == 79 ||
-            plain_variant == 80)
+            plain_variant == 80 || plain_variant == 81)
             return false;
         if (plain_variant == 69 || plain_variant == 70) {  // tile-major table, one bulk copy per tile
             if (!(mid && wk.ctab_ok)) launch_tma<256, 2, 2, false, 6>(wk, s, b, e);
@@ -2306,7 +2306,8 @@ class Engine {
             } else if (timed && wk.ctab_ok && v != 60) {
                 // default: warp-autonomous pipeline, cp.async gathers one tile
                 // ahead (C3 developed, odd step: 14.2k MSUPS; C2 14.9k vs 13.6k)
-                launch_aa_odd_w<4, 3>(wk, s, b, e, v == 80);
+                // with the dynamic warp-tile order (C3 odd step 14.2k vs 13.9k; 81: fixed order)
+                launch_aa_odd_w<4, 3>(wk, s, b, e, v != 81);
             } else lbm_aa_odd<false, false, 128, 4><<<nb, 128, 0, s>>>(F, tab, wk.P, b, e, omega, ia, h);
         }
         if (timed) {
