@@ -1432,7 +1432,7 @@ class Engine {
     int bulk_kernel_of(const WorkerDev& wk) const {
         if (!wk.ctab_ok) return -1;
         if (plain_variant == 43) return 3;
-        if (plain_variant == 76) return 0;
+        if (plain_variant == 76 || (plain_variant >= 82 && plain_variant <= 84)) return 0;
         if (plain_variant == 59) return 1;
         if (plain_variant == 71 || plain_variant == 77) return wk.rtab_ok ? 2 : -1;
         return plain_variant == 0 ? wk.mid_pick : -1;
@@ -1572,6 +1572,11 @@ class Engine {
             const bool pf = plain_variant == 59 || (plain_variant == 0 && wk.mid_pick == 1);
             if (pf) launch_tmc<256, 2, 2, 4102>(wk, s, b, e);
             else if (plain_variant == 43) launch_tmc<256, 2, 2, 6>(wk, s, b, e);
+#ifdef SPLBCU_TUNING
+            else if (plain_variant == 82) launch_dyn<128, 2, 4>(wk, s, b, e);
+            else if (plain_variant == 83) launch_dyn<128, 3, 3>(wk, s, b, e);
+            else if (plain_variant == 84) launch_dyn<256, 3, 1>(wk, s, b, e);
+#endif
             else launch_dyn<256, 2, 2>(wk, s, b, e);
         } else {
             launch_tma<256, 2, 2, false, 6>(wk, s, b, e);
@@ -1585,7 +1590,7 @@ class Engine {
         if (plain_variant == 0 || plain_variant == 24 || plain_variant == 43 || plain_variant == 59 ||
             plain_variant == 60 || plain_variant == 64 || plain_variant == 71 || plain_variant == 72 ||
             plain_variant == 76 || plain_variant == 77 || plain_variant == 78 || plain_variant == 79 ||
-            plain_variant == 80 || plain_variant == 81)
+            plain_variant == 80 || plain_variant == 81 || (plain_variant >= 82 && plain_variant <= 84))
             return false;
         if (plain_variant == 69 || plain_variant == 70) {  // tile-major table, one bulk copy per tile
             if (!(mid && wk.ctab_ok)) launch_tma<256, 2, 2, false, 6>(wk, s, b, e);
