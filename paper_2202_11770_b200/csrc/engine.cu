@@ -1353,7 +1353,7 @@ class Engine {
         const int resident = resident_ctas(lbm_push_tmc<T, S, B, H>, wk.dev, T, kBytes);
         const uint32_t base = b & ((H & 16384) ? ~uint32_t(T - 1) : ((H & 136) == 136 ? ~127u : ~31u));
         const uint32_t ntiles = (e - base + T - 1) / T;
-        const unsigned grid = unsigned(std::min<uint32_t>(ntiles, uint32_t(bulk_grid(resident))));
+        const unsigned grid = unsigned(std::min<uint32_t>(ntiles, uint32_t(resident)));
         check_tiles(wk, base, ntiles, T);
         Planes19 pl;
         for (int i = 0; i < kQ; ++i) pl.p[i] = wk.f_new() + uint64_t(i) * wk.P;
@@ -1380,15 +1380,6 @@ class Engine {
     }
 #endif
 
-    // Persistent grid of the bulk kernels.  With the iolet series on, two CTAs
-    // (one SM's worth) are left free so the previous run's observation
-    // all-gather and series kernels run beside the next bulk kernel instead
-    // of waiting for it (SPLBCU_SERIES_FIRST: the bulk kernel waits for them).
-    const bool series_first = std::getenv("SPLBCU_SERIES_FIRST") != nullptr;
-    int bulk_grid(int resident) const {
-        return (prm.observe_iolets && !series_first) ? std::max(1, resident - 2) : resident;
-    }
-
     // A zeroed tile counter for one dynamic-order launch on stream s (a ring of
     // slots, each zeroed stream-ordered right before its launch).
     unsigned* tile_counter(WorkerDev& wk, cudaStream_t s) {
@@ -1408,7 +1399,7 @@ class Engine {
         const int resident = resident_ctas(lbm_push_dyn<T, S, B>, wk.dev, T, kBytes);
         const uint32_t base = b & ~31u;
         const uint32_t ntiles = (e - base + T - 1) / T;
-        const unsigned grid = unsigned(std::min<uint32_t>(ntiles, uint32_t(bulk_grid(resident))));
+        const unsigned grid = unsigned(std::min<uint32_t>(ntiles, uint32_t(resident)));
         check_tiles(wk, base, ntiles, T);
         unsigned* ctr = tile_counter(wk, s);
         Planes19 pl;
@@ -1425,7 +1416,7 @@ class Engine {
         const int resident = resident_ctas(lbm_push_run<T, S, B>, wk.dev, T, kBytes);
         const uint32_t base = b & ~uint32_t(T - 1);
         const uint32_t ntiles = (e - base + T - 1) / T;
-        const unsigned grid = unsigned(std::min<uint32_t>(ntiles, uint32_t(bulk_grid(resident))));
+        const unsigned grid = unsigned(std::min<uint32_t>(ntiles, uint32_t(resident)));
         check_tiles(wk, base, ntiles, T);
         Planes19 pl;
         for (int i = 0; i < kQ; ++i) pl.p[i] = wk.f_new() + uint64_t(i) * wk.P;
@@ -1950,6 +1941,7 @@ class Engine {
     PendingRun pend;
     uint64_t max_run_n = 0;  // the longest run so far (buffer sizes follow it)
     const bool sync_runs = std::getenv("SPLBCU_SYNC_RUN") != nullptr;  // A/B knob: every run completes before returning
+    const bool wait_series_off = std::getenv("SPLBCU_NO_SERIES_FIRST") != nullptr;  // A/B knob for the ordering below
     int run_par = 0;                                     // event / staging set of the run being enqueued
     PinnedMem h_staged2[2];                              // per-run iolet values, one per run in flight
     std::chrono::steady_clock::time_point last_done{};  // host clock at the last completion
@@ -1998,12 +1990,11 @@ class Engine {
         for (auto& wp : W) {
             if (!wp) continue;
             CK(cudaSetDevice(wp->dev));
-            // dist mode with observation, SPLBCU_SERIES_FIRST: the previous
-            // run's all-gather and series kernels (on sE) go first — without a
-            // free SM (bulk_grid) this run's persistent bulk kernel could take
-            // every SM before the NCCL kernel, which would then land after it
-            // and delay this run's edge kernels queued behind it.
-            if (pend.active && dist && prm.observe_iolets && series_first)
+            // dist mode with observation: the previous run's all-gather and
+            // series kernels (on sE) go first.  Otherwise this run's persistent
+            // bulk kernel can take every SM before the NCCL kernel, which then
+            // lands after it and delays this run's edge kernels behind it.
+            if (pend.active && dist && prm.observe_iolets && !wait_series_off)
                 CK(cudaStreamWaitEvent(wp->sM, wp->evDone[pend.par], 0));
             double* d = wp->staged.reserve<double>(n_staged);
             CK(cudaMemcpyAsync(d, staged, n_staged * sizeof(double), cudaMemcpyHostToDevice, wp->sM));
@@ -2053,11 +2044,8 @@ class Engine {
                 continue;
             }
             if (series) {
-                // on the edge stream, so the next run's bulk kernel (sM) runs
-                // beside it on the SM the bulk grid leaves free (bulk_grid)
-                CK(cudaStreamWaitEvent(wk.sE, wk.evRun1[par], 0));
-                reduce_series_async(wk, wk.sE, wk.obs_buf.get<double>(), 0, ser_next);
-                CK(cudaEventRecord(wk.evDone[par], wk.sE));
+                reduce_series_async(wk, wk.sM, wk.obs_buf.get<double>(), 0, ser_next);
+                CK(cudaEventRecord(wk.evDone[par], wk.sM));
                 continue;
             }
             const size_t nb = prm.observe_iolets ? 3 * wk.obs_rows * wk.n_obs : 0;
