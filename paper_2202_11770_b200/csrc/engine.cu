@@ -1590,7 +1590,8 @@ class Engine {
         if (plain_variant == 0 || plain_variant == 24 || plain_variant == 43 || plain_variant == 59 ||
             plain_variant == 60 || plain_variant == 64 || plain_variant == 71 || plain_variant == 72 ||
             plain_variant == 76 || plain_variant == 77 || plain_variant == 78 || plain_variant == 79 ||
-            plain_variant == 80 || plain_variant == 81 || (plain_variant >= 82 && plain_variant <= 84))
+            plain_variant == 80 || plain_variant == 81 || (plain_variant >= 82 && plain_variant <= 84) ||
+            (plain_variant >= 88 && plain_variant <= 91))
             return false;
         if (plain_variant == 69 || plain_variant == 70) {  // tile-major table, one bulk copy per tile
             if (!(mid && wk.ctab_ok)) launch_tma<256, 2, 2, false, 6>(wk, s, b, e);
@@ -2266,6 +2267,22 @@ class Engine {
                                                            wk.tab.get<uint32_t>(), wk.P, wk.PG, b, e, omega, pl, ctr);
     }
 
+#ifdef SPLBCU_TUNING
+    // The same with the table staged in shared memory (decoded twice, not held).
+    template <int NW, int B>
+    void launch_aa_odd_s(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, bool dyn = true) {
+        using Lm = AaOddS<NW, B>;
+        const int resident = resident_ctas(lbm_aa_odd_s<NW, B>, wk.dev, NW * 32, Lm::kBytes);
+        const uint32_t ntiles = (e - (b & ~31u) + 31) / 32;
+        const unsigned grid = unsigned(std::min<uint32_t>((ntiles + NW - 1) / NW, uint32_t(resident)));
+        Planes19 pl;
+        for (int i = 0; i < kQ; ++i) pl.p[i] = wk.f_old() + uint64_t(i) * wk.P;
+        unsigned* ctr = dyn ? tile_counter(wk, s) : nullptr;
+        lbm_aa_odd_s<NW, B><<<grid, NW * 32, Lm::kBytes, s>>>(wk.f_old(), wk.dtab.get<int16_t>(), wk.gbase.get<uint32_t>(),
+                                                           wk.tab.get<uint32_t>(), wk.P, wk.PG, b, e, omega, pl, ctr);
+    }
+#endif
+
     void launch_aa_range(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, bool iolet, const double* staged,
                          const int32_t* coords, bool timed, bool edge, bool odd) {
         if (e <= b) return;
@@ -2302,7 +2319,18 @@ class Engine {
 #endif
             else if (timed && wk.ctab_ok && v == 72) {
                 launch_aa_odd_w<4, 4>(wk, s, b, e);  // 128 registers: spills (C3 odd 9.6k)
-            } else if (timed && wk.ctab_ok && v == 64) {
+            }
+#ifdef SPLBCU_TUNING
+            // table staged in shared memory (C3 developed odd step: 14.3k at 12
+            // warps/SM, 11.2k at 15 — shared-memory pipe stalls — vs 14.65k)
+            else if (timed && wk.ctab_ok && v >= 88 && v <= 91) {
+                if (v == 88) launch_aa_odd_s<5, 3>(wk, s, b, e);
+                else if (v == 89) launch_aa_odd_s<4, 3>(wk, s, b, e);
+                else if (v == 90) launch_aa_odd_s<7, 2>(wk, s, b, e);
+                else launch_aa_odd_s<4, 3>(wk, s, b, e, false);
+            }
+#endif
+            else if (timed && wk.ctab_ok && v == 64) {
                 // round-1 default: one thread per site, register gather over the
                 // compressed table (C3 developed, odd step: 13.7k MSUPS)
                 const uint32_t b0 = b & ~31u;

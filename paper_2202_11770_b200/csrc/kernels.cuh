@@ -1661,6 +1661,129 @@ lbm_aa_odd_w(double* __restrict__ F, const int16_t* __restrict__ dtab, const uin
     cp_async_wait<0>();
 }
 
+#ifdef SPLBCU_TUNING
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
+// Odd step, the same warp-autonomous pipeline with the compressed table
+// staged in shared memory instead of registers: the table of tile k+3 is
+// copied (cp.async, 72 x 16 B of deltas + 18 group bases) with the gathers of
+// tile k+1, and the 18 locations are decoded from it twice — when tile k+1's
+// gathers are issued and when tile k stores — instead of being held.  That
+// frees the ~56 registers the register version spends on two table sets and
+// two offset sets, for more resident warps (more gathers in flight per SM).
+// Measured slower (the decode's shared-memory reads stall the MIO pipe,
+// profiles/r02_c3_dev_aa_s.md): tuning build only.
+template <int kWarps, int kMinBlocks>
+struct AaOddS {
+    static constexpr uint32_t kF = uint32_t(kQ) * 32 * 8;               // one warp's gathered f
+    static constexpr uint32_t kTD = uint32_t(kQ - 1) * 32 * 2;          // deltas of one tile
+    static constexpr uint32_t kT = kTD + 128;                          // + its 18 group bases
+    static constexpr uint32_t kWarpBytes = 2 * kF + 4 * kT;
+    static constexpr uint32_t kBytes = kWarps * kWarpBytes;
+};
+
+template <int kWarps, int kMinBlocks>
+__global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
+lbm_aa_odd_s(double* __restrict__ F, const int16_t* __restrict__ dtab, const uint32_t* __restrict__ gbase,
+             const uint32_t* __restrict__ tab, uint64_t P, uint64_t PG, uint32_t begin, uint32_t end, double omega,
+             const __grid_constant__ Planes19 planes, unsigned* __restrict__ counter = nullptr) {
+    using L = AaOddS<kWarps, kMinBlocks>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    unsigned char* const wsm = smem + wib * L::kWarpBytes;
+    const uint32_t base = begin & ~31u;  // P is a multiple of 64: whole tiles lie inside the planes
+    const uint32_t ntiles = (end - base + 31) / 32;
+    const uint32_t nw = gridDim.x * kWarps;
+    const uint32_t w0 = blockIdx.x * kWarps + wib;
+    constexpr uint32_t kBatch = 4;  // as lbm_aa_odd_w; the look-ahead (3 tiles) spans <= 2 batches
+    uint32_t bb0 = 0, bb1 = 0, bi0 = 0xffffffffu, bi1 = 0xffffffffu;
+    auto tile_at = [&](uint32_t k) -> uint32_t {
+        if (!counter) return w0 + k * nw;
+        const uint32_t bi = k / kBatch;
+        const bool odd = bi & 1u;
+        if ((odd ? bi1 : bi0) != bi) {
+            uint32_t v = 0;
+            if (lane == 0) v = atomicAdd(counter, kBatch);
+            v = __shfl_sync(0xffffffffu, v, 0);
+            if (odd) bb1 = v, bi1 = bi;
+            else bb0 = v, bi0 = bi;
+        }
+        return (odd ? bb1 : bb0) + k % kBatch;
+    };
+    auto fst = [&](uint32_t k) { return reinterpret_cast<double*>(wsm + (k & 1) * L::kF); };
+    auto tst = [&](uint32_t k) { return wsm + 2 * L::kF + (k & 3) * L::kT; };
+    auto load_table = [&](uint32_t k) {
+        const uint32_t tile = tile_at(k);
+        if (tile >= ntiles) return;
+        const uint32_t tb = base + tile * 32;
+        unsigned char* t = tst(k);
+#pragma unroll
+        for (uint32_t c = lane; c < 4 * (kQ - 1); c += 32)  // row c / 4, 16-byte quarter c % 4
+            cp_async16(t + c * 16, dtab + uint64_t(c >> 2) * P + tb + (c & 3) * 8);
+        if (lane < kQ - 1) cp_async4(t + L::kTD + lane * 4, gbase + uint64_t(lane) * PG + (tb >> 5));
+    };
+    // location of direction j of site s (tile k's table): signed offset from
+    // plane j's base (a bounce-back lives in the inverse plane at s: s +- P)
+    auto loc = [&](uint32_t k, int j, uint32_t s, bool live) -> int32_t {
+        const unsigned char* t = tst(k);
+        const int dj = reinterpret_cast<const int16_t*>(t)[(j - 1) * 32 + lane];
+        const uint32_t bj = reinterpret_cast<const uint32_t*>(t + L::kTD)[j - 1];
+        uint32_t tg = bj + lane + uint32_t(dj);
+        const uint32_t esc = (dj == kDeltaEscape) && live;
+        asm("{\n .reg .pred p;\n setp.ne.u32 p, %1, 0;\n @p ld.global.nc.u32 %0, [%2];\n}"
+            : "+r"(tg)
+            : "r"(esc), "l"(tab + uint64_t(j - 1) * P + s));
+        const int32_t off = (j & 1) ? int32_t(P) : -int32_t(P);
+        return dj == kDeltaBounce ? int32_t(s) + off : int32_t(tg);
+    };
+    auto issue = [&](uint32_t k) {
+        const uint32_t tile = tile_at(k);
+        const uint32_t s = base + tile * 32 + lane;
+        const bool live = tile < ntiles && s >= begin && s < end;
+        if (!live) return;
+        double* st = fst(k);
+        cp_async8(st + lane, F + s);
+#pragma unroll
+        for (int i = 1; i < kQ; ++i) cp_async8(st + inv(i) * 32 + lane, planes.p[i] + loc(k, i, s, true));
+    };
+    load_table(0);
+    load_table(1);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncwarp();
+    if (tile_at(0) >= ntiles) return;  // whole warp
+    issue(0);
+    load_table(2);
+    cp_async_commit();
+    for (uint32_t k = 0;; ++k) {
+        const uint32_t tile = tile_at(k);
+        if (tile >= ntiles) break;
+        issue(k + 1);       // table k+1 landed with tile k-1's gathers
+        load_table(k + 3);  // its stage held table k-1, done
+        cp_async_commit();
+        cp_async_wait<1>();  // tile k's gathers and table k+2 have landed
+        __syncwarp();        // ... for every lane (table rows are copied by other lanes)
+        const uint32_t s = base + tile * 32 + lane;
+        const double* st = fst(k);
+        double f[kQ];
+#pragma unroll
+        for (int i = 0; i < kQ; ++i) f[i] = st[i * 32 + lane];
+        const Macro m = macro_of(f);
+        double feq[kQ];
+        feq_all(m.rho, m.ux, m.uy, m.uz, feq);
+        if (s >= begin && s < end) {
+            F[s] = relax(f[0], feq[0], omega);
+#pragma unroll
+            for (int i = 1; i < kQ; ++i) planes.p[i][loc(k, i, s, true)] = relax(f[i], feq[i], omega);
+        }
+        __syncwarp();  // f stage k & 1 and table stage k & 3 are refilled next
+    }
+    cp_async_wait<0>();
+}
+#endif  // SPLBCU_TUNING
+
 // Gather the 19 populations of site s in the current AA state (state N:
 // plain reads; state S: the rule above).
 template <bool kP2P>
