@@ -9,6 +9,9 @@ tree (BASELINE configs[2], the config the metric "MSUPS at 1/2/4/8 B200" is
 quoted on), pressure iolets, strong scaling (the same total work at every N,
 so the driver's per-N values give the strong-scaling efficiency directly).
 N>1: torchrun, one process per GPU, slab decomposition, fused NVLink P2P halo.
+Storage: the AA single buffer by default (same bits as the reference's
+two-buffer push, half the HBM, faster: DESIGN §6b); `--storage two` runs the
+two-buffer push kernels.
 At N=1 the line also carries `secondary`: config C2 — build_pipe(48, 1400)
 (10,130,400 sites), 60-bpm pulsatile velocity inlet (proj/configs/
 pipe_beat.cfg), outlet p=1/3, tau 0.8, dt 5e-4 s — kernel-only value and
@@ -19,10 +22,11 @@ value  : sites*steps / device time of the step loop (CUDA events on the
 e2e    : the same metric through the public C-ABI call sequence a user makes
          (Simulation.run(1) per step with the iolet series on: per-step BC
          staging H2D and the observation row D2H), host wall clock.
-roofline: the bulk plain-site fused kernel (lbm_push_tmc), its own
-         algorithmic bytes (342.25 B/site: 19*8 read + 19*8 write + 18*(2+4/32)
-         compressed index) per launch / CUDA-event launch time; frac_376
-         restates it in SURVEY §8d's 376 B/site.
+roofline: the bulk plain-site fused kernels (AA: lbm_aa_even_tma /
+         lbm_aa_odd_w, 304 / 342.25 B/site -> 323.125 per step; two buffers:
+         lbm_push_dyn, 342.25 B/site: 19*8 read + 19*8 write + 18*(2+4/32)
+         compressed index), algorithmic bytes per launch / CUDA-event launch
+         time; frac_376 restates it in SURVEY §8d's 376 B/site.
 cpu_baseline: the unmodified reference (oracle/_ref) on this host's cores,
          bounded sample of the same workload (rank 0, N=1 only).
 """
@@ -115,25 +119,33 @@ class ClockSampler:
 
     def __init__(self, gpu):
         self.gpu, self.rows, self.proc = gpu, [], None
+        self.t0 = self.t1 = None
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "25"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # the sampler is running before the timed region starts (nvidia-smi
+            # takes a moment to start): a short region still gets its samples
+            deadline = time.perf_counter() + 5.0
+            while not self.rows and time.perf_counter() < deadline and self.proc.poll() is None:
+                time.sleep(0.005)
         except Exception:
             self.proc = None
+        self.t0 = time.perf_counter()
         return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            self.rows.append((time.perf_counter(), [x.strip() for x in line.split(",")]))
 
     def __exit__(self, *a):
+        self.t1 = time.perf_counter()
         if self.proc:
-            time.sleep(0.25)
+            time.sleep(0.06)  # the sample in flight at the end of the region
             self.proc.terminate()
             try:
                 self.proc.wait(2)
@@ -141,10 +153,14 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        sm = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if len(r) >= 7 and r[2].replace(".", "").isdigit()]
+        """Samples taken inside the timed region (read within one sampling
+        period after its end: nvidia-smi reports the state at the query)."""
+        rows = [r for t, r in self.rows if self.t0 is not None and self.t0 <= t <= (self.t1 or t) + 0.05]
+        self.rows_in = rows
+        sm = [float(r[1]) for r in rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) >= 7 and r[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for r in self.rows if len(r) >= 7 for k in range(4) if r[3 + k] == "Active"})
+        reasons = sorted({names[k] for r in rows if len(r) >= 7 for k in range(4) if r[3 + k] == "Active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": reasons, "samples": len(sm)}
 
@@ -200,6 +216,10 @@ def cpu_reference_run(name, steps_cap, seconds, scale, warmup=1, sample="baselin
 BULK_KERNELS = {0: "void lbm_push_dyn<256, 2, 2>", 1: "void lbm_push_tmc<256, 2, 2, 4102>",
                 2: "void lbm_push_run<256, 2, 2>", 3: "void lbm_push_tmc<256, 2, 2, 6>"}
 RUN_BYTES_PER_SITE = 19 * 8 + 19 * 8 + 3456 / 256  # 317.5: run-length table kernel
+# AA single buffer: even steps 304 B/site (no table), odd steps
+# the compressed-table gather/scatter 342.25 -> 323.125 per step on average
+AA_BYTES_PER_SITE = (19 * 8 * 2 + DESIGN_BYTES_PER_SITE) / 2
+AA_KERNELS = "AA pair: void lbm_aa_even_tma<256, 2, 2> + void lbm_aa_odd_w<4, 3, 1>"
 
 
 def load_profile_traffic(name, kernel=None, developed=False):
@@ -220,7 +240,7 @@ def load_profile_traffic(name, kernel=None, developed=False):
     return None, None
 
 
-def timed_loop(sim, n, steps, warmup, bps, barrier, max_over_ranks, gpu, name, developed=False):
+def timed_loop(sim, n, steps, warmup, bps, barrier, max_over_ranks, gpu, name, developed=False, aa=False):
     """W untimed steps, then K steps timed by CUDA events on the launching
     streams (max over ranks), with per-launch events on the bulk plain kernel
     and nvidia-smi clocks sampled during the timed region."""
@@ -241,13 +261,13 @@ def timed_loop(sim, n, steps, warmup, bps, barrier, max_over_ranks, gpu, name, d
     value = n * steps / dev_s / 1e6
     ks, kl, kn = k1[0] - k0[0], k1[1] - k0[1], k1[2] - k0[2]
     hbm, src = peaks()
-    kernel = BULK_KERNELS.get(sim.bulk_kernel())
-    if sim.bulk_kernel() == 2 and bps == DESIGN_BYTES_PER_SITE:
+    kernel = AA_KERNELS if aa else BULK_KERNELS.get(sim.bulk_kernel())
+    if not aa and sim.bulk_kernel() == 2 and bps == DESIGN_BYTES_PER_SITE:
         bps = RUN_BYTES_PER_SITE  # the online choice launched the run-length table kernel
-    traffic, traffic_key = load_profile_traffic(name, kernel, developed)
+    traffic, traffic_key = load_profile_traffic(name + "_dev_aa" if aa else name, kernel, developed)
     # The default kernel reads a compressed table (int16 deltas + a u32 base per
     # 32 sites): its algorithmic bytes are 304 + 18*(2 + 4/32) = 342.25 B/site
-    # (AA storage: even steps 304, odd steps 376 -> 340 on average).
+    # (AA storage: even steps 304, odd steps 342.25 -> 323.125 on average).
     # `achieved`/`frac` use those bytes (the DRAM rate the kernel really
     # sustains); `achieved_376`/`frac_376` restate it in SURVEY §8d's
     # 376 B/site (the reference data layout), which can exceed 1.0 because the
@@ -257,7 +277,10 @@ def timed_loop(sim, n, steps, warmup, bps, barrier, max_over_ranks, gpu, name, d
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
             "frac": achieved / hbm if achieved else None,
             "traffic": (traffic * kn / kl) if (traffic and kl) else None,
-            "peak_source": src, "kernel": "lbm_push_dyn / lbm_push_tmc / lbm_push_run (Inner+Wall fused collide+stream, TMA-pipelined)",
+            "peak_source": src,
+            "kernel": ("lbm_aa_even_tma / lbm_aa_odd_w (AA single buffer: even steps in place, odd steps "
+                       "gather/scatter)") if aa else
+                      "lbm_push_dyn / lbm_push_tmc / lbm_push_run (Inner+Wall fused collide+stream, TMA-pipelined)",
             "kernel_template": kernel, "traffic_source": traffic_key,
             "bytes_per_site": bps, "achieved_376": achieved_376,
             "frac_376": achieved_376 / hbm if achieved_376 else None,
@@ -310,8 +333,10 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-secondary", action="store_true", help="N=1: skip the C2 kernel-only line")
     ap.add_argument("--quick", action="store_true", help="kernel-only number (tuning runs)")
-    ap.add_argument("--storage", default="two", choices=["two", "aa"],
-                    help="two buffers (push) or one buffer in place (AA pattern)")
+    ap.add_argument("--storage", default="aa", choices=["two", "aa"],
+                    help="one buffer updated in place (AA pattern; the default: the same bits in half the "
+                         "memory, and faster on C3 at N = 1 / 2 / 4, DESIGN §6b) or two buffers (the "
+                         "reference's f_old / f_new push)")
     ap.add_argument("--scheme", default="push", choices=["push", "pull"],
                     help="push (fused collide + scatter) or the reference's pull gather (update_pull)")
     ap.add_argument("--halo", default="p2p", choices=["nccl", "p2p"],
@@ -383,7 +408,7 @@ def main():
         td.all_reduce(t, op=td.ReduceOp.MAX)
         return float(t.item())
 
-    bps = 340.0 if args.storage == "aa" else DESIGN_BYTES_PER_SITE
+    bps = AA_BYTES_PER_SITE if args.storage == "aa" else DESIGN_BYTES_PER_SITE
 
     def develop(sim, steps, chunk=None):
         """Untimed steps that take the flow from rest to a developed state
@@ -407,7 +432,7 @@ def main():
     state = f"developed flow: {args.develop + (args.warmup + args.steps if rest else 0)} untimed steps first" \
         if args.develop > 0 else "from rest"
     value, dev_s, launches, roof, clk = timed_loop(sim, n, args.steps, args.warmup, bps, barrier, max_over_ranks, local,
-                                                  name, developed=args.develop > 0)
+                                                  name, developed=args.develop > 0, aa=storage == 1)
 
     if args.quick:
         if rank == 0:
@@ -473,7 +498,8 @@ def main():
                            "scheme": args.scheme, "storage": "AA single buffer" if storage else "two buffers",
                            "halo": (("NCCL send/recv + PostReceive" if halo_mode == 0 else "fused NVLink P2P stores")
                                     if world > 1 else "none"),
-                           "l2": f"inputs (f, table) {n * 376 / 1e9:.1f} GB per step >> 126 MB L2; no flush needed",
+                           "l2": f"bytes moved per step (f read + written, table) {n * bps / 1e9:.1f} GB >> 126 MB L2; "
+                                 "no flush needed",
                            "setup_s": round(setup_s, 2), "state": state,
                            "geometry": ("slab-local (each rank classifies its own slices)" if sim_slab
                                         else "whole domain on every rank")},

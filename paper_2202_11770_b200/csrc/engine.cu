@@ -1549,7 +1549,7 @@ class Engine {
         return true;
 #else
         return v == 0 || v == 24 || v == 43 || v == 59 || v == 60 || v == 64 || v == 71 || v == 72 || v == 76 ||
-               v == 77 || v == 78 || v == 79 || v == 80 || v == 81;
+               v == 77 || v == 78 || v == 79 || v == 80 || v == 81 || v == 94;
 #endif
     }
     void launch_plain(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, const IoletArgs& ia, bool mid) {
@@ -1591,7 +1591,7 @@ class Engine {
             plain_variant == 60 || plain_variant == 64 || plain_variant == 71 || plain_variant == 72 ||
             plain_variant == 76 || plain_variant == 77 || plain_variant == 78 || plain_variant == 79 ||
             plain_variant == 80 || plain_variant == 81 || (plain_variant >= 82 && plain_variant <= 84) ||
-            (plain_variant >= 88 && plain_variant <= 91))
+            (plain_variant >= 88 && plain_variant <= 96))
             return false;
         if (plain_variant == 69 || plain_variant == 70) {  // tile-major table, one bulk copy per tile
             if (!(mid && wk.ctab_ok)) launch_tma<256, 2, 2, false, 6>(wk, s, b, e);
@@ -2254,16 +2254,16 @@ class Engine {
 #endif
 
     // Warp-autonomous AA odd kernel (persistent; cp.async gathers one tile ahead).
-    template <int NW, int B>
+    template <int NW, int B, int O = 1>
     void launch_aa_odd_w(WorkerDev& wk, cudaStream_t s, uint32_t b, uint32_t e, bool dyn = false) {
         using Lm = AaOddW<NW, B>;
-        const int resident = resident_ctas(lbm_aa_odd_w<NW, B>, wk.dev, NW * 32, Lm::kBytes);
+        const int resident = resident_ctas(lbm_aa_odd_w<NW, B, O>, wk.dev, NW * 32, Lm::kBytes);
         const uint32_t ntiles = (e - (b & ~31u) + 31) / 32;
         const unsigned grid = unsigned(std::min<uint32_t>((ntiles + NW - 1) / NW, uint32_t(resident)));
         Planes19 pl;
         for (int i = 0; i < kQ; ++i) pl.p[i] = wk.f_old() + uint64_t(i) * wk.P;
         unsigned* ctr = dyn ? tile_counter(wk, s) : nullptr;
-        lbm_aa_odd_w<NW, B><<<grid, NW * 32, Lm::kBytes, s>>>(wk.f_old(), wk.dtab.get<int16_t>(), wk.gbase.get<uint32_t>(),
+        lbm_aa_odd_w<NW, B, O><<<grid, NW * 32, Lm::kBytes, s>>>(wk.f_old(), wk.dtab.get<int16_t>(), wk.gbase.get<uint32_t>(),
                                                            wk.tab.get<uint32_t>(), wk.P, wk.PG, b, e, omega, pl, ctr);
     }
 
@@ -2330,7 +2330,22 @@ class Engine {
                 else launch_aa_odd_s<4, 3>(wk, s, b, e, false);
             }
 #endif
-            else if (timed && wk.ctab_ok && v == 64) {
+#ifdef SPLBCU_TUNING
+            // knobs of the default odd kernel (C3 odd step, profiles/r02/aa_split_rawtab*.jsonl):
+            // 92 + the next batch's atomic requested ahead (15.9k vs 16.0k), 93 that alone
+            // with the packed table (14.2k), 95/96 batches of 8 (15.0k / 14.5-14.9k vs 15.2k)
+            else if (timed && wk.ctab_ok && (v == 92 || v == 93 || v == 95 || v == 96)) {
+                if (v == 92) launch_aa_odd_w<4, 3, 3>(wk, s, b, e, true);
+                else if (v == 93) launch_aa_odd_w<4, 3, 2>(wk, s, b, e, true);
+                else if (v == 95) launch_aa_odd_w<4, 3, 5>(wk, s, b, e, true);
+                else launch_aa_odd_w<4, 3, 7>(wk, s, b, e, true);
+            }
+#endif
+            else if (timed && wk.ctab_ok && v == 94) {
+                // the previous default: deltas packed two per register — the packing
+                // waits for the table loads, a memory latency per tile (C3 odd 14.1k vs 15.4k)
+                launch_aa_odd_w<4, 3, 0>(wk, s, b, e, true);
+            } else if (timed && wk.ctab_ok && v == 64) {
                 // round-1 default: one thread per site, register gather over the
                 // compressed table (C3 developed, odd step: 13.7k MSUPS)
                 const uint32_t b0 = b & ~31u;
@@ -2340,6 +2355,7 @@ class Engine {
                 // default: warp-autonomous pipeline, cp.async gathers one tile
                 // ahead (C3 developed, odd step: 14.2k MSUPS; C2 14.9k vs 13.6k)
                 // with the dynamic warp-tile order (C3 odd step 14.2k vs 13.9k; 81: fixed order)
+                // and the table one delta per register (15.4k vs 14.1k packed, 94)
                 launch_aa_odd_w<4, 3>(wk, s, b, e, v != 81);
             } else lbm_aa_odd<false, false, 128, 4><<<nb, 128, 0, s>>>(F, tab, wk.P, b, e, omega, ia, h);
         }

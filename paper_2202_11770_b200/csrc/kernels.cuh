@@ -1545,7 +1545,7 @@ struct AaOddW {
     static constexpr uint32_t kBytes = 2 * kWarps * kStage;
 };
 
-template <int kWarps, int kMinBlocks>
+template <int kWarps, int kMinBlocks, int kOpt = 1>
 __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
 lbm_aa_odd_w(double* __restrict__ F, const int16_t* __restrict__ dtab, const uint32_t* __restrict__ gbase,
              const uint32_t* __restrict__ tab, uint64_t P, uint64_t PG, uint32_t begin, uint32_t end, double omega,
@@ -1562,43 +1562,80 @@ lbm_aa_odd_w(double* __restrict__ F, const int16_t* __restrict__ dtab, const uin
     // warp-tile sequence: the fixed stride w0 + k * nw, or (counter) batches
     // of 4 consecutive tiles taken from a global counter (dynamic order: the
     // tiles in flight stay near the frontier however the warps drift apart)
-    constexpr uint32_t kBatch = 4;
+    // (kOpt & 2: lane 0 requests the next batch as soon as it starts one, so
+    // the atomic's round trip is off the critical path; the last batch
+    // requested lies past the end like the one that stops the warp)
+    constexpr uint32_t kBatch = (kOpt & 4) ? 8 : 4;
+    constexpr bool kAtomAhead = (kOpt & 2) != 0, kRaw = (kOpt & 1) != 0;
     uint32_t bb0 = 0, bb1 = 0, bi0 = 0xffffffffu, bi1 = 0xffffffffu;
+    uint32_t ahead = 0;
+    bool have_ahead = false;
+    auto grab = [&]() -> uint32_t {
+        uint32_t v = 0;
+        if (lane == 0) v = atomicAdd(counter, kBatch);
+        return v;
+    };
     auto tile_at = [&](uint32_t k) -> uint32_t {
         if (!counter) return w0 + k * nw;
         const uint32_t bi = k / kBatch;
         const bool odd = bi & 1u;
         if ((odd ? bi1 : bi0) != bi) {
-            uint32_t v = 0;
-            if (lane == 0) v = atomicAdd(counter, kBatch);
-            v = __shfl_sync(0xffffffffu, v, 0);
+            uint32_t v;
+            if constexpr (kAtomAhead) {
+                if (!have_ahead) ahead = grab();
+                v = __shfl_sync(0xffffffffu, ahead, 0);
+                ahead = grab();
+                have_ahead = true;
+            } else {
+                v = __shfl_sync(0xffffffffu, grab(), 0);
+            }
             if (odd) bb1 = v, bi1 = bi;
             else bb0 = v, bi0 = bi;
         }
         return (odd ? bb1 : bb0) + k % kBatch;
     };
     // compressed table of warp-tile k into registers: the 18 int16 deltas
-    // packed two per register, and this lane's group base
-    constexpr int kD2 = (kQ - 1) / 2;
+    // (kOpt & 1: one per register, loaded by predicated loads that nothing
+    // consumes before the next iteration; else packed two per register — the
+    // packing waits for the loads, a full memory latency per tile) and this
+    // lane's group base
+    constexpr int kD2 = kRaw ? kQ - 1 : (kQ - 1) / 2;
     uint32_t dA[kD2], dB[kD2];
     uint32_t bA = 0, bB = 0;
     auto load_table = [&](uint32_t k, uint32_t* d, uint32_t& b) {
         const uint32_t tile = tile_at(k);
         const uint32_t s = base + tile * 32 + lane;
         const bool live = tile < ntiles && s >= begin && s < end;
+        if constexpr (kRaw) {
 #pragma unroll
-        for (int i = 0; i < kD2; ++i) {
-            const uint32_t lo = live ? uint16_t(__ldg(dtab + uint64_t(2 * i) * P + s)) : uint16_t(kDeltaBounce);
-            const uint32_t hi = live ? uint16_t(__ldg(dtab + uint64_t(2 * i + 1) * P + s)) : uint16_t(kDeltaBounce);
-            d[i] = lo | (hi << 16);
+            for (int i = 0; i < kD2; ++i) {
+                uint32_t v = uint32_t(int(kDeltaBounce));
+                asm("{\n .reg .pred p;\n setp.ne.u32 p, %1, 0;\n @p ld.global.nc.s16 %0, [%2];\n}"
+                    : "+r"(v)
+                    : "r"(uint32_t(live)), "l"(dtab + uint64_t(i) * P + s));
+                d[i] = v;
+            }
+            uint32_t g = 0;
+            asm("{\n .reg .pred p;\n setp.ne.u32 p, %1, 0;\n @p ld.global.nc.u32 %0, [%2];\n}"
+                : "+r"(g)
+                : "r"(uint32_t(lane < kQ - 1 && tile < ntiles)), "l"(gbase + uint64_t(lane) * PG + (s >> 5)));
+            b = g;
+        } else {
+#pragma unroll
+            for (int i = 0; i < kD2; ++i) {
+                const uint32_t lo = live ? uint16_t(__ldg(dtab + uint64_t(2 * i) * P + s)) : uint16_t(kDeltaBounce);
+                const uint32_t hi = live ? uint16_t(__ldg(dtab + uint64_t(2 * i + 1) * P + s)) : uint16_t(kDeltaBounce);
+                d[i] = lo | (hi << 16);
+            }
+            b = (lane < kQ - 1 && tile < ntiles) ? __ldg(gbase + uint64_t(lane) * PG + (s >> 5)) : 0u;
         }
-        b = (lane < kQ - 1 && tile < ntiles) ? __ldg(gbase + uint64_t(lane) * PG + (s >> 5)) : 0u;
     };
     // location of direction j of site s: signed offset from plane j's base
     // (a bounce-back lives in the inverse plane at s: s +- P)
     auto loc = [&](const uint32_t* d, uint32_t b, int j, uint32_t s, bool live) -> int32_t {
         const uint32_t bj = __shfl_sync(0xffffffffu, b, j - 1);
-        const int dj = (j & 1) ? int(int16_t(d[(j - 1) / 2] & 0xffffu)) : int(int16_t(d[(j - 1) / 2] >> 16));
+        const int dj = kRaw ? int(d[j - 1])
+                            : (j & 1) ? int(int16_t(d[(j - 1) / 2] & 0xffffu)) : int(int16_t(d[(j - 1) / 2] >> 16));
         uint32_t t = bj + lane + uint32_t(dj);
         const uint32_t esc = (dj == kDeltaEscape) && live;
         asm("{\n .reg .pred p;\n setp.ne.u32 p, %1, 0;\n @p ld.global.nc.u32 %0, [%2];\n}"

@@ -129,7 +129,7 @@ def test_aa_single_buffer_bit_exact(product, golden, key):
     assert cases.run_digest(res) == golden["runs"][key]
 
 
-@pytest.mark.parametrize("variant", ["0", "60", "61", "62", "63", "64", "65", "66", "72", "79", "81", "88", "89", "90", "91"])
+@pytest.mark.parametrize("variant", ["0", "60", "61", "62", "63", "64", "65", "66", "72", "79", "81", "88", "89", "90", "91", "92", "93", "94", "95", "96"])
 def test_aa_odd_kernel_variants(product, golden, variant, monkeypatch):
     """Odd-step kernels: the default warp-autonomous cp.async pipeline, its
     128-register shape (72), the round-1 register gather over the compressed
