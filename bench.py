@@ -10,8 +10,9 @@ quoted on), pressure iolets, strong scaling (the same total work at every N,
 so the driver's per-N values give the strong-scaling efficiency directly).
 N>1: torchrun, one process per GPU, slab decomposition, fused NVLink P2P halo.
 Storage: the AA single buffer by default (same bits as the reference's
-two-buffer push, half the HBM, faster: DESIGN §6b); `--storage two` runs the
-two-buffer push kernels.
+two-buffer push, half the HBM, faster on the vessel trees: DESIGN §6b); the
+dense C4 channel defaults to the two-buffer push kernels (`--storage two`),
+which are faster there.
 At N=1 the line also carries `secondary`: config C2 — build_pipe(48, 1400)
 (10,130,400 sites), 60-bpm pulsatile velocity inlet (proj/configs/
 pipe_beat.cfg), outlet p=1/3, tau 0.8, dt 5e-4 s — kernel-only value and
@@ -333,10 +334,11 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-secondary", action="store_true", help="N=1: skip the C2 kernel-only line")
     ap.add_argument("--quick", action="store_true", help="kernel-only number (tuning runs)")
-    ap.add_argument("--storage", default="aa", choices=["two", "aa"],
-                    help="one buffer updated in place (AA pattern; the default: the same bits in half the "
-                         "memory, and faster on C3 at N = 1 / 2 / 4, DESIGN §6b) or two buffers (the "
-                         "reference's f_old / f_new push)")
+    ap.add_argument("--storage", default=None, choices=["two", "aa"],
+                    help="one buffer updated in place (AA pattern: the same bits in half the memory; the "
+                         "default for the vessel trees C1-C3/C5, faster there at N = 1 / 2 / 4, DESIGN §6b) "
+                         "or two buffers (the reference's f_old / f_new push; the default for the dense C4 "
+                         "channel)")
     ap.add_argument("--scheme", default="push", choices=["push", "pull"],
                     help="push (fused collide + scatter) or the reference's pull gather (update_pull)")
     ap.add_argument("--halo", default="p2p", choices=["nccl", "p2p"],
@@ -386,6 +388,11 @@ def main():
     slab_src = world > 1 and args.geometry == "source"
     d, bcs, p, desc = workload(P, name, args.scale, source=slab_src, world=world)
     halo_mode = 1 if args.halo == "p2p" else 0
+    if args.storage is None:
+        # per workload, as measured: the AA pair is faster on the
+        # vessel trees (C3 at N = 1/2/4, C5), the two-buffer push on the dense
+        # C4 channel (18,787 vs 18,217 at N=1, 75,059 vs 71,659 at N=4)
+        args.storage = "two" if name in ("c4", "c4w") else "aa"
     storage = 1 if args.storage == "aa" else 0
     scheme = P.PULL if args.scheme == "pull" else P.PUSH
     sim = make_sim(P.EngineParams(workers=world, devices=[local], halo_mode=halo_mode, storage=storage, scheme=scheme,
