@@ -335,6 +335,7 @@ struct WorkerDev {
     cudaEvent_t evSend = nullptr, evMid = nullptr, evEnd = nullptr;
     // run() bracket + host-copy completion, one set per run in flight (Engine::run_par)
     cudaEvent_t evRun0[2] = {}, evRun1[2] = {}, evDone[2] = {};
+    cudaEvent_t evObsFree[2] = {};  // a run's observation rows gathered (N=1 series on sE)
     PinnedMem h_obs;                                                   // observation rows, D2H target
     uint32_t n = 0, n_edge = 0, ep = 0, mp = 0;  // ranges: [0,ep) [ep,n_edge) [n_edge,n_edge+mp) [.., n)
     uint64_t P = 0;
@@ -813,6 +814,7 @@ class Engine {
                 if (wp->evRun0[b]) cudaEventDestroy(wp->evRun0[b]);
                 if (wp->evRun1[b]) cudaEventDestroy(wp->evRun1[b]);
                 if (wp->evDone[b]) cudaEventDestroy(wp->evDone[b]);
+                if (wp->evObsFree[b]) cudaEventDestroy(wp->evObsFree[b]);
             }
             if (wp->sE) cudaStreamDestroy(wp->sE);
             if (wp->sM) cudaStreamDestroy(wp->sM);
@@ -878,6 +880,7 @@ class Engine {
             CK(cudaEventCreate(&wk.evRun0[b]));
             CK(cudaEventCreate(&wk.evRun1[b]));
             CK(cudaEventCreateWithFlags(&wk.evDone[b], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&wk.evObsFree[b], cudaEventDisableTiming));
         }
         cudaStream_t s = wk.sM;
 
@@ -1256,9 +1259,14 @@ class Engine {
     // run()'s series: gather this run's rows into series order, reduce the
     // short iolets on the device, and copy results + the long iolets' entries
     // to pinned host memory, on stream s (behind the step loop).
-    void reduce_series_async(WorkerDev& wk, cudaStream_t s, const double* src, uint64_t per, int buf) {
+    // `gathered` (optional) is recorded once the rows at src have been read.
+    void reduce_series_async(WorkerDev& wk, cudaStream_t s, const double* src, uint64_t per, int buf,
+                             cudaEvent_t gathered = nullptr) {
         const uint32_t rows = uint32_t(wk.obs_rows), n_io = uint32_t(dom.iolets.size());
-        if (!rows || !n_io) return;
+        if (!rows || !n_io) {
+            if (gathered) CK(cudaEventRecord(gathered, s));
+            return;
+        }
         const uint64_t ne = std::max<uint32_t>(n_series_ent, 1);
         double* g = ser_buf.reserve<double>(3 * uint64_t(rows) * ne);
         double* o = ser_out.reserve<double>(3 * uint64_t(rows) * n_io);
@@ -1269,6 +1277,7 @@ class Engine {
                                                                        n_series_ent, rows, g);
             ++launches;
         }
+        if (gathered) CK(cudaEventRecord(gathered, s));
         if (!ser_dev_k.empty()) {
             const uint64_t warps = uint64_t(ser_dev_k.size()) * rows;
             series_chain<<<unsigned(warps), 32, 0, s>>>(g, ser_kdev.get<uint32_t>(), ser_off.get<uint32_t>(),
@@ -1943,6 +1952,7 @@ class Engine {
     uint64_t max_run_n = 0;  // the longest run so far (buffer sizes follow it)
     const bool sync_runs = std::getenv("SPLBCU_SYNC_RUN") != nullptr;  // A/B knob: every run completes before returning
     const bool wait_series_off = std::getenv("SPLBCU_NO_SERIES_FIRST") != nullptr;  // A/B knob for the ordering below
+    const bool series_on_main = std::getenv("SPLBCU_SERIES_ON_MAIN") != nullptr;  // A/B knob: N=1 series behind the steps
     int run_par = 0;                                     // event / staging set of the run being enqueued
     PinnedMem h_staged2[2];                              // per-run iolet values, one per run in flight
     std::chrono::steady_clock::time_point last_done{};  // host clock at the last completion
@@ -1997,6 +2007,9 @@ class Engine {
             // lands after it and delays this run's edge kernels behind it.
             if (pend.active && dist && prm.observe_iolets && !wait_series_off)
                 CK(cudaStreamWaitEvent(wp->sM, wp->evDone[pend.par], 0));
+            // one worker: this run's observations overwrite obs_buf once the
+            // previous run's rows are gathered
+            if (pend.active && !dist && pend.series) CK(cudaStreamWaitEvent(wp->sM, wp->evObsFree[pend.par], 0));
             double* d = wp->staged.reserve<double>(n_staged);
             CK(cudaMemcpyAsync(d, staged, n_staged * sizeof(double), cudaMemcpyHostToDevice, wp->sM));
             wp->tev_used[par] = 0;
@@ -2045,8 +2058,13 @@ class Engine {
                 continue;
             }
             if (series) {
-                reduce_series_async(wk, wk.sM, wk.obs_buf.get<double>(), 0, ser_next);
-                CK(cudaEventRecord(wk.evDone[par], wk.sM));
+                // one worker: the reduction and its copies run on the idle
+                // edge stream beside the next run's steps, which wait only
+                // for the rows to be gathered out of obs_buf (evObsFree)
+                cudaStream_t ss = series_on_main ? wk.sM : wk.sE;
+                if (!series_on_main) CK(cudaStreamWaitEvent(wk.sE, wk.evRun1[par], 0));
+                reduce_series_async(wk, ss, wk.obs_buf.get<double>(), 0, ser_next, wk.evObsFree[par]);
+                CK(cudaEventRecord(wk.evDone[par], ss));
                 continue;
             }
             const size_t nb = prm.observe_iolets ? 3 * wk.obs_rows * wk.n_obs : 0;
