@@ -123,9 +123,12 @@ class ClockSampler:
         self.t0 = self.t1 = None
 
     def __enter__(self):
+        self.t0 = time.perf_counter()
+        if self.gpu is None:
+            return self
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "25"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -251,9 +254,19 @@ def timed_loop(sim, n, steps, warmup, bps, barrier, max_over_ranks, gpu, name, d
     k0 = sim.kernel_stats()
     l0 = sim.launch_count()
     d0 = sim.device_loop_seconds()
-    with ClockSampler(gpu) as clk:
+    # rank 0 samples its GPU (the line it prints); one nvidia-smi per node
+    # keeps the driver queries off the other ranks' launch paths.  The
+    # sampler is up before the barrier, so every rank enters the timed steps
+    # together (a rank waiting for nvidia-smi to start would otherwise hold
+    # its neighbours' steps at the halo exchange inside their timed region).
+    clk = ClockSampler(gpu if int(os.environ.get("RANK", "0")) == 0 else None).__enter__()
+    barrier()
+    clk.t0 = time.perf_counter()
+    try:
         sim.run(steps)
         sim.device_loop_seconds()  # run() returns while its last steps execute: wait inside the sampled window
+    finally:
+        clk.__exit__(None, None, None)
     barrier()
     dev_s = max_over_ranks(sim.device_loop_seconds() - d0)
     k1 = sim.kernel_stats()

@@ -332,10 +332,12 @@ struct Seg {
 struct WorkerDev {
     int w = 0, dev = 0;
     cudaStream_t sE = nullptr, sM = nullptr;
+    cudaStream_t sS = nullptr;  // dist mode: the series reduction beside the next run
     cudaEvent_t evSend = nullptr, evMid = nullptr, evEnd = nullptr;
     // run() bracket + host-copy completion, one set per run in flight (Engine::run_par)
     cudaEvent_t evRun0[2] = {}, evRun1[2] = {}, evDone[2] = {};
-    cudaEvent_t evObsFree[2] = {};  // a run's observation rows gathered (N=1 series on sE)
+    cudaEvent_t evObsFree[2] = {};  // a run's observation rows gathered (N=1) / all-gathered (dist)
+    cudaEvent_t evSerRead[2] = {};  // dist: the series gather has read the all-gathered rows
     PinnedMem h_obs;                                                   // observation rows, D2H target
     uint32_t n = 0, n_edge = 0, ep = 0, mp = 0;  // ranges: [0,ep) [ep,n_edge) [n_edge,n_edge+mp) [.., n)
     uint64_t P = 0;
@@ -815,8 +817,10 @@ class Engine {
                 if (wp->evRun1[b]) cudaEventDestroy(wp->evRun1[b]);
                 if (wp->evDone[b]) cudaEventDestroy(wp->evDone[b]);
                 if (wp->evObsFree[b]) cudaEventDestroy(wp->evObsFree[b]);
+                if (wp->evSerRead[b]) cudaEventDestroy(wp->evSerRead[b]);
             }
             if (wp->sE) cudaStreamDestroy(wp->sE);
+            if (wp->sS) cudaStreamDestroy(wp->sS);
             if (wp->sM) cudaStreamDestroy(wp->sM);
         }
     }
@@ -873,6 +877,7 @@ class Engine {
         CK(cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri));
         CK(cudaStreamCreateWithPriority(&wk.sE, cudaStreamNonBlocking, hi_pri));
         CK(cudaStreamCreateWithPriority(&wk.sM, cudaStreamNonBlocking, lo_pri));
+        CK(cudaStreamCreateWithPriority(&wk.sS, cudaStreamNonBlocking, lo_pri));
         CK(cudaEventCreateWithFlags(&wk.evSend, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&wk.evMid, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&wk.evEnd, cudaEventDisableTiming));
@@ -881,6 +886,7 @@ class Engine {
             CK(cudaEventCreate(&wk.evRun1[b]));
             CK(cudaEventCreateWithFlags(&wk.evDone[b], cudaEventDisableTiming));
             CK(cudaEventCreateWithFlags(&wk.evObsFree[b], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&wk.evSerRead[b], cudaEventDisableTiming));
         }
         cudaStream_t s = wk.sM;
 
@@ -1953,6 +1959,7 @@ class Engine {
     const bool sync_runs = std::getenv("SPLBCU_SYNC_RUN") != nullptr;  // A/B knob: every run completes before returning
     const bool wait_series_off = std::getenv("SPLBCU_NO_SERIES_FIRST") != nullptr;  // A/B knob for the ordering below
     const bool series_on_main = std::getenv("SPLBCU_SERIES_ON_MAIN") != nullptr;  // A/B knob: N=1 series behind the steps
+    const bool series_side_off = std::getenv("SPLBCU_SERIES_SIDE_OFF") != nullptr;  // A/B knob: dist series before the next run
     int run_par = 0;                                     // event / staging set of the run being enqueued
     PinnedMem h_staged2[2];                              // per-run iolet values, one per run in flight
     std::chrono::steady_clock::time_point last_done{};  // host clock at the last completion
@@ -2006,7 +2013,8 @@ class Engine {
             // bulk kernel can take every SM before the NCCL kernel, which then
             // lands after it and delays this run's edge kernels behind it.
             if (pend.active && dist && prm.observe_iolets && !wait_series_off)
-                CK(cudaStreamWaitEvent(wp->sM, wp->evDone[pend.par], 0));
+                CK(cudaStreamWaitEvent(wp->sM, (pend.series && !series_side_off) ? wp->evObsFree[pend.par]
+                                                                                 : wp->evDone[pend.par], 0));
             // one worker: this run's observations overwrite obs_buf once the
             // previous run's rows are gathered
             if (pend.active && !dist && pend.series) CK(cudaStreamWaitEvent(wp->sM, wp->evObsFree[pend.par], 0));
@@ -2046,8 +2054,21 @@ class Engine {
             if (prm.observe_iolets && dist) {
                 const uint64_t per = obs_gather_per(wk);
                 CK(cudaStreamWaitEvent(wk.sE, wk.evRun1[par], 0));
+                const bool side = dev_series && !series_side_off;
+                // the previous run's series gather has read the all-gathered rows
+                if (side && pend.active && pend.series) CK(cudaStreamWaitEvent(wk.sE, wk.evSerRead[pend.par], 0));
                 double* dr = obs_gather.reserve<double>(per * uint64_t(nranks));
                 NK(nccl().AllGather(wk.obs_buf.get<double>(), dr, per, ncclDouble, comm, wk.sE));
+                if (side) {
+                    // the next run's steps wait for the all-gather only (it must
+                    // not queue behind their persistent bulk kernel); the series
+                    // kernels and copies run beside them on sS
+                    CK(cudaEventRecord(wk.evObsFree[par], wk.sE));
+                    CK(cudaStreamWaitEvent(wk.sS, wk.evObsFree[par], 0));
+                    reduce_series_async(wk, wk.sS, dr, per, ser_next, wk.evSerRead[par]);
+                    CK(cudaEventRecord(wk.evDone[par], wk.sS));
+                    continue;
+                }
                 if (dev_series) {
                     reduce_series_async(wk, wk.sE, dr, per, ser_next);
                 } else {
