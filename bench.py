@@ -470,12 +470,19 @@ def main():
         sim.run(1)
     barrier()
     e2e_steps = max(50, min(args.steps, 200))  # a window long enough that the final series() read is not a fixed cost
+    dd0 = sim.device_loop_seconds()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         sim.run(1)
+    t_ser = time.perf_counter()
     ser = sim.series()  # completes the last row (the host part of the reduction is lazy)
+    t_end = time.perf_counter()
     barrier()
     e2e_s = max_over_ranks(time.perf_counter() - t0)
+    # diagnostics: the same window's device time of the steps (CUDA events, as
+    # `value`) and the final series() call's share of the wall time
+    e2e_dev_s = max_over_ranks(sim.device_loop_seconds() - dd0)
+    series_call_s = max_over_ranks(t_end - t_ser)
     # the series row's device -> host bytes (reduced values + the entries of
     # the iolets the host reduces)
     d2h = sim.series_d2h_bytes()
@@ -483,7 +490,9 @@ def main():
            "h2d_bytes_per_step": 8 * len(bcs.entries), "d2h_bytes_per_step": d2h,
            "note": "Simulation.run(1) per step via the C-ABI with the iolet series on: per-step BC values "
                    "H2D, the step, the series row (all-gathered across ranks, reduced in the reference's order) "
-                   "D2H, host wall clock; " + state}
+                   "D2H, host wall clock; " + state,
+           "device_value": n * e2e_steps / e2e_dev_s / 1e6 if e2e_dev_s > 0 else None,
+           "final_series_call_ms": series_call_s * 1e3}
     sim.close()
 
     secondary = None
